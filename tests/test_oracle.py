@@ -1,0 +1,294 @@
+"""Pins for the CPU oracle (oracle/): each check ties the oracle to something other than itself —
+numpy's matmul, closed forms, SPEC/SURVEY worked examples (tests/golden), brute force over the
+densified matrix, round trips, and injected corruptions the invariant checker must catch.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hrpb_v1_examples.json")))
+
+
+def rand_csr(M, K, density, seed, exact=True):
+    rng = np.random.default_rng(seed)
+    mask = rng.random((M, K)) < density
+    rp = np.zeros(M + 1, np.int64)
+    rp[1:] = np.cumsum(mask.sum(1))
+    ci = np.nonzero(mask)[1].astype(np.int32)
+    if exact:
+        v = rng.choice(np.array([-2, -1, 1, 2], np.float32), size=ci.shape[0])
+    else:
+        v = (rng.random(ci.shape[0]) * 2 - 1).astype(np.float32)
+    return rp, ci, v.astype(np.float32)
+
+
+def to_csr(M, entries):
+    entries = sorted(entries)
+    rp = np.zeros(M + 1, np.int64)
+    for r, _, _ in entries:
+        rp[r + 1] += 1
+    rp = np.cumsum(rp)
+    ci = np.array([c for _, c, _ in entries], np.int32)
+    v = np.array([x for _, _, x in entries], np.float32)
+    return rp, ci, v
+
+
+# ----------------------------------------------------------------------------- O1
+def test_csr_validate_codes():
+    rp, ci, v = to_csr(3, [(0, 1, 1.0), (0, 3, 1.0), (2, 0, 1.0)])
+    assert oracle.csr_validate(3, 4, rp, ci) == 0
+    assert oracle.csr_validate(3, 3, rp, ci) == 4               # column out of range
+    bad = ci.copy(); bad[1] = 1
+    assert oracle.csr_validate(3, 4, rp, bad) == 5              # duplicate in a row
+    bad = ci.copy(); bad[0], bad[1] = 3, 1
+    assert oracle.csr_validate(3, 4, rp, bad) == 5              # unsorted
+    rpb = rp.copy(); rpb[1] = 3; rpb[2] = 1
+    assert oracle.csr_validate(3, 4, rpb, ci) == 2              # non-monotone row_ptr
+
+
+# ----------------------------------------------------------------------------- O2 / O3
+@pytest.mark.parametrize("seed", range(6))
+def test_csr_spmm_matches_numpy_exact(seed):
+    rng = np.random.default_rng(100 + seed)
+    M, K, N = rng.integers(1, 70, 3)
+    rp, ci, v = rand_csr(M, K, rng.random() * 0.5, seed)
+    B = rng.integers(-2, 3, (K, N)).astype(np.float32)
+    C, S = oracle.csr_spmm(M, K, rp, ci, v, B, with_bound=True)
+    A = oracle.densify(M, K, rp, ci, v)
+    assert np.array_equal(C, A @ B.astype(np.float64))            # library matmul, exact on integers
+    assert np.array_equal(S, np.abs(A) @ np.abs(B.astype(np.float64)))
+    assert np.array_equal(oracle.dense_gemm(A, B), A @ B.astype(np.float64))  # O3 pinned to numpy too
+
+
+def test_csr_spmm_special_cases():
+    rng = np.random.default_rng(5)
+    K, N = 37, 9
+    B = rng.random((K, N)).astype(np.float32)
+    rp = np.arange(K + 1, dtype=np.int64)
+    ci = np.arange(K, dtype=np.int32)
+    C = oracle.csr_spmm(K, K, rp, ci, np.ones(K, np.float32), B)
+    assert np.array_equal(C, B.astype(np.float64))                # identity -> C = B
+    perm = rng.permutation(K).astype(np.int32)
+    C = oracle.csr_spmm(K, K, rp, perm, np.ones(K, np.float32), B)
+    assert np.array_equal(C, B[perm].astype(np.float64))          # permutation -> permuted rows
+    rp0 = np.zeros(K + 1, np.int64)
+    C = oracle.csr_spmm(K, K, rp0, np.zeros(0, np.int32), np.zeros(0, np.float32), B)
+    assert not C.any()                                            # empty -> 0
+
+
+def test_csr_spmm_rows_subset_and_f32out():
+    rng = np.random.default_rng(9)
+    M, K, N = 50, 40, 7
+    rp, ci, v = rand_csr(M, K, 0.2, 3, exact=False)
+    B = rng.random((K, N)).astype(np.float32)
+    full = oracle.csr_spmm(M, K, rp, ci, v, B)
+    rows = np.array([49, 0, 17], np.int64)
+    assert np.array_equal(oracle.csr_spmm(M, K, rp, ci, v, B, rows=rows), full[rows])
+    c32, th = oracle.csr_spmm_f32out(M, rp, ci, v, B)
+    assert th >= 1 and np.array_equal(c32, full.astype(np.float32))
+
+
+# ----------------------------------------------------------------------------- O4 golden examples
+def _gold_csr(case):
+    M, K = case["M"], case["K"]
+    if "rows" in case:
+        return (M, K) + to_csr(M, [tuple(x) for x in case["rows"]])
+    if "dense_value" in case:
+        ents = [(r, c, float(1 + 16 * r + c)) for r in range(M) for c in range(K)]
+        return (M, K) + to_csr(M, ents)
+    ents = [(i, i, 1.0) for i in range(M)]
+    return (M, K) + to_csr(M, ents)
+
+
+@pytest.mark.parametrize("name", ["spec_16x20", "spec_dense16", "identity32"])
+def test_convert_golden(name):
+    case = GOLD[name]
+    M, K, rp, ci, v = _gold_csr(case)
+    h = oracle.csr_to_hrpb(M, K, rp, ci, v)
+    assert h.blockedRowPtr.tolist() == case["blockedRowPtr"]
+    assert h.activeCols.tolist() == case["activeCols"]
+    assert h.sizePtr.tolist() == case["sizePtr"]
+    assert h.packedBlocks.tobytes().hex() == case["packed_hex"]
+    assert oracle.hrpb_check(h, ci.shape[0]) == (0, "")
+
+
+def test_pattern_bit_order_matches_spec_examples():
+    # encode({0,5,63}) = 0x8000000000000021: a single brick whose row-major positions
+    # {0,5,63} = (r0,c0), (r1,c1), (r15,c3) hold entries; prefix_index examples.
+    # (column 2 needs an entry too, else compaction moves column 3 left: entry (14,2) = bit 58)
+    ents = [(0, 0, 1.0), (1, 1, 2.0), (14, 2, 4.0), (15, 3, 3.0)]
+    rp, ci, v = to_csr(16, ents)
+    h = oracle.csr_to_hrpb(16, 4, rp, ci, v)
+    pat = int(np.frombuffer(h.packedBlocks[8:16].tobytes(), "<u8")[0])
+    assert pat & ~(1 << 58) == int(GOLD["encode_example"]["pattern"], 16) and pat >> 58 & 1
+    # the oracle stores values in ascending-bit order, so value index == prefix_index(pattern, bit)
+    vals = np.frombuffer(h.packedBlocks[16:32].tobytes(), "<f4")
+    assert vals.tolist() == [1.0, 2.0, 4.0, 3.0]
+    for p_hex, pos, want in GOLD["prefix_example"]["cases"]:
+        assert bin(int(p_hex, 16) & ((1 << pos) - 1)).count("1") == want
+
+
+def test_convert_empty_and_ragged():
+    h = oracle.csr_to_hrpb(40, 30, np.zeros(41, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32))
+    assert h.blockedRowPtr.tolist() == [0, 0, 0, 0] and h.num_blocks == 0
+    rp, ci, v = to_csr(37, [(36, 5, 2.0), (36, 29, -1.0), (0, 0, 1.0)])
+    h = oracle.csr_to_hrpb(37, 30, rp, ci, v)
+    assert h.blockedRowPtr.tolist() == [0, 1, 1, 2]                            # ceil(37/16) panels (R9)
+    assert oracle.hrpb_check(h, 3)[0] == 0
+
+
+# ----------------------------------------------------------------------------- O4 brute force
+def brute_hrpb(M, K, rp, ci, v, tm=16, tk=16):
+    """Independent tiny-input derivation from the dense matrix (numpy)."""
+    A = oracle.densify(M, K, rp, ci, v)
+    S = np.zeros((M, K), bool)
+    for i in range(M):
+        S[i, ci[rp[i]:rp[i + 1]]] = True
+    P = (M + tm - 1) // tm
+    brp, ac, blocks = [0], [], []
+    for p in range(P):
+        Sp = np.zeros((tm, K), bool); Ap = np.zeros((tm, K))
+        rows = min(tm, M - p * tm)
+        Sp[:rows] = S[p * tm:p * tm + rows]; Ap[:rows] = A[p * tm:p * tm + rows]
+        act = np.nonzero(Sp.any(0))[0]
+        nblk = -(-len(act) // tk)
+        for j in range(nblk):
+            cols = act[j * tk:(j + 1) * tk]
+            ac += cols.tolist() + [K] * (tk - len(cols))
+            Sb = np.zeros((tm, tk), bool); Ab = np.zeros((tm, tk))
+            Sb[:, :len(cols)] = Sp[:, cols]; Ab[:, :len(cols)] = Ap[:, cols]
+            bricks = []
+            for bc in range(tk // 4):
+                for br in range(tm // 16):
+                    tile = Sb[16 * br:16 * br + 16, 4 * bc:4 * bc + 4].reshape(-1)
+                    pat = sum(1 << int(i) for i in np.nonzero(tile)[0])
+                    if pat:
+                        vals = Ab[16 * br:16 * br + 16, 4 * bc:4 * bc + 4].reshape(-1)[tile]
+                        bricks.append((bc, br, pat, vals))
+            blocks.append(bricks)
+        brp.append(brp[-1] + nblk)
+    return brp, ac, blocks
+
+
+def parse_blocks(h, tk=16):
+    out = []
+    nbc = tk // 4
+    for b in range(h.num_blocks):
+        blk = h.packedBlocks[int(h.sizePtr[b]):int(h.sizePtr[b + 1])].tobytes()
+        colptr = list(blk[:nbc + 1]); nbr = colptr[-1]
+        rows = list(blk[nbc + 1:nbc + 1 + nbr])
+        hdr = -(-(nbc + 1 + nbr) // 8) * 8
+        pats = np.frombuffer(blk[hdr:hdr + 8 * nbr], "<u8")
+        nz = int(sum(bin(int(p)).count("1") for p in pats))
+        vals = np.frombuffer(blk[hdr + 8 * nbr:hdr + 8 * nbr + 4 * nz], "<f4")
+        bricks, off = [], 0
+        for bc in range(nbc):
+            for k in range(colptr[bc], colptr[bc + 1]):
+                c = bin(int(pats[k])).count("1")
+                bricks.append((bc, rows[k], int(pats[k]), vals[off:off + c].astype(np.float64)))
+                off += c
+        out.append(bricks)
+    return out
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_convert_vs_bruteforce(seed):
+    rng = np.random.default_rng(seed)
+    M, K = int(rng.integers(1, 70)), int(rng.integers(1, 90))
+    tm, tk = [(16, 16), (32, 16), (16, 32), (64, 16)][seed % 4]
+    rp, ci, v = rand_csr(M, K, float(rng.choice([0.02, 0.1, 0.4, 0.9])), seed, exact=False)
+    h = oracle.csr_to_hrpb(M, K, rp, ci, v, tm=tm, tk=tk)
+    brp, ac, blocks = brute_hrpb(M, K, rp, ci, v, tm, tk)
+    assert h.blockedRowPtr.tolist() == brp
+    assert h.activeCols.tolist() == ac
+    got = parse_blocks(h, tk)
+    assert len(got) == len(blocks)
+    for g, w in zip(got, blocks):
+        assert [(a, b, c) for a, b, c, _ in g] == [(a, b, c) for a, b, c, _ in w]
+        for (_, _, _, gv), (_, _, _, wv) in zip(g, w):
+            assert np.array_equal(gv, wv)
+    assert oracle.hrpb_check(h, ci.shape[0])[0] == 0
+
+
+def test_convert_panel_range_equals_full_slice():
+    w = synth.make("c5", scale=4)
+    full = oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    p0, p1 = 7, 19
+    part = oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals, p0=p0, p1=p1)
+    b0, b1 = int(full.blockedRowPtr[p0]), int(full.blockedRowPtr[p1])
+    assert np.array_equal(part.blockedRowPtr, full.blockedRowPtr[p0:p1 + 1] - b0)
+    assert np.array_equal(part.activeCols, full.activeCols[b0 * 16:b1 * 16])
+    s0, s1 = int(full.sizePtr[b0]), int(full.sizePtr[b1])
+    assert np.array_equal(part.sizePtr, full.sizePtr[b0:b1 + 1] - s0)
+    assert part.packedBlocks.tobytes() == full.packedBlocks[s0:s1].tobytes()
+
+
+# ----------------------------------------------------------------------------- O5 / O6 / O7
+@pytest.mark.parametrize("seed", range(20))
+def test_round_trip(seed):
+    rng = np.random.default_rng(1000 + seed)
+    M, K = int(rng.integers(16, 300)), int(rng.integers(16, 300))
+    dens = float(10 ** rng.uniform(-3, np.log10(0.3)))
+    rp, ci, v = rand_csr(M, K, dens, seed, exact=False)
+    h = oracle.csr_to_hrpb(M, K, rp, ci, v)
+    rp2, ci2, v2 = oracle.hrpb_to_csr(h, ci.shape[0] + 1)
+    assert np.array_equal(rp, rp2) and np.array_equal(ci, ci2) and np.array_equal(v, v2)
+    code, msg = oracle.hrpb_check(h, ci.shape[0])
+    assert code == 0, msg
+
+
+def test_round_trip_keeps_explicit_zeros():
+    rp, ci, v = to_csr(20, [(3, 4, 0.0), (3, 9, 1.5), (19, 0, 0.0)])
+    h = oracle.csr_to_hrpb(20, 12, rp, ci, v)
+    rp2, ci2, v2 = oracle.hrpb_to_csr(h, 10)
+    assert ci2.tolist() == ci.tolist() and oracle.hrpb_check(h, 3)[0] == 0   # R11: structural
+
+
+def _corrupt_cases(h):
+    def mod(fn):
+        import copy
+        g = copy.deepcopy(h)
+        fn(g)
+        return g
+    hdr = 8  # nbr <= 3 for the fixture below -> header 8 bytes
+    yield "flip a pattern bit", mod(lambda g: g.packedBlocks.__setitem__(hdr, g.packedBlocks[hdr] ^ 0x40))
+    yield "zero pattern", mod(lambda g: g.packedBlocks.__setitem__(slice(hdr, hdr + 8), 0))
+    yield "swap activeCols", mod(lambda g: g.activeCols.__setitem__(slice(0, 2), g.activeCols[[1, 0]]))
+    yield "blockedRowPtr", mod(lambda g: g.blockedRowPtr.__setitem__(1, g.blockedRowPtr[2] + 1))
+    yield "pad byte", mod(lambda g: g.packedBlocks.__setitem__(7, 7))
+    yield "colPtr", mod(lambda g: g.packedBlocks.__setitem__(1, 3))
+
+
+def test_checker_catches_corruption():
+    rp, ci, v = to_csr(40, [(0, 1, 1.0), (1, 2, 2.0), (3, 3, 3.0), (5, 9, 1.0), (17, 2, 4.0), (33, 7, 1.0)])
+    h = oracle.csr_to_hrpb(40, 12, rp, ci, v)
+    assert oracle.hrpb_check(h, 6)[0] == 0
+    for what, g in _corrupt_cases(h):
+        assert oracle.hrpb_check(g, 6)[0] != 0, what
+    assert oracle.hrpb_check(h, 7)[0] != 0          # conservation: sum popcount = nnz
+
+
+def test_popcount_floor_tm16():
+    # with TM = brick_m each real column of a brick has >= 1 nnz -> popcount >= 4
+    w = synth.make("c2a", scale=8)
+    h = oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    ok = 0
+    for bricks, b in zip(parse_blocks(h), range(h.num_blocks)):
+        for bc, _, pat, _ in bricks:
+            if all(h.activeCols[b * 16 + 4 * bc + j] != w.K for j in range(4)):
+                assert bin(pat).count("1") >= 4
+                ok += 1
+    assert ok > 0
+
+
+@pytest.mark.parametrize("tm", [16, 32])
+def test_emulator_equals_csr_exact(tm):
+    w = synth.make("c1", scale=3, N=24)
+    B = w.B()
+    h = oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm)
+    assert np.array_equal(oracle.hrpb_spmm(h, B), oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B))
