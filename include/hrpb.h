@@ -1,0 +1,128 @@
+/*
+ * hrpb.h — C ABI of libhrpb: B200-native (sm_100a) HRPB construction and SpMM.
+ *
+ * Method: cuTeSpMM / HRPB, arxiv 2504.06443 (cited as P:Lnnn = /root/reference/PAPER.md line).
+ *   Problem statement (§Notations): C = A.B with A sparse M x K, B dense K x N, C dense M x N.
+ *   HRPB (Figs. "Block Data Structure" P:L43-48 and "HRPB data structure" P:L59-64):
+ *   rows are grouped into TM-row panels; each panel's active columns are compacted into
+ *   (TM, TK) blocks; a block is split into 16 x 4 bricks carrying a 64-bit non-zero pattern and
+ *   packed values in brick-CSC order.
+ *   Kernel (Alg. "cuTeSpMM kernel design"): per block, gather the TK rows of B named by
+ *   activeCols, decode bricks into zero-filled tiles and multiply them on tensor cores.
+ *
+ * All matrix pointers are DEVICE pointers except in hrpb_build_spmm_host (HOST pointers).
+ * Streams are CUDA runtime streams (cudaStream_t); NULL means the legacy default stream.
+ * No function aborts or throws; every failure is reported as an hrpb_status_t.
+ */
+#ifndef HRPB_H_
+#define HRPB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+struct CUstream_st;
+typedef struct CUstream_st* hrpb_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  HRPB_SUCCESS = 0,
+  HRPB_ERROR_INVALID_VALUE = 1,       /* null pointer, negative size, unsupported tm/tk, M or K >= 2^31 */
+  HRPB_ERROR_INVALID_CSR = 2,         /* row_ptr not monotone / row_ptr[0] != 0 / row_ptr[M] != nnz /
+                                         column out of range / columns not strictly increasing in a row */
+  HRPB_ERROR_DIMENSION_MISMATCH = 3,  /* hrpb_spmm M or K differ from the handle's */
+  HRPB_ERROR_OUT_OF_MEMORY = 4,
+  HRPB_ERROR_NOT_SUPPORTED = 5,       /* current device is not sm_100 (B200) */
+  HRPB_ERROR_CUDA = 6                 /* any other CUDA error (see hrpb_last_cuda_error) */
+} hrpb_status_t;
+
+/* Tile parameters ("TM either 16 or 32", "TK is set to 16"). The hot path is
+ * tm = 16, tk = 16. NULL config => {16, 16}. */
+typedef struct {
+  int32_t tm; /* rows per panel: 16 */
+  int32_t tk; /* compacted columns per block: 16 */
+} hrpb_config_t;
+
+typedef struct hrpb_handle* hrpb_t;
+
+/* Device view of a built HRPB (HRPB-v1 layout, reading R7). Pointers are owned by the
+ * handle and valid until hrpb_free. Block b occupies packedBlocks[sizePtr[b] .. sizePtr[b+1]):
+ *   u8 colPtr[tk/4+1] | u8 rows[nbr] | zero pad to 8 | u64 patterns[nbr] | f32 values[nz] | pad 16. */
+typedef struct {
+  int64_t M, K, nnz;
+  int64_t num_panels;   /* ceil(M / tm) */
+  int64_t num_blocks;   /* NUM_BLKS */
+  int64_t packed_bytes; /* sizePtr[num_blocks] */
+  int32_t tm, tk;
+  const uint32_t* blockedRowPtr; /* [num_panels + 1], first block of each panel */
+  const uint32_t* activeCols;    /* [num_blocks * tk], original column id; K = padding (R2) */
+  const uint64_t* sizePtr;       /* [num_blocks + 1], byte offset of each block (R8) */
+  const uint8_t* packedBlocks;   /* [packed_bytes] */
+} hrpb_view_t;
+
+/*
+ * hrpb_build — CSR -> HRPB on the GPU (steps B1..B5 of SURVEY §8(a); P:L81-149 Phase 1/2).
+ *   M, K, nnz : dimensions of A (0 allowed); M, K < 2^31.
+ *   row_ptr   : device int64 [M+1], row_ptr[0] = 0, non-decreasing, row_ptr[M] = nnz.
+ *   col_idx   : device int32 [nnz], 0 <= col < K, strictly increasing within a row.
+ *   values    : device float [nnz] (bits copied verbatim; explicit zeros are structural, R11).
+ *   cfg       : NULL or {16, 16}.
+ *   stream    : all work is enqueued on it; the call synchronizes it once at the end to read
+ *               back sizes and the validation status, so the CSR buffers may be freed on return.
+ *   out       : receives the handle (set to NULL on any error).
+ * The result is bit-identical to the CPU oracle converter for the same CSR.
+ * Errors: INVALID_VALUE, INVALID_CSR, OUT_OF_MEMORY, NOT_SUPPORTED, CUDA.
+ */
+hrpb_status_t hrpb_build(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                         const float* values, const hrpb_config_t* cfg, hrpb_stream_t stream, hrpb_t* out);
+
+/*
+ * hrpb_spmm — C = A.B (Alg. "cuTeSpMM kernel design" P:L170-231), steps S1..S5.
+ *   A : handle from hrpb_build (immutable; concurrent calls on different streams are allowed
+ *       when each call has its own C).
+ *   B : device float, row-major K x N (ld = N), finite values (R17). Must not alias C.
+ *   C : device float, row-major M x N (ld = N); fully overwritten (empty rows become 0, R13).
+ *   M, K must equal the handle's (else DIMENSION_MISMATCH); N >= 0 (N = 0 is a no-op).
+ * Arithmetic: TF32 tensor cores (A rounded to TF32 by cvt.rna, B truncated by the tensor core),
+ * FP32 accumulation in TMEM. Asynchronous on `stream`; no host synchronization.
+ */
+hrpb_status_t hrpb_spmm(const hrpb_t A, const float* B, float* C, int64_t M, int64_t K, int64_t N,
+                        hrpb_stream_t stream);
+
+/*
+ * hrpb_build_spmm_host — the whole hot path from HOST buffers (end-to-end entry point):
+ * H2D copies of the CSR and B, hrpb_build, hrpb_spmm, D2H copy of C, all on `stream`, returning
+ * after C is in host memory. Host buffers should be pinned for full PCIe bandwidth.
+ * Arguments as for hrpb_build / hrpb_spmm, with host pointers.
+ */
+hrpb_status_t hrpb_build_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr_h,
+                                   const int32_t* col_idx_h, const float* values_h, const float* B_h, float* C_h,
+                                   const hrpb_config_t* cfg, hrpb_stream_t stream);
+
+/* Releases the handle's device memory (stream-ordered on the build stream). NULL is a no-op. */
+hrpb_status_t hrpb_free(hrpb_t A);
+
+/* Fills *view with the handle's metadata and device pointers. */
+hrpb_status_t hrpb_get_view(const hrpb_t A, hrpb_view_t* view);
+
+/* Test/introspection: copies the four HRPB arrays to HOST buffers sized from hrpb_get_view
+ * (blockedRowPtr [num_panels+1] u32, activeCols [num_blocks*tk] u32, sizePtr [num_blocks+1] u64,
+ * packedBlocks [packed_bytes] u8). Any destination may be NULL to skip it. Synchronous. */
+hrpb_status_t hrpb_copy_view_to_host(const hrpb_t A, uint32_t* blockedRowPtr, uint32_t* activeCols, uint64_t* sizePtr,
+                                     uint8_t* packedBlocks);
+
+/* Human-readable name of a status code (static storage). */
+const char* hrpb_get_error_string(hrpb_status_t status);
+
+/* cudaError_t value behind the last HRPB_ERROR_CUDA on this thread (0 if none). */
+int hrpb_last_cuda_error(void);
+
+/* Number of kernel launches the library enqueued since process start (instrumentation for the
+ * bench's gpu_launches count). */
+int64_t hrpb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HRPB_H_ */

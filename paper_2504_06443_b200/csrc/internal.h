@@ -1,0 +1,36 @@
+// internal.h — library-internal declarations shared by api.cu, build.cu and spmm.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hrpb.h"
+
+struct hrpb_handle {
+  int64_t M, K, nnz, P, NB, bytes;
+  int32_t tm, tk;
+  uint32_t* brp;    // [P+1]
+  uint32_t* ac;     // [NB_cap * tk]
+  uint64_t* sp;     // [NB_cap + 1]
+  uint8_t* packed;  // [bytes_cap]
+  cudaStream_t stream;  // build stream (frees are ordered on it)
+  // lazily sized SpMM workspace (padded B copy when N % 4 != 0)
+  float* bpad;
+  size_t bpad_bytes;
+};
+
+namespace hrpb {
+
+// device allocation helpers (stream-ordered pool); return nullptr on failure
+void* dalloc(size_t bytes, cudaStream_t s);
+void dfree(void* p, cudaStream_t s);
+void note_launch(int n = 1);
+hrpb_status_t cuda_status(cudaError_t e);
+
+hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                         const float* values, int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h);
+
+hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace hrpb

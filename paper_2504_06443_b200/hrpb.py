@@ -1,0 +1,185 @@
+"""ctypes binding of libhrpb (include/hrpb.h). Argument marshalling only — every step runs in the
+library's sm_100a kernels. Names follow the C ABI: build -> hrpb_build, spmm -> hrpb_spmm, ...
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libhrpb.so")
+_HEADER = os.path.join(os.path.dirname(_HERE), "include", "hrpb.h")
+_lib = None
+
+STATUS = {0: "HRPB_SUCCESS", 1: "HRPB_ERROR_INVALID_VALUE", 2: "HRPB_ERROR_INVALID_CSR",
+          3: "HRPB_ERROR_DIMENSION_MISMATCH", 4: "HRPB_ERROR_OUT_OF_MEMORY", 5: "HRPB_ERROR_NOT_SUPPORTED",
+          6: "HRPB_ERROR_CUDA"}
+
+
+def _header_functions():
+    txt = open(_HEADER).read()
+    return sorted(set(re.findall(r"^[a-z_0-9 ]+?\**\s*\b(hrpb_[a-z_0-9]+)\(", txt, flags=re.M)))
+
+
+EXPORTED_SYMBOLS = _header_functions()
+
+
+class HrpbError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {STATUS.get(status, status)}")
+
+
+class _Config(C.Structure):
+    _fields_ = [("tm", C.c_int32), ("tk", C.c_int32)]
+
+
+class _View(C.Structure):
+    _fields_ = [("M", C.c_int64), ("K", C.c_int64), ("nnz", C.c_int64), ("num_panels", C.c_int64),
+                ("num_blocks", C.c_int64), ("packed_bytes", C.c_int64), ("tm", C.c_int32), ("tk", C.c_int32),
+                ("blockedRowPtr", C.c_void_p), ("activeCols", C.c_void_p), ("sizePtr", C.c_void_p),
+                ("packedBlocks", C.c_void_p)]
+
+
+def lib_path() -> str:
+    return _SO
+
+
+def lib():
+    """Loads libhrpb.so. Raises if it has not been built — there is no fallback path."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            raise ImportError(f"{_SO} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(_SO)
+        i64, vp = C.c_int64, C.c_void_p
+        L.hrpb_build.argtypes = [i64, i64, i64, vp, vp, vp, C.POINTER(_Config), vp, C.POINTER(vp)]
+        L.hrpb_spmm.argtypes = [vp, vp, vp, i64, i64, i64, vp]
+        L.hrpb_build_spmm_host.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Config), vp]
+        L.hrpb_free.argtypes = [vp]
+        L.hrpb_get_view.argtypes = [vp, C.POINTER(_View)]
+        L.hrpb_copy_view_to_host.argtypes = [vp, vp, vp, vp, vp]
+        L.hrpb_get_error_string.argtypes = [C.c_int]
+        L.hrpb_get_error_string.restype = C.c_char_p
+        L.hrpb_last_cuda_error.restype = C.c_int
+        L.hrpb_launch_count.restype = C.c_int64
+        for f in ("hrpb_build", "hrpb_spmm", "hrpb_build_spmm_host", "hrpb_free", "hrpb_get_view",
+                  "hrpb_copy_view_to_host"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise HrpbError(st, where)
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dev(t, dtype, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+class Hrpb:
+    """Owning wrapper of an hrpb_t handle (immutable HRPB matrix resident in HBM)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        v = _View()
+        _check(lib().hrpb_get_view(self._h, C.byref(v)), "hrpb_get_view")
+        self.M, self.K, self.nnz = v.M, v.K, v.nnz
+        self.num_panels, self.num_blocks, self.packed_bytes = v.num_panels, v.num_blocks, v.packed_bytes
+        self.tm, self.tk = v.tm, v.tk
+        self._view = v
+
+    @property
+    def handle(self):
+        return self._h
+
+    def device_pointers(self):
+        v = self._view
+        return dict(blockedRowPtr=v.blockedRowPtr, activeCols=v.activeCols, sizePtr=v.sizePtr,
+                    packedBlocks=v.packedBlocks)
+
+    def to_host(self):
+        """(blockedRowPtr u32, activeCols u32, sizePtr u64, packedBlocks u8) as numpy arrays."""
+        brp = np.zeros(self.num_panels + 1, np.uint32)
+        ac = np.zeros(max(self.num_blocks * self.tk, 1), np.uint32)
+        sp = np.zeros(self.num_blocks + 1, np.uint64)
+        packed = np.zeros(max(self.packed_bytes, 1), np.uint8)
+        _check(lib().hrpb_copy_view_to_host(self._h, brp.ctypes.data, ac.ctypes.data, sp.ctypes.data,
+                                            packed.ctypes.data), "hrpb_copy_view_to_host")
+        return brp, ac[: self.num_blocks * self.tk], sp, packed[: self.packed_bytes]
+
+    def free(self):
+        if self._h:
+            lib().hrpb_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def build(row_ptr, col_idx, values, M: int, K: int, tm: int = 16, tk: int = 16, stream=None) -> Hrpb:
+    """hrpb_build: CSR (CUDA tensors int64/int32/float32) -> HRPB handle."""
+    import torch
+    nnz = int(col_idx.numel())
+    cfg = _Config(tm, tk)
+    h = C.c_void_p()
+    st = lib().hrpb_build(M, K, nnz, _dev(row_ptr, torch.int64, "row_ptr"), _dev(col_idx, torch.int32, "col_idx"),
+                          _dev(values, torch.float32, "values"), C.byref(cfg), _stream(stream), C.byref(h))
+    _check(st, "hrpb_build")
+    return Hrpb(h)
+
+
+def spmm(A: Hrpb, B, out=None, stream=None):
+    """hrpb_spmm: C = A.B with B a CUDA float32 (K x N) tensor; returns C (M x N)."""
+    import torch
+    if B.dim() != 2 or B.shape[0] != A.K:
+        raise ValueError(f"B must be ({A.K}, N)")
+    N = int(B.shape[1])
+    if out is None:
+        out = torch.empty((A.M, N), dtype=torch.float32, device=B.device)
+    elif tuple(out.shape) != (A.M, N):
+        raise ValueError("out has the wrong shape")
+    st = lib().hrpb_spmm(A.handle, _dev(B, torch.float32, "B"), _dev(out, torch.float32, "out"), A.M, A.K, N,
+                         _stream(stream))
+    _check(st, "hrpb_spmm")
+    return out
+
+
+def build_spmm_host(row_ptr, col_idx, values, B, M: int, K: int, out=None, tm: int = 16, tk: int = 16, stream=None):
+    """hrpb_build_spmm_host: the whole hot path from host buffers (numpy or pinned CPU tensors)."""
+    def ptr(a):
+        return C.c_void_p(a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data)
+    N = int(B.shape[1])
+    if out is None:
+        out = np.empty((M, N), np.float32)
+    nnz = int(col_idx.shape[0])
+    cfg = _Config(tm, tk)
+    st = lib().hrpb_build_spmm_host(M, K, N, nnz, ptr(row_ptr), ptr(col_idx), ptr(values), ptr(B), ptr(out),
+                                    C.byref(cfg), _stream(stream))
+    _check(st, "hrpb_build_spmm_host")
+    return out
+
+
+def launch_count() -> int:
+    return int(lib().hrpb_launch_count())

@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on the same seeded inputs.
+
+HRPB construction: byte-identical arrays (blockedRowPtr, activeCols, sizePtr, packedBlocks).
+SpMM exact mode: bit-identical C. Float mode: |C - C_ref| <= 4*2^-11*sum|a||b| + 1e-6 (north star).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from helpers import check_exact, check_float, rand_csr
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a B200", allow_module_level=True)
+
+import paper_2504_06443_b200 as hp  # noqa: E402
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_build(M, K, rp, ci, v, tm=16, tk=16):
+    return hp.build(dev(rp), dev(ci), dev(v), M, K, tm=tm, tk=tk)
+
+
+def assert_same_hrpb(A, ref, what=""):
+    brp, ac, sp, packed = A.to_host()
+    assert np.array_equal(brp, ref.blockedRowPtr), f"{what}: blockedRowPtr"
+    assert np.array_equal(ac, ref.activeCols), f"{what}: activeCols"
+    assert np.array_equal(sp, ref.sizePtr), f"{what}: sizePtr"
+    assert packed.tobytes() == ref.packedBlocks.tobytes(), f"{what}: packedBlocks"
+
+
+# --------------------------------------------------------------------------- builder (B1..B5)
+BUILD_CASES = [("c1", 0), ("c2a", 5), ("c2b", 5), ("c3", 8), ("c3p", 8), ("c4", 6), ("c5", 3)]
+
+
+@pytest.mark.parametrize("name,scale", BUILD_CASES)
+def test_builder_bit_exact_configs(name, scale):
+    w = synth.make(name, scale=scale)
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    ref = oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    assert A.num_blocks == ref.num_blocks
+    assert_same_hrpb(A, ref, name)
+    assert oracle.hrpb_check(ref, w.nnz)[0] == 0
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_builder_bit_exact_random_ragged(seed):
+    rng = np.random.default_rng(seed)
+    M, K = int(rng.integers(1, 400)), int(rng.integers(1, 3000))
+    rp, ci, v = rand_csr(M, K, float(rng.choice([0.001, 0.01, 0.1, 0.5])), seed, exact=False)
+    A = gpu_build(M, K, rp, ci, v)
+    assert_same_hrpb(A, oracle.csr_to_hrpb(M, K, rp, ci, v), f"seed {seed}")
+
+
+def test_builder_edge_cases():
+    # empty matrix, single nnz, K = 1, explicit zeros, dense panel, a hub panel (> 2048 entries)
+    cases = []
+    cases.append((40, 30, np.zeros(41, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32)))
+    cases.append((17, 9, np.array([0] * 17 + [1], np.int64), np.array([8], np.int32), np.array([3.5], np.float32)))
+    rp = np.arange(34, dtype=np.int64); rp[-1] = 33
+    cases.append((33, 1, np.arange(34, dtype=np.int64), np.zeros(33, np.int32), np.zeros(33, np.float32)))
+    d = np.ones((16, 64), bool)
+    cases.append((16, 64, np.arange(0, 16 * 64 + 1, 64, dtype=np.int64), np.tile(np.arange(64, dtype=np.int32), 16),
+                  np.arange(16 * 64, dtype=np.float32)))
+    rng = np.random.default_rng(0)
+    hub_cols = [np.sort(rng.choice(100000, 3000, replace=False)).astype(np.int32) for _ in range(20)]
+    rp = np.zeros(21, np.int64); rp[1:] = np.cumsum([len(c) for c in hub_cols])
+    cases.append((20, 100000, rp, np.concatenate(hub_cols), rng.random(int(rp[-1])).astype(np.float32)))
+    for i, (M, K, rp, ci, v) in enumerate(cases):
+        A = gpu_build(M, K, rp, ci, v)
+        assert_same_hrpb(A, oracle.csr_to_hrpb(M, K, rp, ci, v), f"edge case {i}")
+
+
+@pytest.mark.parametrize("tm,tk", [(32, 16), (64, 16), (16, 32), (128, 16)])
+def test_builder_other_tiles(tm, tk):
+    w = synth.make("c5", scale=4)
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm, tk=tk)
+    assert_same_hrpb(A, oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm, tk=tk), f"{tm}x{tk}")
+
+
+def test_builder_rejects_invalid_csr():
+    M, K = 40, 50
+    rp, ci, v = rand_csr(M, K, 0.2, 1)
+    bad = []
+    c2 = ci.copy(); c2[rp[3]], c2[rp[3] + 1] = c2[rp[3] + 1], c2[rp[3]]; bad.append((rp, c2))   # unsorted
+    c3 = ci.copy(); c3[rp[5] + 1] = c3[rp[5]]; bad.append((rp, c3))                             # duplicate
+    c4 = ci.copy(); c4[7] = K; bad.append((rp, c4))                                             # out of range
+    r5 = rp.copy(); r5[10], r5[11] = r5[11], r5[10]; bad.append((r5, ci))                       # non-monotone
+    for i, (r, c) in enumerate(bad):
+        assert r[1 + 10] >= 0
+        with pytest.raises(hp.HrpbError) as e:
+            gpu_build(M, K, r, c, v)
+        assert e.value.status == 2, i
+    with pytest.raises(hp.HrpbError) as e:   # row_ptr[M] != nnz
+        hp.build(dev(rp), dev(ci[:-1]), dev(v[:-1]), M, K)
+    assert e.value.status == 2
+
+
+# --------------------------------------------------------------------------- SpMM (S1..S5)
+@pytest.mark.parametrize("N", [1, 8, 31, 32, 33, 100, 128, 200, 256, 384, 512, 520])
+def test_spmm_exact_bitwise_widths(N):
+    w = synth.make("c1", scale=2, N=N)  # 1024 x 1024, 1%, exact-mode integers
+    B = w.B()
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    C = hp.spmm(A, dev(B)).cpu().numpy()
+    Cref = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B)
+    check_exact(C, Cref, f"N={N}")
+
+
+def test_spmm_exact_config1_full():
+    w = synth.make("c1")  # BASELINE configs[0]: 4096^2, 1%, N = 32, exact mode
+    B = w.B()
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    C = hp.spmm(A, dev(B)).cpu().numpy()
+    check_exact(C, oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B), "c1")
+
+
+@pytest.mark.parametrize("name,scale,N", [("c2a", 4, 128), ("c2b", 4, 128), ("c3", 7, 256), ("c3p", 7, 256),
+                                          ("c4", 5, 512), ("c5", 3, 32), ("c5", 3, 64), ("c5", 3, 512)])
+def test_spmm_float_tolerance(name, scale, N):
+    w = synth.make(name, scale=scale, N=N)
+    B = w.B()
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    C = hp.spmm(A, dev(B)).cpu().numpy()
+    Cref, S = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B, with_bound=True)
+    check_float(C, Cref, S, f"{name}/{N}")
+
+
+@pytest.mark.parametrize("name,scale", [("c2a", 4), ("c3", 7), ("c5", 3)])
+def test_spmm_exact_mode_other_structures(name, scale):
+    w = synth.make(name, scale=scale, N=64, mode=synth.EXACT)
+    B = w.B()
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    C = hp.spmm(A, dev(B)).cpu().numpy()
+    check_exact(C, oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B), name)
+
+
+def test_spmm_edge_cases():
+    rng = np.random.default_rng(3)
+    # empty rows / empty panels are zeroed, C fully overwritten; M not a multiple of 16
+    M, K, N = 53, 70, 48
+    rp2 = np.zeros(M + 1, np.int64)
+    # rows 20..35 emptied (panel 1 fully empty)
+    r0, c0, v0 = rand_csr(M, K, 0.05, 7)
+    cnt = np.diff(r0); cnt[20:36] = 0
+    rp2[1:] = np.cumsum(cnt)
+    ci2 = np.concatenate([c0[r0[i]:r0[i + 1]] if cnt[i] else c0[0:0] for i in range(M)]).astype(np.int32)
+    v2 = np.concatenate([v0[r0[i]:r0[i + 1]] if cnt[i] else v0[0:0] for i in range(M)]).astype(np.float32)
+    B = rng.integers(-2, 3, (K, N)).astype(np.float32)
+    A = gpu_build(M, K, rp2, ci2, v2)
+    Cd = torch.full((M, N), float("nan"), device="cuda")
+    hp.spmm(A, dev(B), out=Cd)
+    check_exact(Cd.cpu().numpy(), oracle.csr_spmm(M, K, rp2, ci2, v2, B), "empty panel")
+    # all-empty matrix
+    A0 = gpu_build(M, K, np.zeros(M + 1, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32))
+    Cd = torch.full((M, N), float("nan"), device="cuda")
+    hp.spmm(A0, dev(B), out=Cd)
+    assert not Cd.cpu().numpy().any()
+    # N = 0 is a no-op; dimension mismatch
+    hp.spmm(A, dev(np.zeros((K, 0), np.float32)))
+    with pytest.raises(hp.HrpbError) as e:
+        hp.hrpb._check(hp.hrpb.lib().hrpb_spmm(A.handle, dev(B).data_ptr(), Cd.data_ptr(), M + 1, K, N, None),
+                       "hrpb_spmm")
+    assert e.value.status == 3
+
+
+def test_spmm_hub_panel_and_dense_panel():
+    rng = np.random.default_rng(11)
+    M, K, N = 48, 20000, 96
+    cols = [np.sort(rng.choice(K, rng.integers(1, 4000), replace=False)).astype(np.int32) for _ in range(M)]
+    rp = np.zeros(M + 1, np.int64); rp[1:] = np.cumsum([len(c) for c in cols])
+    ci = np.concatenate(cols)
+    v = rng.choice(np.array([-2, -1, 1, 2], np.float32), size=ci.shape[0])
+    B = rng.integers(-2, 3, (K, N)).astype(np.float32)
+    A = gpu_build(M, K, rp, ci, v)
+    assert_same_hrpb(A, oracle.csr_to_hrpb(M, K, rp, ci, v), "hub")
+    check_exact(hp.spmm(A, dev(B)).cpu().numpy(), oracle.csr_spmm(M, K, rp, ci, v, B), "hub")
+
+
+def test_spmm_unaligned_B_pointer():
+    w = synth.make("c1", scale=3, N=20)
+    B = w.B()
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    big = torch.zeros(w.K * w.N + 1, device="cuda")
+    Bd = big[1:].view(w.K, w.N)
+    Bd.copy_(dev(B))
+    C = torch.empty((w.M, w.N), device="cuda")
+    hp.hrpb._check(hp.hrpb.lib().hrpb_spmm(A.handle, Bd.data_ptr(), C.data_ptr(), w.M, w.K, w.N, None), "spmm")
+    torch.cuda.synchronize()
+    check_exact(C.cpu().numpy(), oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B), "unaligned")
+
+
+def test_host_entry_point_matches_device_path():
+    w = synth.make("c5", scale=4, N=64)
+    B = w.B()
+    C = hp.build_spmm_host(w.row_ptr, w.col_idx, w.vals, B, w.M, w.K)
+    Cref, S = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B, with_bound=True)
+    check_float(C, Cref, S, "host path")
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    Cd = hp.spmm(A, dev(B)).cpu().numpy()
+    assert np.array_equal(C.view(np.uint32), Cd.view(np.uint32))   # same kernels, same bits
+
+
+def test_spmm_deterministic():
+    w = synth.make("c3", scale=7, N=128)
+    B = dev(w.B())
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    c1 = hp.spmm(A, B).cpu().numpy()
+    c2 = hp.spmm(A, B).cpu().numpy()
+    assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
