@@ -40,7 +40,7 @@ def _L():
         i64, u64, f64 = C.c_int64, C.c_uint64, C.c_double
         P = C.POINTER(_Csr)
         lib.synth_banded.argtypes = [i64, i64, i64, i64, u64, P]
-        lib.synth_banded_rows.argtypes = [i64, i64, i64, i64, i64, u64, P]
+        lib.synth_banded_rows.argtypes = [i64, i64, i64, i64, i64, i64, u64, P]
         lib.synth_uniform_d.argtypes = [i64, i64, i64, u64, P]
         lib.synth_bernoulli.argtypes = [i64, i64, f64, u64, P]
         lib.synth_clustered.argtypes = [i64, i64, i64, i64, u64, P]
@@ -77,9 +77,10 @@ def _call(fn, *args):
     return _take(o)
 
 
-def banded(M, K, d=16, w=32, seed=1, r0=0):
-    """Rows [r0, r0+M) of the banded matrix with K columns (row slabs are independent)."""
-    return _call(_L().synth_banded_rows, r0, M, K, d, w, seed)
+def banded(M, K, d=16, w=32, seed=1, r0=0, shift=0):
+    """Rows [r0, r0+M) of the banded matrix with K columns (row slabs are independent); row g's
+    band is centred at column g - shift."""
+    return _call(_L().synth_banded_rows, r0, M, K, d, w, shift, seed)
 
 
 def uniform_d(M, K, d=8, seed=1):

@@ -107,12 +107,14 @@ static int alloc_csr(synth_csr_t* o, int64_t M, int64_t K) {
 
 /* banded: rows [r0, r0+M) of the banded matrix (global row index g = r0 + i), so a rank can draw
  * its own row slab of a larger matrix without generating the rest. */
-int synth_banded_rows(int64_t r0, int64_t M, int64_t K, int64_t d, int64_t w, uint64_t seed, synth_csr_t* o) {
+int synth_banded_rows(int64_t r0, int64_t M, int64_t K, int64_t d, int64_t w, int64_t shift, uint64_t seed,
+                      synth_csr_t* o) {
+  /* row g = r0 + i draws from the band centred at g - shift (shift lets a rank's slab reuse B) */
   if (alloc_csr(o, M, K)) return -1;
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < M; ++i) {
-    int64_t g = r0 + i;
-    int64_t lo = g - w < 0 ? 0 : g - w, hi = g + w > K ? K : g + w;
+    int64_t g = r0 + i, ctr = g - shift;
+    int64_t lo = ctr - w < 0 ? 0 : ctr - w, hi = ctr + w > K ? K : ctr + w;
     int64_t r = hi - lo;
     o->row_ptr[i] = r < 0 ? 0 : (d < r ? d : r);
   }
@@ -122,14 +124,14 @@ int synth_banded_rows(int64_t r0, int64_t M, int64_t K, int64_t d, int64_t w, ui
   if (!o->col_idx) return -1;
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < M; ++i) {
-    int64_t g = r0 + i;
-    int64_t lo = g - w < 0 ? 0 : g - w, hi = g + w > K ? K : g + w;
+    int64_t g = r0 + i, ctr = g - shift;
+    int64_t lo = ctr - w < 0 ? 0 : ctr - w, hi = ctr + w > K ? K : ctr + w;
     draw_distinct(seed, g, lo, hi, d, o->col_idx + o->row_ptr[i]);
   }
   return 0;
 }
 int synth_banded(int64_t M, int64_t K, int64_t d, int64_t w, uint64_t seed, synth_csr_t* o) {
-  return synth_banded_rows(0, M, K, d, w, seed, o);
+  return synth_banded_rows(0, M, K, d, w, 0, seed, o);
 }
 
 int synth_uniform_d(int64_t M, int64_t K, int64_t d, uint64_t seed, synth_csr_t* o) {
