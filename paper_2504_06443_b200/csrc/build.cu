@@ -4,13 +4,14 @@
 // chunks and prefix sums; §"HRPB Sparse Matrix Data structure" defines the output.
 // B200 design: no host round trip until the end; outputs are allocated at
 // upper bounds computable from (M, nnz), so the pipeline is
-//   k_rank_small / k_rank_big  (B1: per-panel sorted-unique active columns -> compacted rank q of
-//                               every entry, nact per panel; validation of the CSR)
-//   scan(nblk) -> blockedRowPtr (B2)
-//   k_fill                     (B3: activeCols incl. sentinel K, brick patterns, block sizes)
-//   scan(size) -> sizePtr      (B4)
-//   k_pack                     (B5: HRPB-v1 headers, patterns, values in brick-CSC / row-major order)
-//   k_finalize                 (NUM_BLKS, byte total, status) -> one 32-byte D2H read + sync.
+//   k_count / k_count_big  (B1 + B3 counting: per-panel sorted-unique active columns -> compacted
+//                           rank q of every entry, nact; brick patterns; block sizes; CSR validation)
+//   scan(nblk) -> blockedRowPtr (B2); scan(panel bytes) -> panel byte offsets (B4, panel level)
+//   k_emit                 (B3 + B4 + B5: activeCols with sentinel K, sizePtr, HRPB-v1 headers,
+//                           patterns, values in brick-CSC / row-major order)
+//   k_finalize             (NUM_BLKS, byte total, status) -> one 32-byte D2H read + sync.
+// Panel p keeps its brick patterns between the two passes in a scratch region addressed from its
+// first entry offset, base(p) = floor(e0 * nbk / tk) + 2 p nbk, which never overlaps the next panel's.
 #include <cstdio>
 
 #include "common.cuh"
@@ -27,11 +28,10 @@ enum : uint32_t {
 };
 
 constexpr int kSmallThreads = 128;
-constexpr int kSmallCap = 2048;      // entries per panel handled in shared memory (bitonic path)
-constexpr int kSpanWords = 512;      // bitmap path when the panel's column span <= 16384
+constexpr int kSmallCap = 2048;      // entries per panel handled in shared memory
+constexpr int kSpanWords = 512;      // bitmap ranking when the panel's column span <= 16384
 constexpr int kBigThreads = 512;
-constexpr int kFillThreads = 128;
-constexpr int kFillSmemBricks = 1024;  // patterns kept in shared memory up to this many bricks
+constexpr int kEmitThreads = 128;
 
 // ------------------------------------------------------------------ block-wide helpers
 template <int NT>
@@ -78,77 +78,114 @@ __device__ __forceinline__ void block_minmax(int32_t& mn, int32_t& mx, int32_t* 
   __syncthreads();
 }
 
-struct PanelRows {
-  int64_t r0, r1;  // rows [r0, r1)
-};
-
-// Loads the (clamped, monotone-repaired) row pointers of panel p into shared memory; thread 0 flags a
-// decreasing row_ptr in *status (if non-null). Clamping keeps every later access inside [0, nnz).
+// Row pointers of panel p -> shared memory, clamped to [0, nnz] and repaired to be monotone (memory
+// safety on invalid input); a decreasing raw row_ptr is flagged in *status. One warp, one sync.
 __device__ __forceinline__ void load_panel_rows(const int64_t* __restrict__ rp, int64_t M, int64_t nnz, int tm,
                                                 int64_t p, int64_t* s_rp, uint32_t* status) {
   const int64_t r0 = p * tm;
   const int nrows = (int)min((int64_t)tm, M - r0);
-  __syncthreads();
-  for (int i = threadIdx.x; i <= nrows; i += blockDim.x) {
-    int64_t v = rp[r0 + i];
-    s_rp[i] = v < 0 ? 0 : (v > nnz ? nnz : v);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  __syncthreads();  // s_rp may still be read by the previous panel iteration
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int64_t carry = 0;
     bool bad = false;
-    for (int i = 1; i <= nrows; ++i) {
-      if (rp[r0 + i] < rp[r0 + i - 1]) bad = true;
-      if (s_rp[i] < s_rp[i - 1]) s_rp[i] = s_rp[i - 1];
+    for (int base = 0; base <= nrows; base += 32) {
+      const int i = base + lane;
+      const int64_t raw = i <= nrows ? rp[r0 + i] : INT64_MAX;
+      int64_t prev = __shfl_up_sync(0xffffffffu, raw, 1);
+      if (lane == 0) prev = base == 0 ? raw : carry;
+      if (i <= nrows && raw < prev) bad = true;
+      int64_t v = raw < 0 ? 0 : (raw > nnz ? nnz : raw);
+      if (i > nrows) v = 0;
+      for (int o = 1; o < 32; o <<= 1) {  // inclusive running max (monotone repair)
+        const int64_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = max(v, y);
+      }
+      if (base > 0) v = max(v, s_rp[base - 1]);
+      if (i <= nrows) s_rp[i] = v;
+      carry = __shfl_sync(0xffffffffu, raw, 31);
+      __syncwarp();
     }
-    if (bad && status) atomicOr(status, ST_RP_MONO);
+    if (__any_sync(0xffffffffu, bad) && status && lane == 0) atomicOr(status, ST_RP_MONO);
   }
   __syncthreads();
 }
 
-// ------------------------------------------------------------------ B1: panels with <= kSmallCap entries
-// One CTA per panel. q[e] = rank of col_idx[e] among the panel's distinct columns (ascending, R23),
-// nact[p] = number of distinct columns ("active_cols = uniq(cols[row_start: row_end])").
-__global__ void __launch_bounds__(kSmallThreads) k_rank_small(const int64_t* __restrict__ rp,
-                                                             const int32_t* __restrict__ ci, int64_t M, int64_t K,
-                                                             int64_t nnz, int tm, int tk, uint32_t* __restrict__ q,
-                                                             uint32_t* __restrict__ nact_out,
-                                                             uint32_t* __restrict__ nblk_out, uint32_t* status) {
+// local row of panel entry e (s_rp[r] <= e < s_rp[r+1]); binary search over <= 129 row pointers
+__device__ __forceinline__ int row_of(const int64_t* s_rp, int nrows, int64_t e) {
+  int lo = 0, hi = nrows - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_rp[mid] <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int64_t pat_base(int64_t e0, int64_t p, int nbk, int tk) {
+  return e0 * nbk / tk + 2 * p * nbk;
+}
+
+// ------------------------------------------------------------------ pass A, panels with <= kSmallCap entries
+// One CTA per panel ("for row_panel in rowPanels_chunk"). q[e] = rank of col_idx[e] among the
+// panel's distinct columns (ascending, R23; "active_cols = uniq(cols[...])"), nblk = ceil(nact/TK)
+// (R1), brick patterns (bit = (r % 16) * 4 + q % 4, R3) and the panel's total block bytes.
+__global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restrict__ rp,
+                                                        const int32_t* __restrict__ ci, int64_t M, int64_t K,
+                                                        int64_t nnz, int tm, int tk, uint32_t* __restrict__ q,
+                                                        uint32_t* __restrict__ nact_out,
+                                                        uint32_t* __restrict__ nblk_out,
+                                                        uint32_t* __restrict__ pbytes_out,
+                                                        uint64_t* __restrict__ gpat, uint32_t* __restrict__ biglist,
+                                                        uint32_t* __restrict__ nbig, uint32_t* status) {
+  extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ int64_t s_rp[129];
-  __shared__ __align__(16) uint64_t s_keys[kSmallCap];  // also reused as the bitmap (2 x 512 words)
   __shared__ uint32_t s_scan[kSmallThreads / 32 + 1];
   __shared__ int32_t s_mm[2 * kSmallThreads / 32];
+  uint64_t* s_keys = reinterpret_cast<uint64_t*>(dsm);                 // [kSmallCap] (also the bitmap)
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(s_keys + kSmallCap);   // [kSmallCap]
+  uint32_t* s_q = s_col + kSmallCap;                                   // [kSmallCap]
+  uint8_t* s_row = reinterpret_cast<uint8_t*>(s_q + kSmallCap);        // [kSmallCap]
+  unsigned long long* s_pat = reinterpret_cast<unsigned long long*>(s_row + kSmallCap);  // [cap bricks]
+
   const int64_t p = blockIdx.x;
   load_panel_rows(rp, M, nnz, tm, p, s_rp, status);
   const int nrows = (int)min((int64_t)tm, M - p * tm);
   const int64_t e0 = s_rp[0];
-  const int64_t E = s_rp[nrows] - e0;
-  if (E > kSmallCap) return;  // handled by k_rank_big (uniform exit: E is CTA-uniform)
-  if (E == 0) {
-    if (threadIdx.x == 0) { nact_out[p] = 0; nblk_out[p] = 0; }
+  const int E = (int)min((int64_t)kSmallCap + 1, s_rp[nrows] - e0);
+  if (E > kSmallCap) {  // CTA-uniform: handled by k_count_big
+    if (threadIdx.x == 0) biglist[atomicAdd(nbig, 1u)] = (uint32_t)p;
     return;
   }
-  // validation + column span
-  int32_t mn = INT32_MAX, mx = INT32_MIN;
-  for (int r = 0; r < nrows; ++r) {
-    for (int64_t e = s_rp[r] + threadIdx.x; e < s_rp[r + 1]; e += blockDim.x) {
-      int32_t c = ci[e];
-      if (c < 0 || c >= K) atomicOr(status, ST_COL_RANGE);
-      if (e > s_rp[r] && ci[e - 1] >= c) atomicOr(status, ST_COL_ORDER);
-      mn = min(mn, c);
-      mx = max(mx, c);
-    }
+  if (E == 0) {
+    if (threadIdx.x == 0) { nact_out[p] = 0; nblk_out[p] = 0; pbytes_out[p] = 0; }
+    return;
   }
-  block_minmax<kSmallThreads>(mn, mx, s_mm);
+  // entries -> shared memory (local row, column)
+  int32_t mn = INT32_MAX, mx = INT32_MIN;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {  // one flat pass: all loads in flight together
+    const int32_t c = ci[e0 + i];
+    s_col[i] = (uint32_t)c;
+    s_row[i] = (uint8_t)row_of(s_rp, nrows, e0 + i);
+    mn = min(mn, c);
+    mx = max(mx, c);
+  }
+  block_minmax<kSmallThreads>(mn, mx, s_mm);  // (contains __syncthreads)
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {  // validation
+    const int32_t c = (int32_t)s_col[i];
+    if (c < 0 || c >= K) atomicOr(status, ST_COL_RANGE);
+    if (i > 0 && s_row[i - 1] == s_row[i] && (int32_t)s_col[i - 1] >= c) atomicOr(status, ST_COL_ORDER);
+  }
   uint32_t nact = 0;
   const int64_t span = (int64_t)mx - (int64_t)mn + 1;
   if (span <= 32 * kSpanWords) {
-    // bitmap path: set bits, popcount prefix per word, rank = prefix + popc(word & below)
+    // bitmap ranking: set bits, exclusive popcount prefix per word, rank = prefix + popc(word & below)
     uint32_t* bm = reinterpret_cast<uint32_t*>(s_keys);
     uint32_t* pre = bm + kSpanWords;
     for (int i = threadIdx.x; i < kSpanWords; i += blockDim.x) bm[i] = 0;
     __syncthreads();
-    for (int64_t e = e0 + threadIdx.x; e < e0 + E; e += blockDim.x) {
-      uint32_t off = (uint32_t)(ci[e] - mn);
+    for (int i = threadIdx.x; i < E; i += blockDim.x) {
+      const uint32_t off = s_col[i] - (uint32_t)mn;
       atomicOr(&bm[off >> 5], 1u << (off & 31));
     }
     __syncthreads();
@@ -160,82 +197,102 @@ __global__ void __launch_bounds__(kSmallThreads) k_rank_small(const int64_t* __r
 #pragma unroll
     for (int i = 0; i < kPer; ++i) { pre[threadIdx.x * kPer + i] = run; run += cnt[i]; }
     __syncthreads();
-    for (int64_t e = e0 + threadIdx.x; e < e0 + E; e += blockDim.x) {
-      uint32_t off = (uint32_t)(ci[e] - mn);
-      uint32_t w = off >> 5, b = off & 31;
-      q[e] = pre[w] + __popc(bm[w] & ((1u << b) - 1u));
+    for (int i = threadIdx.x; i < E; i += blockDim.x) {
+      const uint32_t off = s_col[i] - (uint32_t)mn;
+      const uint32_t w = off >> 5, b = off & 31;
+      s_q[i] = pre[w] + __popc(bm[w] & ((1u << b) - 1u));
     }
   } else {
-    // sort path: bitonic sort of (col << 32 | local index), then unique ranks
+    // sort ranking: bitonic sort of (col << 32 | local index), unique flags, scan
     int n = 32;
     while (n < E) n <<= 1;
     for (int i = threadIdx.x; i < n; i += blockDim.x)
-      s_keys[i] = i < E ? ((uint64_t)(uint32_t)ci[e0 + i] << 32) | (uint32_t)i : ~0ull;
+      s_keys[i] = i < E ? ((uint64_t)s_col[i] << 32) | (uint32_t)i : ~0ull;
     __syncthreads();
     for (int k = 2; k <= n; k <<= 1) {
       for (int j = k >> 1; j > 0; j >>= 1) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
-          int ixj = i ^ j;
+          const int ixj = i ^ j;
           if (ixj > i) {
-            uint64_t a = s_keys[i], b = s_keys[ixj];
-            bool up = (i & k) == 0;
-            if ((a > b) == up) { s_keys[i] = b; s_keys[ixj] = a; }
+            const uint64_t a = s_keys[i], b = s_keys[ixj];
+            if ((a > b) == ((i & k) == 0)) { s_keys[i] = b; s_keys[ixj] = a; }
           }
         }
         __syncthreads();
       }
     }
-    // ranks: chunk of consecutive sorted positions per thread
     const int per = n / kSmallThreads > 0 ? n / kSmallThreads : 1;
     const int beg = threadIdx.x * per;
     uint32_t sum = 0;
-    for (int i = beg; i < beg + per && i < n; ++i)
-      if (i < E && (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32))) ++sum;
+    for (int i = beg; i < beg + per && i < E; ++i)
+      if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++sum;
     uint32_t run = block_excl_scan<kSmallThreads>(sum, &nact, s_scan);
-    for (int i = beg; i < beg + per && i < n; ++i) {
-      if (i >= E) break;
+    for (int i = beg; i < beg + per && i < E; ++i) {
       if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++run;
-      q[e0 + (uint32_t)s_keys[i]] = run - 1;
+      s_q[(uint32_t)s_keys[i]] = run - 1;
     }
   }
-  if (threadIdx.x == 0) {
-    nact_out[p] = nact;
-    nblk_out[p] = (nact + tk - 1) / tk;  // reading R1: ceil(nact / TK)
+  // patterns (fill_brick_nnz_pattern): brick i = bc * (TM/16) + br in CSC order
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const uint32_t nblk = (nact + tk - 1) / tk;
+  const int nbricks = (int)nblk * nbk;
+  for (int i = threadIdx.x; i < nbricks; i += blockDim.x) s_pat[i] = 0ull;
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    const uint32_t qq = s_q[i], r = s_row[i];
+    const uint32_t j = qq / tk, lc = qq % tk;
+    const int bit = (int)(((r & 15) << 2) | (lc & 3));
+    // 32-bit OR on the half holding the bit (a 64-bit shared atomicOr is a CAS loop on sm_100)
+    uint32_t* half = reinterpret_cast<uint32_t*>(&s_pat[j * nbk + (lc >> 2) * nbrow + (r >> 4)]) + (bit >> 5);
+    atomicOr(half, 1u << (bit & 31));
+    q[e0 + i] = qq;
   }
+  __syncthreads();
+  uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
+  for (int i = threadIdx.x; i < nbricks; i += blockDim.x) gp[i] = s_pat[i];
+  uint32_t bytes = 0;
+  for (uint32_t j = threadIdx.x; j < nblk; j += blockDim.x) {
+    uint32_t nbr = 0, nz = 0;
+    for (int i = 0; i < nbk; ++i) { const uint64_t v = s_pat[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
+    bytes += block_bytes(nbc, nbr, nz);
+  }
+  uint32_t total;
+  block_excl_scan<kSmallThreads>(bytes, &total, s_scan);
+  if (threadIdx.x == 0) { nact_out[p] = nact; nblk_out[p] = nblk; pbytes_out[p] = total; }
 }
 
-// ------------------------------------------------------------------ B1: panels with > kSmallCap entries
-// Persistent CTAs; each owns a global bitmap over the panel's column span (words + prefix).
-__global__ void __launch_bounds__(kBigThreads) k_rank_big(const int64_t* __restrict__ rp,
-                                                         const int32_t* __restrict__ ci, int64_t M, int64_t K,
-                                                         int64_t nnz, int tm, int tk, int64_t P,
-                                                         uint32_t* __restrict__ q, uint32_t* __restrict__ nact_out,
-                                                         uint32_t* __restrict__ nblk_out, uint32_t* scratch,
-                                                         int64_t words_per_cta, uint32_t* status) {
+// ------------------------------------------------------------------ pass A, panels with > kSmallCap entries
+// Persistent CTAs over the hub-panel list; each CTA owns a global bitmap over the panel's column span.
+__global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __restrict__ rp,
+                                                          const int32_t* __restrict__ ci, int64_t M, int64_t K,
+                                                          int64_t nnz, int tm, int tk, uint32_t* __restrict__ q,
+                                                          uint32_t* __restrict__ nact_out,
+                                                          uint32_t* __restrict__ nblk_out,
+                                                          uint32_t* __restrict__ pbytes_out,
+                                                          uint64_t* __restrict__ gpat,
+                                                          const uint32_t* __restrict__ biglist,
+                                                          const uint32_t* __restrict__ nbig, uint32_t* scratch,
+                                                          int64_t words_per_cta, uint32_t* status) {
   __shared__ int64_t s_rp[129];
   __shared__ uint32_t s_scan[kBigThreads / 32 + 1];
   __shared__ int32_t s_mm[2 * kBigThreads / 32];
   uint32_t* bm = scratch + (int64_t)blockIdx.x * 2 * words_per_cta;
   uint32_t* pre = bm + words_per_cta;
-  for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
-    int64_t r0 = p * tm;
-    int nrows = (int)min((int64_t)tm, M - r0);
-    int64_t a = rp[r0], b = rp[r0 + nrows];
-    a = a < 0 ? 0 : (a > nnz ? nnz : a);
-    b = b < 0 ? 0 : (b > nnz ? nnz : b);
-    if (b - a <= kSmallCap) continue;  // CTA-uniform
-    __syncthreads();
+  const uint32_t count = *nbig;
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  for (uint32_t t = blockIdx.x; t < count; t += gridDim.x) {
+    const int64_t p = biglist[t];
     load_panel_rows(rp, M, nnz, tm, p, s_rp, status);
+    const int nrows = (int)min((int64_t)tm, M - p * tm);
     const int64_t e0 = s_rp[0], e1 = s_rp[nrows];
     int32_t mn = INT32_MAX, mx = INT32_MIN;
-    for (int r = 0; r < nrows; ++r) {
-      for (int64_t e = s_rp[r] + threadIdx.x; e < s_rp[r + 1]; e += blockDim.x) {
-        int32_t c = ci[e];
-        bool ok = c >= 0 && c < K;
-        if (!ok) atomicOr(status, ST_COL_RANGE);
-        if (e > s_rp[r] && ci[e - 1] >= c) atomicOr(status, ST_COL_ORDER);
-        if (ok) { mn = min(mn, c); mx = max(mx, c); }
-      }
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const int32_t c = ci[e];
+      const bool ok = c >= 0 && c < K;
+      if (!ok) atomicOr(status, ST_COL_RANGE);
+      const int r = row_of(s_rp, nrows, e);
+      if (e > s_rp[r] && ci[e - 1] >= c) atomicOr(status, ST_COL_ORDER);
+      if (ok) { mn = min(mn, c); mx = max(mx, c); }
     }
     block_minmax<kBigThreads>(mn, mx, s_mm);
     if (mn > mx) { mn = 0; mx = 0; }
@@ -244,7 +301,7 @@ __global__ void __launch_bounds__(kBigThreads) k_rank_big(const int64_t* __restr
     for (int64_t i = threadIdx.x; i < W; i += blockDim.x) bm[i] = 0;
     __syncthreads();
     for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      int32_t c = ci[e];
+      const int32_t c = ci[e];
       if (c >= 0 && c < K) atomicOr(&bm[(c >> 5) - base], 1u << (c & 31));
     }
     __threadfence_block();
@@ -256,19 +313,36 @@ __global__ void __launch_bounds__(kBigThreads) k_rank_big(const int64_t* __restr
     uint32_t nact;
     uint32_t run = block_excl_scan<kBigThreads>(sum, &nact, s_scan);
     for (int64_t i = beg; i < end; ++i) { pre[i] = run; run += __popc(__ldcg(&bm[i])); }
+    const uint32_t nblk = (nact + tk - 1) / tk;
+    unsigned long long* gp = reinterpret_cast<unsigned long long*>(gpat + pat_base(e0, p, nbk, tk));
+    for (int64_t i = threadIdx.x; i < (int64_t)nblk * nbk; i += blockDim.x) gp[i] = 0ull;
     __threadfence_block();
     __syncthreads();
     for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      int32_t c = ci[e];
+      const int32_t c = ci[e];
       if (c < 0 || c >= K) { q[e] = 0xFFFFFFFFu; continue; }
-      int64_t w = (c >> 5) - base;
-      q[e] = __ldcg(&pre[w]) + __popc(__ldcg(&bm[w]) & ((1u << (c & 31)) - 1u));
+      const int r = row_of(s_rp, nrows, e);
+      const int64_t w = (c >> 5) - base;
+      const uint32_t qq = __ldcg(&pre[w]) + __popc(__ldcg(&bm[w]) & ((1u << (c & 31)) - 1u));
+      q[e] = qq;
+      const uint32_t j = qq / tk, lc = qq % tk;
+      atomicOr(&gp[(int64_t)j * nbk + (lc >> 2) * nbrow + (r >> 4)], 1ull << (((r & 15) << 2) | (lc & 3)));
     }
-    if (threadIdx.x == 0) {
-      nact_out[p] = nact;
-      nblk_out[p] = (nact + tk - 1) / tk;
-    }
+    __threadfence_block();
     __syncthreads();
+    uint32_t bytes = 0;
+    for (int64_t j = threadIdx.x; j < nblk; j += blockDim.x) {
+      uint32_t nbr = 0, nz = 0;
+      for (int i = 0; i < nbk; ++i) {
+        const unsigned long long v = __ldcg(&gp[j * nbk + i]);
+        nbr += v != 0ull;
+        nz += __popcll(v);
+      }
+      bytes += block_bytes(nbc, nbr, nz);
+    }
+    uint32_t total;
+    block_excl_scan<kBigThreads>(bytes, &total, s_scan);
+    if (threadIdx.x == 0) { nact_out[p] = nact; nblk_out[p] = nblk; pbytes_out[p] = total; }
   }
 }
 
@@ -372,131 +446,119 @@ static void scan_excl(const uint32_t* in, int64_t n, OutT* out, uint64_t* part, 
   note_launch(3);
 }
 
-// ------------------------------------------------------------------ B3: activeCols + patterns + sizes
-// One CTA per panel. Pattern bit for entry (row lr of the panel, compacted column q):
-// block q / TK, brick (bc = (q % TK) / 4, br = lr / 16), bit = (lr % 16) * 4 + q % 4 (R3).
-// Bricks of a block are indexed in CSC order: i = bc * (TM/16) + br.
-__global__ void __launch_bounds__(kFillThreads) k_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                                      int64_t M, int64_t K, int64_t nnz, int tm, int tk,
-                                                      const uint32_t* __restrict__ q,
-                                                      const uint32_t* __restrict__ nact_in,
-                                                      const uint32_t* __restrict__ brp, uint32_t* __restrict__ ac,
-                                                      uint64_t* __restrict__ gpat, uint32_t* __restrict__ blksz) {
-  __shared__ int64_t s_rp[129];
-  __shared__ unsigned long long s_pat[kFillSmemBricks];
-  const int64_t p = blockIdx.x;
-  const uint32_t nact = nact_in[p];
-  const uint32_t nblk = (nact + tk - 1) / tk;
-  if (nblk == 0) return;
-  const int64_t b0 = brp[p];
-  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
-  const int64_t nbricks = (int64_t)nblk * nbk;
-  const bool in_smem = nbricks <= kFillSmemBricks;
-  unsigned long long* pat = in_smem ? s_pat : reinterpret_cast<unsigned long long*>(gpat + b0 * nbk);
-  load_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);
-  const int nrows = (int)min((int64_t)tm, M - p * tm);
-  for (int64_t i = threadIdx.x; i < nbricks; i += blockDim.x) pat[i] = 0ull;
-  __threadfence_block();
-  __syncthreads();
-  for (int r = 0; r < nrows; ++r) {
-    for (int64_t e = s_rp[r] + threadIdx.x; e < s_rp[r + 1]; e += blockDim.x) {
-      uint32_t qq = q[e];
-      if (qq >= nact) continue;  // only for invalid CSR input
-      uint32_t j = qq / tk, lc = qq % tk;
-      int bc = lc >> 2, br = r >> 4;
-      int bit = ((r & 15) << 2) | (lc & 3);
-      atomicOr(&pat[(int64_t)j * nbk + bc * nbrow + br], 1ull << bit);
-      ac[(b0 + j) * tk + lc] = (uint32_t)ci[e];
-    }
-  }
-  for (int64_t t = nact + threadIdx.x; t < (int64_t)nblk * tk; t += blockDim.x) ac[b0 * tk + t] = (uint32_t)K;
-  __threadfence_block();
-  __syncthreads();
-  for (int64_t j = threadIdx.x; j < nblk; j += blockDim.x) {
-    uint32_t nbr = 0, nz = 0;
-    for (int i = 0; i < nbk; ++i) {
-      unsigned long long v = in_smem ? pat[j * nbk + i] : __ldcg(&pat[j * nbk + i]);
-      nbr += v != 0ull;
-      nz += __popcll(v);
-      if (in_smem) gpat[(b0 + j) * nbk + i] = v;
-    }
-    blksz[b0 + j] = block_bytes(nbc, nbr, nz);
-  }
-}
-
-// ------------------------------------------------------------------ B5: pack HRPB-v1 blocks
-__global__ void __launch_bounds__(kFillThreads) k_pack(const int64_t* __restrict__ rp, const float* __restrict__ vals,
-                                                      int64_t M, int64_t nnz, int tm, int tk,
-                                                      const uint32_t* __restrict__ q,
+// ------------------------------------------------------------------ pass B: emit the HRPB arrays
+// One CTA per panel. Block j of panel p is global block b0 + j (b0 = blockedRowPtr[p]); its byte offset
+// is the panel offset plus the in-panel exclusive scan of block sizes (sizePtr). Header,
+// patterns and values follow the HRPB-v1 layout; value destination = values base + popcount of the
+// earlier bricks + popcount of the lower bits of its own brick.
+__global__ void __launch_bounds__(kEmitThreads) k_emit(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                      const float* __restrict__ vals, int64_t M, int64_t K,
+                                                      int64_t nnz, int tm, int tk, const uint32_t* __restrict__ q,
                                                       const uint32_t* __restrict__ nact_in,
                                                       const uint32_t* __restrict__ brp,
-                                                      const uint64_t* __restrict__ gpat,
-                                                      const uint64_t* __restrict__ sp, uint8_t* __restrict__ packed) {
+                                                      const uint64_t* __restrict__ poff,
+                                                      const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac,
+                                                      uint64_t* __restrict__ sp, uint8_t* __restrict__ packed) {
   __shared__ int64_t s_rp[129];
+  __shared__ uint32_t s_scan[kEmitThreads / 32 + 1];
+  __shared__ uint64_t s_vbase[kEmitThreads];     // byte offset of each block's values (single-chunk panels)
+  __shared__ uint64_t s_pt[kEmitThreads * 4];    // patterns (single-chunk panels with nbk <= 4)
   const int64_t p = blockIdx.x;
-  const uint32_t nact = nact_in[p];
-  const uint32_t nblk = (nact + tk - 1) / tk;
+  const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0;
   if (nblk == 0) return;
-  const int64_t b0 = brp[p];
-  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const uint32_t nact = nact_in[p];
   load_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);
   const int nrows = (int)min((int64_t)tm, M - p * tm);
-  // headers, patterns and padding: one thread per block
-  for (int64_t j = threadIdx.x; j < nblk; j += blockDim.x) {
-    const uint64_t* pt = gpat + (b0 + j) * nbk;
-    uint8_t* blk = packed + sp[b0 + j];
-    uint32_t nbr = 0, nz = 0;
-    for (int i = 0; i < nbk; ++i) { nbr += pt[i] != 0; nz += __popcll(pt[i]); }
-    const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
-    uint32_t k = 0;
-    blk[0] = 0;
-    for (int bc = 0; bc < nbc; ++bc) {
-      for (int br = 0; br < nbrow; ++br) {
-        uint64_t v = pt[bc * nbrow + br];
-        if (!v) continue;
-        blk[nbc + 1 + k] = (uint8_t)br;                                   // rows[]
-        reinterpret_cast<uint64_t*>(blk + hdr)[k] = v;                    // patterns[]
-        ++k;
-      }
-      blk[bc + 1] = (uint8_t)k;                                           // colPtr[]
-    }
-    for (uint32_t i = nbc + 1 + nbr; i < hdr; ++i) blk[i] = 0;
-    const uint32_t end = hdr + 8 * nbr + 4 * nz, size = block_bytes(nbc, nbr, nz);
-    for (uint32_t i = end; i < size; ++i) blk[i] = 0;
-  }
-  // values: destination = values base + prefix popcount of earlier bricks + rank of the bit
-  for (int r = 0; r < nrows; ++r) {
-    for (int64_t e = s_rp[r] + threadIdx.x; e < s_rp[r + 1]; e += blockDim.x) {
-      uint32_t qq = q[e];
-      if (qq >= nact) continue;
-      uint32_t j = qq / tk, lc = qq % tk;
-      int bc = lc >> 2, br = r >> 4;
-      int bit = ((r & 15) << 2) | (lc & 3);
-      const uint64_t* pt = gpat + (b0 + j) * nbk;
-      const int mine = bc * nbrow + br;
-      uint32_t nbr = 0, off = 0;
+  const int64_t e0 = s_rp[0];
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
+  // blocks: sizes, sizePtr, headers, patterns, padding (chunks of kEmitThreads blocks)
+  uint64_t carry = poff[p];
+  for (uint32_t c0 = 0; c0 < nblk; c0 += kEmitThreads) {
+    const uint32_t j = c0 + threadIdx.x;
+    uint32_t nbr = 0, nz = 0, size = 0;
+    if (j < nblk) {
       for (int i = 0; i < nbk; ++i) {
-        uint64_t v = pt[i];
-        nbr += v != 0;
-        if (i < mine) off += __popcll(v);
+        const uint64_t v = gp[(int64_t)j * nbk + i];
+        nbr += v != 0ull;
+        nz += __popcll(v);
       }
-      const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
-      off += __popcll(pt[mine] & ((1ull << bit) - 1ull));
-      float* dst = reinterpret_cast<float*>(packed + sp[b0 + j] + hdr + 8 * nbr) + off;
-      *dst = vals[e];
+      size = block_bytes(nbc, nbr, nz);
     }
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<kEmitThreads>(size, &tot, s_scan);
+    if (j < nblk) {
+      const uint64_t off = carry + ex;
+      sp[b0 + j] = off;
+      uint8_t* blk = packed + off;
+      const uint64_t* pt = gp + (int64_t)j * nbk;
+      const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+      uint32_t k = 0;
+      blk[0] = 0;
+      for (int bc = 0; bc < nbc; ++bc) {
+        for (int br = 0; br < nbrow; ++br) {
+          const uint64_t v = pt[bc * nbrow + br];
+          if (!v) continue;
+          blk[nbc + 1 + k] = (uint8_t)br;                 // rows[]
+          reinterpret_cast<uint64_t*>(blk + hdr)[k] = v;  // patterns[]
+          ++k;
+        }
+        blk[bc + 1] = (uint8_t)k;  // colPtr[]
+      }
+      for (uint32_t i = nbc + 1 + nbr; i < hdr; ++i) blk[i] = 0;
+      for (uint32_t i = hdr + 8 * nbr + 4 * nz; i < size; ++i) blk[i] = 0;
+      if (nblk <= kEmitThreads) {
+        s_vbase[j] = off + hdr + 8 * nbr;
+        if (nbk <= 4)
+          for (int i = 0; i < nbk; ++i) s_pt[j * nbk + i] = pt[i];
+      }
+    }
+    carry += tot;
+  }
+  for (int64_t t = nact + threadIdx.x; t < (int64_t)nblk * tk; t += blockDim.x) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
+  __syncthreads();  // sizePtr entries / staged metadata of this panel are visible to the whole CTA
+  const bool staged = nblk <= kEmitThreads && nbk <= 4;
+  const int64_t e1 = s_rp[nrows];
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const uint32_t qq = q[e];
+    const int32_t c = ci[e];
+    const float v = vals[e];
+    if (qq >= nact) continue;  // only for invalid CSR input
+    const int r = row_of(s_rp, nrows, e);
+    const uint32_t j = qq / tk, lc = qq % tk;
+    ac[((int64_t)b0 + j) * tk + lc] = (uint32_t)c;
+    const int bit = ((r & 15) << 2) | (lc & 3);
+    const int mine = (lc >> 2) * nbrow + (r >> 4);
+    const uint64_t* pt = staged ? s_pt + j * nbk : gp + (int64_t)j * nbk;
+    uint32_t nbr = 0, off = 0;
+    for (int i = 0; i < nbk; ++i) {
+      const uint64_t w = pt[i];
+      nbr += w != 0ull;
+      if (i < mine) off += __popcll(w);
+    }
+    off += __popcll(pt[mine] & ((1ull << bit) - 1ull));
+    uint64_t vb;
+    if (staged) {
+      vb = s_vbase[j];
+    } else {
+      const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+      vb = sp[b0 + j] + hdr + 8 * nbr;
+    }
+    reinterpret_cast<float*>(packed + vb)[off] = v;
   }
 }
 
 __global__ void k_finalize(const int64_t* __restrict__ rp, int64_t M, int64_t nnz, int64_t P,
-                           const uint32_t* __restrict__ brp, const uint64_t* __restrict__ sp,
-                           const uint32_t* __restrict__ status, uint64_t* __restrict__ info) {
+                           const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff,
+                           uint64_t* __restrict__ sp, const uint32_t* __restrict__ status,
+                           uint64_t* __restrict__ info) {
   uint32_t st = *status;
   if (rp[0] != 0) st |= ST_RP0;
   if (rp[M] != nnz) st |= ST_NNZ;
-  uint64_t nb = brp[P];
+  const uint64_t nb = brp[P];
+  sp[nb] = poff[P];
   info[0] = nb;
-  info[1] = sp[nb];
+  info[1] = poff[P];
   info[2] = st;
 }
 
@@ -510,6 +572,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   const int64_t hdr_cap = align_up(nbc + 1 + nbk, 8) + 15;
   const int64_t brick_cap = nnz < nb_cap * nbk ? nnz : nb_cap * nbk;
   const int64_t bytes_cap = nb_cap * hdr_cap + 8 * brick_cap + 4 * nnz;
+  const int64_t pat_cap = nnz * nbk / tk + 2 * (P + 1) * nbk + nbk;
 
   h->M = M; h->K = K; h->nnz = nnz; h->P = P; h->tm = tm; h->tk = tk; h->stream = s;
   h->brp = (uint32_t*)dalloc((P + 1) * sizeof(uint32_t), s);
@@ -517,51 +580,58 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   h->sp = (uint64_t*)dalloc((nb_cap + 1) * sizeof(uint64_t), s);
   h->packed = (uint8_t*)dalloc(bytes_cap + 16, s);
   uint32_t* q = (uint32_t*)dalloc((nnz + 1) * sizeof(uint32_t), s);
-  uint32_t* nact = (uint32_t*)dalloc((P + 1) * sizeof(uint32_t), s);
-  uint32_t* nblk = (uint32_t*)dalloc((P + 1) * sizeof(uint32_t), s);
-  uint32_t* blksz = (uint32_t*)dalloc((nb_cap + 1) * sizeof(uint32_t), s);
-  uint64_t* gpat = (uint64_t*)dalloc((nb_cap * nbk + 1) * sizeof(uint64_t), s);
-  const int64_t nparts = ceil_div((nb_cap > P ? nb_cap : P) + 1, kScanChunk) + 1;
+  uint32_t* cnt = (uint32_t*)dalloc(3 * (P + 1) * sizeof(uint32_t), s);  // nact | nblk | panel bytes
+  uint32_t* nact = cnt;
+  uint32_t* nblk = cnt + (P + 1);
+  uint32_t* pbytes = cnt + 2 * (P + 1);
+  uint64_t* poff = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t), s);
+  uint64_t* gpat = (uint64_t*)dalloc(pat_cap * sizeof(uint64_t), s);
+  uint32_t* biglist = (uint32_t*)dalloc((P + 1) * sizeof(uint32_t), s);
+  const int64_t nparts = ceil_div(P + 1, kScanChunk) + 1;
   uint64_t* part = (uint64_t*)dalloc(nparts * sizeof(uint64_t), s);
-  uint64_t* info = (uint64_t*)dalloc(4 * sizeof(uint64_t), s);  // [3] = status word
+  uint64_t* info = (uint64_t*)dalloc(4 * sizeof(uint64_t), s);  // [3] = status word | hub count
   const int big_ctas = num_sms();
   const int64_t words = ceil_div(K, 32) + 2;
   uint32_t* bigscr = (uint32_t*)dalloc((size_t)big_ctas * 2 * words * sizeof(uint32_t), s);
   hrpb_status_t st = HRPB_SUCCESS;
-  if (!h->brp || !h->ac || !h->sp || !h->packed || !q || !nact || !nblk || !blksz || !gpat || !part || !info ||
+  if (!h->brp || !h->ac || !h->sp || !h->packed || !q || !cnt || !poff || !gpat || !biglist || !part || !info ||
       !bigscr) {
     st = HRPB_ERROR_OUT_OF_MEMORY;
   }
   uint64_t hinfo[3] = {0, 0, 0};
   if (st == HRPB_SUCCESS) {
     uint32_t* status = reinterpret_cast<uint32_t*>(info + 3);
-    cudaMemsetAsync(status, 0, sizeof(uint32_t), s);
-    cudaMemsetAsync(blksz, 0, (nb_cap + 1) * sizeof(uint32_t), s);  // tail of the sizePtr scan input
-    if (P > 0) {  // B1
-      k_rank_small<<<(unsigned)P, kSmallThreads, 0, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk, status);
-      k_rank_big<<<big_ctas, kBigThreads, 0, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, P, q, nact, nblk, bigscr,
-                                                   words, status);
+    uint32_t* nbig = status + 1;
+    cudaMemsetAsync(status, 0, 2 * sizeof(uint32_t), s);
+    const size_t count_smem =
+        (size_t)kSmallCap * (8 + 4 + 4 + 1) + (size_t)ceil_div(kSmallCap, tk) * nbk * sizeof(uint64_t);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    if (P > 0) {  // pass A
+      k_count<<<(unsigned)P, kSmallThreads, count_smem, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
+                                                            pbytes, gpat, biglist, nbig, status);
+      k_count_big<<<big_ctas, kBigThreads, 0, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk, pbytes, gpat,
+                                                    biglist, nbig, bigscr, words, status);
       note_launch(2);
     }
     scan_excl<uint32_t>(nblk, P, h->brp, part, s);  // B2: blockedRowPtr
-    if (P > 0) {                                     // B3
-      k_fill<<<(unsigned)P, kFillThreads, 0, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, h->brp, h->ac, gpat,
-                                                  blksz);
+    scan_excl<uint64_t>(pbytes, P, poff, part, s);  // B4 (panel level): byte offset of each panel
+    if (P > 0) {                                    // pass B
+      k_emit<<<(unsigned)P, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp, poff,
+                                                  gpat, h->ac, h->sp, h->packed);
       note_launch();
     }
-    scan_excl<uint64_t>(blksz, nb_cap, h->sp, part, s);  // B4: sizePtr (entries past NUM_BLKS are zero)
-    if (P > 0) {                                          // B5
-      k_pack<<<(unsigned)P, kFillThreads, 0, s>>>(row_ptr, values, M, nnz, tm, tk, q, nact, h->brp, gpat, h->sp,
-                                                  h->packed);
-      note_launch();
-    }
-    k_finalize<<<1, 1, 0, s>>>(row_ptr, M, nnz, P, h->brp, h->sp, status, info);
+    k_finalize<<<1, 1, 0, s>>>(row_ptr, M, nnz, P, h->brp, poff, h->sp, status, info);
     note_launch();
-    cudaError_t e = cudaMemcpyAsync(hinfo, info, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hinfo, info, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) st = cuda_status(e);
   }
-  dfree(q, s); dfree(nact, s); dfree(nblk, s); dfree(blksz, s); dfree(gpat, s); dfree(part, s); dfree(info, s);
+  dfree(q, s); dfree(cnt, s); dfree(poff, s); dfree(gpat, s); dfree(biglist, s); dfree(part, s); dfree(info, s);
   dfree(bigscr, s);
   if (st == HRPB_SUCCESS && hinfo[2] != 0) st = HRPB_ERROR_INVALID_CSR;
   h->NB = (int64_t)hinfo[0];

@@ -18,6 +18,7 @@
 //  * warps 3..6: epilogue — tcgen05.ld 32x32b, coalesced 128-B row stores of C (S5);
 //  * mbarrier rings: full_a/full_b (TMA), dec (decoder), empty (tcgen05.commit), tfull/tempty.
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -25,7 +26,8 @@
 
 namespace hrpb {
 
-constexpr int kSpmmThreads = 224;  // 7 warps
+constexpr int kSpmmThreads = 320;  // 10 warps: 4 producers, decoder, MMA, 4 epilogue
+constexpr int kProdWarps = 4;
 constexpr int kARawBytes = 1152;   // >= 1072 (largest TM=16/TK=16 block), multiple of 128
 constexpr int kATileBytes = 1024;  // 16 x 16 fp32 decoded block
 constexpr int kMaxStages = 16;
@@ -37,6 +39,8 @@ struct SpmmParams {
   const uint8_t* packed;
   float* C;
   int64_t M, N, P, NB;
+  const float* B;  // row-major K x ldb (cp.async gather mode)
+  int64_t K, ldb;
   int n0;      // first output column of this launch
   int stages;  // pipeline depth
 };
@@ -63,7 +67,55 @@ __device__ __forceinline__ int64_t panel_lower_bound(const uint32_t* brp, int64_
   return lo;
 }
 
-template <int NT>
+// Warp-cooperative iteration over panels [pa, pb): blockedRowPtr is fetched 32 panels per coalesced
+// load, one chunk ahead. All 32 lanes must call next() convergently; it returns false at the end.
+struct PanelCursor {
+  const uint32_t* brp;
+  int64_t pb, base, j;
+  int cnt;
+  uint32_t cur, cur_last, nxt, nxt_last;
+  int lane;
+  __device__ void load(int64_t b0, uint32_t& v, uint32_t& last) {
+    const int64_t idx = b0 + lane;
+    v = idx <= pb ? __ldg(brp + idx) : 0u;
+    last = __ldg(brp + (b0 + 32 <= pb ? b0 + 32 : pb));
+  }
+  __device__ PanelCursor(const uint32_t* brp_, int64_t pa, int64_t pb_, int lane_)
+      : brp(brp_), pb(pb_), base(pa), j(-1), lane(lane_) {
+    cnt = (int)min((int64_t)32, pb - pa);
+    if (pa < pb) load(pa, cur, cur_last);
+    if (pa + 32 < pb) load(pa + 32, nxt, nxt_last);
+  }
+  // advances to the next panel; p = panel id, bb/be = its block range
+  __device__ bool next(int64_t& p, uint32_t& bb, uint32_t& be) {
+    if (base >= pb) return false;
+    if (++j == cnt) {
+      base += 32;
+      if (base >= pb) return false;
+      cur = nxt;
+      cur_last = nxt_last;
+      cnt = (int)min((int64_t)32, pb - base);
+      j = 0;
+      if (base + 32 < pb) load(base + 32, nxt, nxt_last);
+    }
+    p = base + j;
+    bb = __shfl_sync(0xffffffffu, cur, (int)j);
+    const uint32_t nx = __shfl_sync(0xffffffffu, cur, (int)(j + 1) & 31);
+    be = j + 1 < 32 ? nx : cur_last;
+    return true;
+  }
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// GM = gather mode: 0 = TMA tile::gather4 (one issuing lane per producer warp),
+//                   1 = cp.async 16-B copies by all 128 producer threads into the same swizzled layout.
+template <int NT, int GM>
 __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant__ CUtensorMap tmB, SpmmParams prm) {
   using L = SmemLayout<NT>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -88,7 +140,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_a[s], 1);
-      mbar_init(&full_b[s], 1);
+      mbar_init(&full_b[s], GM == 0 ? kProdWarps : kProdWarps * 32);
       mbar_init(&dec[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -101,7 +153,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     range[1] = c + 1 == G ? prm.P : panel_lower_bound(prm.brp, prm.P, (c + 1) * W / G);
     prefetch_tmap(&tmB);
   }
-  if (warp == 2) tmem_alloc(&misc[0], tmem_cols);
+  if (warp == 5) tmem_alloc(&misc[0], tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -111,37 +163,84 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   const int n0 = prm.n0;
   const int64_t N = prm.N, M = prm.M;
 
-  if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
-    if (lane == 0) {
-      const uint64_t pol_a = policy_evict_first();
-      const int na_eff = (int)min((int64_t)L::kNA, ceil_div(N - n0, 32));  // atoms with any column < N
-      const uint32_t b_bytes = 16u * 128u * (uint32_t)na_eff;
-      uint32_t i = 0;
-      const int64_t b_begin = brp[pa], b_end = brp[pb];
-      for (int64_t b = b_begin; b < b_end; ++b, ++i) {
-        const int s = i % S;
-        const uint32_t ph = (i / S) & 1;
-        const uint4* acv = reinterpret_cast<const uint4*>(prm.ac + b * 16);
-        uint4 c0 = __ldg(acv), c1 = __ldg(acv + 1), c2 = __ldg(acv + 2), c3 = __ldg(acv + 3);
-        const uint64_t s0 = __ldg(prm.sp + b), s1 = __ldg(prm.sp + b + 1);
-        mbar_wait(&empty[s], ph ^ 1);
-        const uint32_t a_bytes = (uint32_t)(s1 - s0);
-        mbar_expect_tx(&full_a[s], a_bytes);
-        bulk_g2s(araw0 + (size_t)s * kARawBytes, prm.packed + s0, a_bytes, &full_a[s], pol_a);
-        mbar_expect_tx(&full_b[s], b_bytes);
-        uint8_t* bt = btile0 + (size_t)s * L::kBTile;
-        const uint4 rows[4] = {c0, c1, c2, c3};
-#pragma unroll
-        for (int g4 = 0; g4 < 4; ++g4) {
-          for (int a = 0; a < na_eff; ++a) {
-            tma_gather4(bt + (g4 * L::kNA + a) * 512, &tmB, n0 + 32 * a, (int32_t)rows[g4].x, (int32_t)rows[g4].y,
-                        (int32_t)rows[g4].z, (int32_t)rows[g4].w, &full_b[s]);
-          }
+  if (warp < kProdWarps) {
+    // ---------------------------------------------------------------- producers (warps 0..3)
+    // Warp w stages rows 4w..4w+3 of every block's gathered B tile (S3); warp 0 also copies the
+    // packed block bytes (S2). Metadata of 32 consecutive blocks is fetched by one coalesced load per
+    // warp (lane l: block base + l), one chunk ahead, so no global latency sits between two issues.
+    const uint64_t pol_a = policy_evict_first();
+    const int na_eff = (int)min((int64_t)L::kNA, ceil_div(N - n0, 32));  // 32-col atoms with a column < N
+    const int64_t b_begin = brp[pa], b_end = brp[pb];
+    const int pw = warp;
+    uint4 cur = make_uint4(0, 0, 0, 0), nxt = make_uint4(0, 0, 0, 0);
+    uint64_t cs0 = 0, cs1 = 0, ns0 = 0, ns1 = 0;
+    auto load_chunk = [&](int64_t base, uint4& r, uint64_t& s0, uint64_t& s1) {
+      const int64_t bl = base + lane;
+      if (bl < b_end) {
+        r = __ldg(reinterpret_cast<const uint4*>(prm.ac + bl * 16) + pw);
+        if (pw == 0) {
+          s0 = __ldg(prm.sp + bl);
+          s1 = __ldg(prm.sp + bl + 1);
         }
       }
+    };
+    if (b_begin < b_end) load_chunk(b_begin, cur, cs0, cs1);
+    const uint32_t bt0 = smem_u32(btile0);
+    uint32_t i = 0;
+    for (int64_t base = b_begin; base < b_end; base += 32) {
+      if (base + 32 < b_end) load_chunk(base + 32, nxt, ns0, ns1);
+      const int cnt = (int)min((int64_t)32, b_end - base);
+      for (int j = 0; j < cnt; ++j, ++i) {
+        const int s = i % S;
+        const uint32_t ph = (i / S) & 1;
+        const uint32_t r0 = __shfl_sync(0xffffffffu, cur.x, j), r1 = __shfl_sync(0xffffffffu, cur.y, j);
+        const uint32_t r2 = __shfl_sync(0xffffffffu, cur.z, j), r3 = __shfl_sync(0xffffffffu, cur.w, j);
+        uint64_t s0 = 0, s1 = 0;
+        if (pw == 0) { s0 = __shfl_sync(0xffffffffu, cs0, j); s1 = __shfl_sync(0xffffffffu, cs1, j); }
+        mbar_wait(&empty[s], ph ^ 1);
+        if (pw == 0 && lane == 0) {
+          const uint32_t a_bytes = (uint32_t)(s1 - s0);
+          mbar_expect_tx(&full_a[s], a_bytes);
+          bulk_g2s(araw0 + (size_t)s * kARawBytes, prm.packed + s0, a_bytes, &full_a[s], pol_a);
+        }
+        const uint32_t bt = bt0 + s * L::kBTile + pw * L::kNA * 512;  // this warp's 4-row group
+        if constexpr (GM == 0) {
+          if (lane == 0) {
+            mbar_expect_tx(&full_b[s], 4u * 128u * (uint32_t)na_eff);
+            uint8_t* btg = btile0 + (size_t)s * L::kBTile + pw * L::kNA * 512;
+            for (int a = 0; a < na_eff; ++a)
+              tma_gather4(btg + a * 512, &tmB, n0 + 32 * a, (int32_t)r0, (int32_t)r1, (int32_t)r2, (int32_t)r3,
+                          &full_b[s]);
+          }
+        } else {
+          // lane copies 16-B chunk c = lane + 32 t of each of the 4 rows; destination follows the UMMA
+          // SWIZZLE_128B_BASE32B MN-major atom (4 rows x 128 B, 32-B granule g stored at g ^ row)
+          const uint32_t rows[4] = {r0, r1, r2, r3};
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) {
+            const bool real = rows[rr] < (uint32_t)prm.K;  // sentinel K -> zero fill
+            const float* src_row = prm.B + (int64_t)(real ? rows[rr] : 0) * prm.ldb + n0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              const int c = lane + 32 * t;  // 16-B chunk along N
+              const int a = c >> 3;         // atom
+              if (a < na_eff) {
+                const int g = (c >> 1) & 3, h = c & 1;
+                const uint32_t dst = bt + a * 512 + rr * 128 + ((g ^ rr) << 5) + (h << 4);
+                const bool inb = real && (n0 + 4 * c) < N;
+                cp_async16(dst, src_row + 4 * c, inb ? 16u : 0u);
+              }
+            }
+          }
+          cp_async_arrive_noinc(&full_b[s]);
+        }
+        __syncwarp();
+      }
+      cur = nxt;
+      cs0 = ns0;
+      cs1 = ns1;
     }
-  } else if (warp == 1) {
+  } else if (warp == 4) {
     // ---------------------------------------------------------------- decoder
     uint32_t i = 0;
     const int64_t b_begin = brp[pa], b_end = brp[pb];
@@ -177,24 +276,26 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       __syncwarp();
       if (lane == 0) mbar_arrive(&dec[s]);
     }
-  } else if (warp == 2) {
+  } else if (warp == 5) {
     // ---------------------------------------------------------------- MMA issuer (one thread)
-    if (lane == 0) {
-      uint32_t i = 0, pc = 0;
-      const uint32_t bt0 = smem_u32(btile0), at0 = smem_u32(atile0);
-      for (int64_t p = pa; p < pb; ++p) {
-        const int64_t bb = brp[p], be = brp[p + 1];
-        if (bb == be) continue;
-        const uint32_t slot = pc & 1;
-        mbar_wait(&tempty[slot], ((pc >> 1) & 1) ^ 1);
+    uint32_t i = 0, pc = 0;
+    const uint32_t bt0 = smem_u32(btile0), at0 = smem_u32(atile0);
+    PanelCursor cursor(brp, pa, pb, lane);
+    int64_t p;
+    uint32_t bb, be;
+    while (cursor.next(p, bb, be)) {
+      if (bb == be) continue;
+      const uint32_t slot = pc & 1;
+      mbar_wait(&tempty[slot], ((pc >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dcol = tbase + slot * NT * 16;
+      for (uint32_t b = bb; b < be; ++b, ++i) {
+        const int s = i % S;
+        const uint32_t ph = (i / S) & 1;
+        mbar_wait(&full_b[s], ph);
+        mbar_wait(&dec[s], ph);
         tc_fence_after();
-        const uint32_t dcol = tbase + slot * NT * 16;
-        for (int64_t b = bb; b < be; ++b, ++i) {
-          const int s = i % S;
-          const uint32_t ph = (i / S) & 1;
-          mbar_wait(&full_b[s], ph);
-          mbar_wait(&dec[s], ph);
-          tc_fence_after();
+        if (lane == 0) {
           const uint32_t bt = bt0 + s * L::kBTile, at = at0 + s * kATileBytes;
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
@@ -207,21 +308,25 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
           }
           umma_commit(&empty[s]);
         }
-        umma_commit(&tfull[slot]);
-        ++pc;
+        __syncwarp();
       }
+      if (lane == 0) umma_commit(&tfull[slot]);
+      __syncwarp();
+      ++pc;
     }
-    __syncwarp();
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 3..6)
+    // ---------------------------------------------------------------- epilogue (warps 6..9)
     const int qd = warp & 3;            // TMEM lane quadrant accessible to this warp
-    const int et = tid - 96;            // 0..127
+    const int et = tid - 192;           // 0..127
     const int64_t ncols = min((int64_t)128 * NT, N - n0);
     uint32_t pc = 0;
-    for (int64_t p = pa; p < pb; ++p) {
+    PanelCursor cursor(brp, pa, pb, lane);
+    int64_t p;
+    uint32_t bb, be;
+    while (cursor.next(p, bb, be)) {
       const int64_t row0 = p * 16;
       const int nrows = (int)min((int64_t)16, M - row0);
-      if (brp[p] == brp[p + 1]) {  // empty panel: zero rows (R13)
+      if (bb == be) {  // empty panel: zero rows (R13)
         for (int r = 0; r < nrows; ++r)
           for (int64_t c = et; c < ncols; c += 128) prm.C[(row0 + r) * N + n0 + c] = 0.f;
         continue;
@@ -250,7 +355,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 5) {
     tc_fence_after();
     tmem_dealloc(tbase, tmem_cols);
   }
@@ -283,9 +388,9 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-template <int NT>
-static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, float* C, int64_t N, int n0,
-                               cudaStream_t s) {
+template <int NT, int GM>
+static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, const float* B, int64_t ldb, float* C,
+                               int64_t N, int n0, cudaStream_t s) {
   using L = SmemLayout<NT>;
   const int budget = 227 * 1024 - 1024 /*alignment*/ - 512 /*barriers, misc*/;
   int stages = budget / L::kStage;
@@ -293,14 +398,14 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, floa
   const size_t smem = 1024 + (size_t)stages * L::kStage + (4 * stages + 4) * 8 + 64;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_spmm<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_spmm<NT, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return cuda_status(e);
     attr_set = true;
   }
-  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, n0, stages};
+  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, B, h->K, ldb, n0, stages};
   int grid = num_sms();
   if ((int64_t)grid > h->P) grid = (int)(h->P > 0 ? h->P : 1);
-  k_spmm<NT><<<grid, kSpmmThreads, smem, s>>>(tm, prm);
+  k_spmm<NT, GM><<<grid, kSpmmThreads, smem, s>>>(tm, prm);
   note_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);
@@ -345,11 +450,24 @@ hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float
     const int64_t w = N - n0 < 512 ? N - n0 : 512;
     const int nt = (int)ceil_div(w, 128);
     hrpb_status_t st;
-    switch (nt) {
-      case 1: st = launch_nt<1>(h, tm, C, N, (int)n0, s); break;
-      case 2: st = launch_nt<2>(h, tm, C, N, (int)n0, s); break;
-      case 3: st = launch_nt<3>(h, tm, C, N, (int)n0, s); break;
-      default: st = launch_nt<4>(h, tm, C, N, (int)n0, s); break;
+    static const int gm = [] {
+      const char* e = getenv("HRPB_GATHER");  // 0 = TMA gather4, 1 = cp.async (default)
+      return e ? atoi(e) : 1;
+    }();
+    if (gm == 0) {
+      switch (nt) {
+        case 1: st = launch_nt<1, 0>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+        case 2: st = launch_nt<2, 0>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+        case 3: st = launch_nt<3, 0>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+        default: st = launch_nt<4, 0>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+      }
+    } else {
+      switch (nt) {
+        case 1: st = launch_nt<1, 1>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+        case 2: st = launch_nt<2, 1>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+        case 3: st = launch_nt<3, 1>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+        default: st = launch_nt<4, 1>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+      }
     }
     if (st != HRPB_SUCCESS) return st;
   }
