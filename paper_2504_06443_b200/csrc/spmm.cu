@@ -26,11 +26,14 @@
 
 namespace hrpb {
 
-constexpr int kSpmmThreads = 320;  // 10 warps: 4 producers, decoder, MMA, 4 epilogue
-constexpr int kProdWarps = 4;
+constexpr int kProdWarps = 4;                              // warps 0..3: gather producers
+constexpr int kDecWarps = 4;                               // warps 4..7: brick decoders
+constexpr int kMmaWarp = kProdWarps + kDecWarps;           // warp 8: TMEM alloc + MMA issue
+constexpr int kEpiWarp0 = kMmaWarp + 1;                    // warps 9..12: epilogue
+constexpr int kSpmmThreads = 32 * (kEpiWarp0 + 4);        // 416
 constexpr int kARawBytes = 1152;   // >= 1072 (largest TM=16/TK=16 block), multiple of 128
 constexpr int kATileBytes = 1024;  // 16 x 16 fp32 decoded block
-constexpr int kMaxStages = 16;
+constexpr int kMaxStages = 20;
 
 struct SpmmParams {
   const uint32_t* brp;
@@ -43,7 +46,14 @@ struct SpmmParams {
   int64_t K, ldb;
   int n0;      // first output column of this launch
   int stages;  // pipeline depth
+  long long* trace;  // optional: per-block event timestamps of CTA 0 (HRPB_TRACE), [6][kTraceN]
 };
+constexpr int kTraceN = 1024;
+// trace slots: 0 producer issue (after empty), 1 A arrived (decoder), 2 decode done, 3 B arrived (MMA),
+//              4 MMA issued, 5 epilogue got tfull (per panel)
+__device__ __forceinline__ void trace_ev(const SpmmParams& p, int slot, uint32_t i) {
+  if (p.trace != nullptr && blockIdx.x == 0 && i < kTraceN) p.trace[slot * kTraceN + i] = clock64();
+}
 
 // instruction descriptor: D F32, A/B TF32, A MN-major, B K-major, N = 16, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (0u << 16) | ((16u >> 3) << 17) |
@@ -140,7 +150,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_a[s], 1);
-      mbar_init(&full_b[s], GM == 0 ? kProdWarps : kProdWarps * 32);
+      mbar_init(&full_b[s], GM == 0 ? 1 : 32);  // one producer warp per block
       mbar_init(&dec[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -153,7 +163,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     range[1] = c + 1 == G ? prm.P : panel_lower_bound(prm.brp, prm.P, (c + 1) * W / G);
     prefetch_tmap(&tmB);
   }
-  if (warp == 5) tmem_alloc(&misc[0], tmem_cols);
+  if (warp == kMmaWarp) tmem_alloc(&misc[0], tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -165,89 +175,127 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
 
   if (warp < kProdWarps) {
     // ---------------------------------------------------------------- producers (warps 0..3)
-    // Warp w stages rows 4w..4w+3 of every block's gathered B tile (S3); warp 0 also copies the
-    // packed block bytes (S2). Metadata of 32 consecutive blocks is fetched by one coalesced load per
-    // warp (lane l: block base + l), one chunk ahead, so no global latency sits between two issues.
+    // Warp w stages blocks i = w, w+4, ... (the i-th block of this CTA uses stage i % S): the packed
+    // block bytes (S2, one bulk copy) and its 16 gathered B rows (S3). One cp.async instruction moves one
+    // contiguous 512-B row segment (lane = 16-B chunk); lanes 0..15 prefetch the block's activeCols 8 blocks
+    // ahead and the row index is broadcast by shuffle.
     const uint64_t pol_a = policy_evict_first();
     const int na_eff = (int)min((int64_t)L::kNA, ceil_div(N - n0, 32));  // 32-col atoms with a column < N
     const int64_t b_begin = brp[pa], b_end = brp[pb];
     const int pw = warp;
-    uint4 cur = make_uint4(0, 0, 0, 0), nxt = make_uint4(0, 0, 0, 0);
-    uint64_t cs0 = 0, cs1 = 0, ns0 = 0, ns1 = 0;
-    auto load_chunk = [&](int64_t base, uint4& r, uint64_t& s0, uint64_t& s1) {
-      const int64_t bl = base + lane;
-      if (bl < b_end) {
-        r = __ldg(reinterpret_cast<const uint4*>(prm.ac + bl * 16) + pw);
-        if (pw == 0) {
-          s0 = __ldg(prm.sp + bl);
-          s1 = __ldg(prm.sp + bl + 1);
-        }
-      }
-    };
-    if (b_begin < b_end) load_chunk(b_begin, cur, cs0, cs1);
+    const uint32_t Kr = (uint32_t)prm.K;
+    const int64_t ldb = prm.ldb;
+    const float* __restrict__ Bsrc = prm.B + n0;
+    const uint32_t* __restrict__ acp = prm.ac;
+    const uint64_t* __restrict__ spp = prm.sp;
+    const uint8_t* __restrict__ pk = prm.packed;
+    const int row = lane & 15;
     const uint32_t bt0 = smem_u32(btile0);
-    uint32_t i = 0;
-    for (int64_t base = b_begin; base < b_end; base += 32) {
-      if (base + 32 < b_end) load_chunk(base + 32, nxt, ns0, ns1);
-      const int cnt = (int)min((int64_t)32, b_end - base);
-      for (int j = 0; j < cnt; ++j, ++i) {
-        const int s = i % S;
-        const uint32_t ph = (i / S) & 1;
-        const uint32_t r0 = __shfl_sync(0xffffffffu, cur.x, j), r1 = __shfl_sync(0xffffffffu, cur.y, j);
-        const uint32_t r2 = __shfl_sync(0xffffffffu, cur.z, j), r3 = __shfl_sync(0xffffffffu, cur.w, j);
-        uint64_t s0 = 0, s1 = 0;
-        if (pw == 0) { s0 = __shfl_sync(0xffffffffu, cs0, j); s1 = __shfl_sync(0xffffffffu, cs1, j); }
+    // per-lane prefetch ring: block b_begin + pw + 4*(j + 8*chunk)
+    constexpr int kPf = 8;
+    uint32_t acur[kPf], anxt[kPf];
+    uint64_t scur = 0, snxt = 0;  // lane j < 8 (and j+8 < 16 for the +1) holds sp of block j of the chunk
+    auto prefetch = [&](int64_t first, uint32_t (&ar)[kPf], uint64_t& sv) {
+#pragma unroll
+      for (int j = 0; j < kPf; ++j) {
+        const int64_t bl = first + 4 * j;
+        ar[j] = bl < b_end ? __ldg(acp + bl * 16 + row) : Kr;
+      }
+      const int64_t bl = first + 4 * (lane & 7);
+      sv = 0;
+      if (lane < 16 && bl < b_end) sv = __ldg(spp + bl + (lane >> 3));
+    };
+    // lane-constant destination offsets (per 128-column tile t and row % 4) and column bounds
+    uint32_t doff[NT][4];
+    bool col_ok[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int c = lane + 32 * t;  // 16-B chunk along N
+      const int at = c >> 3;
+      const uint32_t g = (c >> 1) & 3;
+#pragma unroll
+      for (int rq = 0; rq < 4; ++rq) doff[t][rq] = at * 512 + ((g ^ rq) << 5) + ((c & 1) << 4);
+      col_ok[t] = (n0 + 4 * c) < N && at < na_eff;
+    }
+    int s = pw % S;
+    uint32_t ph = (pw / S) & 1;
+    int64_t first = b_begin + pw;
+    if (first < b_end) prefetch(first, acur, scur);
+    while (first < b_end) {
+      const int64_t nfirst = first + 4 * kPf;
+      if (nfirst < b_end) prefetch(nfirst, anxt, snxt);
+#pragma unroll
+      for (int j = 0; j < kPf; ++j) {
+        const int64_t b = first + 4 * j;
+        if (b >= b_end) break;
+        const uint64_t s0 = __shfl_sync(0xffffffffu, scur, j), s1 = __shfl_sync(0xffffffffu, scur, 8 + j);
         mbar_wait(&empty[s], ph ^ 1);
-        if (pw == 0 && lane == 0) {
+        if (lane == 0) {
+          trace_ev(prm, 0, (uint32_t)(b - b_begin));
           const uint32_t a_bytes = (uint32_t)(s1 - s0);
           mbar_expect_tx(&full_a[s], a_bytes);
-          bulk_g2s(araw0 + (size_t)s * kARawBytes, prm.packed + s0, a_bytes, &full_a[s], pol_a);
+          bulk_g2s(araw0 + (size_t)s * kARawBytes, pk + s0, a_bytes, &full_a[s], pol_a);
         }
-        const uint32_t bt = bt0 + s * L::kBTile + pw * L::kNA * 512;  // this warp's 4-row group
+        const uint32_t bt = bt0 + s * L::kBTile;
+        const uint32_t r = acur[j];
         if constexpr (GM == 0) {
+          const uint32_t r0 = __shfl_sync(0xffffffffu, r, 0), r1 = __shfl_sync(0xffffffffu, r, 1);
+          const uint32_t r2 = __shfl_sync(0xffffffffu, r, 2), r3 = __shfl_sync(0xffffffffu, r, 3);
+          const uint32_t r4 = __shfl_sync(0xffffffffu, r, 4), r5 = __shfl_sync(0xffffffffu, r, 5);
+          const uint32_t r6 = __shfl_sync(0xffffffffu, r, 6), r7 = __shfl_sync(0xffffffffu, r, 7);
+          const uint32_t r8 = __shfl_sync(0xffffffffu, r, 8), r9 = __shfl_sync(0xffffffffu, r, 9);
+          const uint32_t ra = __shfl_sync(0xffffffffu, r, 10), rb = __shfl_sync(0xffffffffu, r, 11);
+          const uint32_t rc = __shfl_sync(0xffffffffu, r, 12), rd = __shfl_sync(0xffffffffu, r, 13);
+          const uint32_t re = __shfl_sync(0xffffffffu, r, 14), rf = __shfl_sync(0xffffffffu, r, 15);
           if (lane == 0) {
-            mbar_expect_tx(&full_b[s], 4u * 128u * (uint32_t)na_eff);
-            uint8_t* btg = btile0 + (size_t)s * L::kBTile + pw * L::kNA * 512;
-            for (int a = 0; a < na_eff; ++a)
-              tma_gather4(btg + a * 512, &tmB, n0 + 32 * a, (int32_t)r0, (int32_t)r1, (int32_t)r2, (int32_t)r3,
-                          &full_b[s]);
+            mbar_expect_tx(&full_b[s], 16u * 128u * (uint32_t)na_eff);
+            uint8_t* btg = btile0 + (size_t)s * L::kBTile;
+            const uint32_t rr[16] = {r0, r1, r2, r3, r4, r5, r6, r7, r8, r9, ra, rb, rc, rd, re, rf};
+#pragma unroll
+            for (int g4 = 0; g4 < 4; ++g4)
+              for (int a = 0; a < na_eff; ++a)
+                tma_gather4(btg + (g4 * L::kNA + a) * 512, &tmB, n0 + 32 * a, (int32_t)rr[4 * g4],
+                            (int32_t)rr[4 * g4 + 1], (int32_t)rr[4 * g4 + 2], (int32_t)rr[4 * g4 + 3], &full_b[s]);
           }
         } else {
-          // lane copies 16-B chunk c = lane + 32 t of each of the 4 rows; destination follows the UMMA
-          // SWIZZLE_128B_BASE32B MN-major atom (4 rows x 128 B, 32-B granule g stored at g ^ row)
-          const uint32_t rows[4] = {r0, r1, r2, r3};
+          // lane copies 16-B chunk c = lane + 32 t (along N) of each of the 16 rows; destination in the UMMA
+          // SWIZZLE_128B_BASE32B MN-major atom: 4 rows x 128 B, 32-B granule g stored at g ^ (row % 4).
+          // Lane-constant parts (offsets per row%4, column bound) are hoisted out of the block loop.
 #pragma unroll
-          for (int rr = 0; rr < 4; ++rr) {
-            const bool real = rows[rr] < (uint32_t)prm.K;  // sentinel K -> zero fill
-            const float* src_row = prm.B + (int64_t)(real ? rows[rr] : 0) * prm.ldb + n0;
+          for (int rw = 0; rw < 16; ++rw) {
+            const uint32_t rk = __shfl_sync(0xffffffffu, r, rw);
+            const bool real = rk < Kr;  // sentinel K -> zero fill
+            const float* src = Bsrc + (int64_t)(real ? rk : 0) * ldb + 4 * lane;
+            const uint32_t rowb = bt + (rw >> 2) * (L::kNA * 512) + (rw & 3) * 128;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-              const int c = lane + 32 * t;  // 16-B chunk along N
-              const int a = c >> 3;         // atom
-              if (a < na_eff) {
-                const int g = (c >> 1) & 3, h = c & 1;
-                const uint32_t dst = bt + a * 512 + rr * 128 + ((g ^ rr) << 5) + (h << 4);
-                const bool inb = real && (n0 + 4 * c) < N;
-                cp_async16(dst, src_row + 4 * c, inb ? 16u : 0u);
+              if (t * 4 < na_eff) {
+                cp_async16(rowb + doff[t][rw & 3], src + 128 * t, (real && col_ok[t]) ? 16u : 0u);
               }
             }
           }
           cp_async_arrive_noinc(&full_b[s]);
         }
-        __syncwarp();
+        s += 4;
+        if (s >= S) { s -= S; ph ^= 1; }
       }
-      cur = nxt;
-      cs0 = ns0;
-      cs1 = ns1;
+#pragma unroll
+      for (int j = 0; j < kPf; ++j) acur[j] = anxt[j];
+      scur = snxt;
+      first = nfirst;
     }
-  } else if (warp == 4) {
-    // ---------------------------------------------------------------- decoder
-    uint32_t i = 0;
+  } else if (warp < kMmaWarp) {
+    // ---------------------------------------------------------------- decoders (block i -> warp 4 + i % 4)
+    // Lane l expands bits l and l+32 of each brick. All four patterns are loaded first, then
+    // the values, so the per-block latency is ~3 dependent shared loads.
+    const int dw = warp - kProdWarps;
     const int64_t b_begin = brp[pa], b_end = brp[pb];
-    for (int64_t b = b_begin; b < b_end; ++b, ++i) {
-      const int s = i % S;
-      const uint32_t ph = (i / S) & 1;
+    const uint32_t below = (1u << lane) - 1u;
+    int s = dw % S;
+    uint32_t ph = (dw / S) & 1;
+    for (int64_t b = b_begin + dw; b < b_end; b += kDecWarps) {
       mbar_wait(&full_a[s], ph);
+      if (lane == 0) trace_ev(prm, 1, (uint32_t)(b - b_begin));
       const uint8_t* blk = araw0 + (size_t)s * kARawBytes;
       float* tile = reinterpret_cast<float*>(atile0 + (size_t)s * kATileBytes);
       const uint32_t cp = *reinterpret_cast<const uint32_t*>(blk);  // colPtr[0..3]
@@ -255,30 +303,40 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       const uint32_t hdr = (5 + nbr + 7) & ~7u;
       const uint64_t* pats = reinterpret_cast<const uint64_t*>(blk + hdr);
       const float* vals = reinterpret_cast<const float*>(blk + hdr + 8 * nbr);
-      const uint32_t below = (1u << lane) - 1u;
-      uint32_t off = 0;
+      uint64_t pt[4];
 #pragma unroll
-      for (int bc = 0; bc < 4; ++bc) {
+      for (int bc = 0; bc < 4; ++bc) {  // TM = 16: at most one brick per brick column
         const uint32_t k0 = (cp >> (8 * bc)) & 0xFF;
         const uint32_t k1 = bc < 3 ? (cp >> (8 * (bc + 1))) & 0xFF : nbr;
-        float v0 = 0.f, v1 = 0.f;
-        if (k1 > k0) {  // TM = 16: at most one brick per brick column
-          const uint64_t pt = pats[k0];
-          const uint32_t lo = (uint32_t)pt, hi = (uint32_t)(pt >> 32);
-          if ((lo >> lane) & 1u) v0 = vals[off + __popc(lo & below)];
-          if ((hi >> lane) & 1u) v1 = vals[off + __popc(lo) + __popc(hi & below)];
-          off += __popc(lo) + __popc(hi);
-        }
-        tile[bc * 64 + lane] = to_tf32_rna(v0);
-        tile[bc * 64 + 32 + lane] = to_tf32_rna(v1);
+        pt[bc] = k1 > k0 ? pats[k0] : 0ull;
+      }
+      uint32_t off = 0;
+      float v0[4], v1[4];
+#pragma unroll
+      for (int bc = 0; bc < 4; ++bc) {
+        const uint32_t lo = (uint32_t)pt[bc], hi = (uint32_t)(pt[bc] >> 32);
+        v0[bc] = ((lo >> lane) & 1u) ? vals[off + __popc(lo & below)] : 0.f;
+        v1[bc] = ((hi >> lane) & 1u) ? vals[off + __popc(lo) + __popc(hi & below)] : 0.f;
+        off += __popc(lo) + __popc(hi);
+      }
+#pragma unroll
+      for (int bc = 0; bc < 4; ++bc) {
+        tile[bc * 64 + lane] = to_tf32_rna(v0[bc]);
+        tile[bc * 64 + 32 + lane] = to_tf32_rna(v1[bc]);
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&dec[s]);
+      if (lane == 0) {
+        trace_ev(prm, 2, (uint32_t)(b - b_begin));
+        mbar_arrive(&dec[s]);
+      }
+      s += kDecWarps;
+      if (s >= S) { s -= S; ph ^= 1; }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     // ---------------------------------------------------------------- MMA issuer (one thread)
-    uint32_t i = 0, pc = 0;
+    uint32_t i = 0, pc = 0, ph = 0;
+    int st = 0;
     const uint32_t bt0 = smem_u32(btile0), at0 = smem_u32(atile0);
     PanelCursor cursor(brp, pa, pb, lane);
     int64_t p;
@@ -290,12 +348,13 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       tc_fence_after();
       const uint32_t dcol = tbase + slot * NT * 16;
       for (uint32_t b = bb; b < be; ++b, ++i) {
-        const int s = i % S;
-        const uint32_t ph = (i / S) & 1;
+        const int s = st;
         mbar_wait(&full_b[s], ph);
+        if (lane == 0) trace_ev(prm, 3, i);
         mbar_wait(&dec[s], ph);
         tc_fence_after();
         if (lane == 0) {
+          trace_ev(prm, 4, i);
           const uint32_t bt = bt0 + s * L::kBTile, at = at0 + s * kATileBytes;
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
@@ -309,15 +368,16 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
           umma_commit(&empty[s]);
         }
         __syncwarp();
+        if (++st == S) { st = 0; ph ^= 1; }
       }
       if (lane == 0) umma_commit(&tfull[slot]);
       __syncwarp();
       ++pc;
     }
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 6..9)
+    // ---------------------------------------------------------------- epilogue (warps 9..12)
     const int qd = warp & 3;            // TMEM lane quadrant accessible to this warp
-    const int et = tid - 192;           // 0..127
+    const int et = tid - 32 * kEpiWarp0;  // 0..127
     const int64_t ncols = min((int64_t)128 * NT, N - n0);
     uint32_t pc = 0;
     PanelCursor cursor(brp, pa, pb, lane);
@@ -333,6 +393,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       }
       const uint32_t slot = pc & 1;
       mbar_wait(&tfull[slot], (pc >> 1) & 1);
+      if (et == 0) trace_ev(prm, 5, pc);
       tc_fence_after();
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
@@ -355,7 +416,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tbase, tmem_cols);
   }
@@ -395,6 +456,10 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   const int budget = 227 * 1024 - 1024 /*alignment*/ - 512 /*barriers, misc*/;
   int stages = budget / L::kStage;
   if (stages > kMaxStages) stages = kMaxStages;
+  // producer warp w (and decoder warp w) owns blocks i = w mod 4; with S a multiple of 4 every stage is
+  // only ever filled by one warp, so a warp running ahead cannot alias an mbarrier phase.
+  stages -= stages % kProdWarps;
+  static_assert(kProdWarps == kDecWarps, "stage ownership assumes equal producer/decoder warp counts");
   const size_t smem = 1024 + (size_t)stages * L::kStage + (4 * stages + 4) * 8 + 64;
   static bool attr_set = false;
   if (!attr_set) {
@@ -402,11 +467,27 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     if (e != cudaSuccess) return cuda_status(e);
     attr_set = true;
   }
-  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, B, h->K, ldb, n0, stages};
+  static const char* trace_path = getenv("HRPB_TRACE");
+  long long* trace = nullptr;
+  if (trace_path) {
+    trace = (long long*)dalloc(6 * kTraceN * sizeof(long long), s);
+    cudaMemsetAsync(trace, 0, 6 * kTraceN * sizeof(long long), s);
+  }
+  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, B, h->K, ldb, n0, stages, trace};
   int grid = num_sms();
   if ((int64_t)grid > h->P) grid = (int)(h->P > 0 ? h->P : 1);
   k_spmm<NT, GM><<<grid, kSpmmThreads, smem, s>>>(tm, prm);
   note_launch();
+  if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)
+    static long long host[6 * kTraceN];
+    cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (FILE* f = fopen(trace_path, "wb")) {
+      fwrite(host, sizeof(host), 1, f);
+      fclose(f);
+    }
+    dfree(trace, s);
+  }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);
 }

@@ -1,0 +1,20 @@
+"""Analyse an HRPB_TRACE dump (CTA 0 per-block clock64 events of k_spmm)."""
+import sys
+import numpy as np
+
+N = 1024
+t = np.fromfile(sys.argv[1], dtype=np.int64).reshape(6, N).astype(np.float64)
+valid = (t[0] > 0) & (t[4] > 0)
+n = int(valid.sum())
+t0 = t[0][valid].min()
+ev = {k: t[i][:n] - t0 for i, k in enumerate(["issue", "a_ready", "dec_done", "b_ready", "mma", "tfull"])}
+print(f"blocks traced: {n}")
+for a, b in [("issue", "a_ready"), ("a_ready", "dec_done"), ("issue", "b_ready"), ("dec_done", "mma"),
+             ("b_ready", "mma"), ("issue", "mma")]:
+    d = ev[b] - ev[a]
+    print(f"{a:>9s} -> {b:<9s}: median {np.median(d):8.0f}  p90 {np.percentile(d, 90):8.0f} cycles")
+iss = np.diff(ev["issue"])
+print(f"issue interval median {np.median(iss):.0f} cycles; mma interval median {np.median(np.diff(ev['mma'])):.0f}")
+print("first 24 blocks (cycles rel. to first issue):")
+for i in range(min(24, n)):
+    print(i, " ".join(f"{ev[k][i]:9.0f}" for k in ["issue", "a_ready", "dec_done", "b_ready", "mma"]))
