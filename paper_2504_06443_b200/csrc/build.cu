@@ -32,6 +32,10 @@ constexpr int kSmallCap = 2048;      // entries per panel handled in shared memo
 constexpr int kSpanWords = 512;      // bitmap ranking when the panel's column span <= 16384
 constexpr int kBigThreads = 512;
 constexpr int kEmitThreads = 128;
+constexpr int kWarpCap = 256;        // entries per panel handled by one warp (no CTA barriers)
+constexpr int kWarpPer = kWarpCap / 32;
+constexpr int kWarpSpanWords = 256;  // warp bitmap ranking when the column span < 8192 (bitmap + prefix = s_keys)
+constexpr int kWarpsPerCta = 8;
 
 // ------------------------------------------------------------------ block-wide helpers
 template <int NT>
@@ -126,8 +130,284 @@ __device__ __forceinline__ int64_t pat_base(int64_t e0, int64_t p, int nbk, int 
   return e0 * nbk / tk + 2 * p * nbk;
 }
 
-// ------------------------------------------------------------------ pass A, panels with <= kSmallCap entries
-// One CTA per panel ("for row_panel in rowPanels_chunk"). q[e] = rank of col_idx[e] among the
+// ------------------------------------------------------------------ warp-level helpers
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t* total) {
+  const int lane = threadIdx.x & 31;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (total) *total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+// Warp-wide version of load_panel_rows (no CTA barrier): clamped, monotone-repaired row pointers.
+__device__ __forceinline__ void warp_panel_rows(const int64_t* __restrict__ rp, int64_t M, int64_t nnz, int tm,
+                                                int64_t p, int64_t* s_rp, uint32_t* status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r0 = p * tm;
+  const int nrows = (int)min((int64_t)tm, M - r0);
+  int64_t carry_raw = 0, carry_v = 0;
+  bool bad = false;
+  for (int base = 0; base <= nrows; base += 32) {
+    const int i = base + lane;
+    const int64_t raw = i <= nrows ? rp[r0 + i] : INT64_MAX;
+    int64_t prev = __shfl_up_sync(0xffffffffu, raw, 1);
+    if (lane == 0) prev = base == 0 ? raw : carry_raw;
+    if (i <= nrows && raw < prev) bad = true;
+    int64_t v = i <= nrows ? (raw < 0 ? 0 : (raw > nnz ? nnz : raw)) : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v = max(v, y);
+    }
+    v = max(v, carry_v);
+    if (i <= nrows) s_rp[i] = v;
+    carry_raw = __shfl_sync(0xffffffffu, raw, 31);
+    carry_v = __shfl_sync(0xffffffffu, v, 31);
+  }
+  if (__any_sync(0xffffffffu, bad) && status && lane == 0) atomicOr(status, ST_RP_MONO);
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------ pass A, panels with <= kWarpCap entries
+// One warp per panel, no CTA barriers: entries live in registers (kWarpPer per lane), ranks come from a
+// per-warp bitmap (column span <= 16384) or a warp bitonic sort; patterns via 32-bit shared atomics.
+// Larger panels are appended to the mid list (k_count).
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp(
+    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t M, int64_t K, int64_t nnz, int tm,
+    int tk, int64_t P, uint32_t* __restrict__ q, uint32_t* __restrict__ nact_out, uint32_t* __restrict__ nblk_out,
+    uint32_t* __restrict__ pbytes_out, uint64_t* __restrict__ gpat, uint32_t* __restrict__ midlist,
+    uint32_t* __restrict__ nmid, uint32_t* status, int warp_smem_bytes) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t p = (int64_t)blockIdx.x * kWarpsPerCta + wid;
+  if (p >= P) return;
+  uint8_t* my = dsm + (size_t)wid * warp_smem_bytes;
+  uint64_t* s_keys = reinterpret_cast<uint64_t*>(my);                    // [kWarpCap] / bitmap + prefix
+  uint32_t* s_qb = reinterpret_cast<uint32_t*>(s_keys + kWarpCap);       // [kWarpCap] rank by index
+  int64_t* s_rp = reinterpret_cast<int64_t*>(s_qb + kWarpCap);           // [tm + 1]
+  unsigned long long* s_pat = reinterpret_cast<unsigned long long*>(s_rp + ((tm + 2) & ~1));
+  warp_panel_rows(rp, M, nnz, tm, p, s_rp, status);
+  const int nrows = (int)min((int64_t)tm, M - p * tm);
+  const int64_t e0 = s_rp[0];
+  const int64_t E64 = s_rp[nrows] - e0;
+  if (E64 > kWarpCap) {
+    if (lane == 0) midlist[atomicAdd(nmid, 1u)] = (uint32_t)p;
+    return;
+  }
+  static_assert(2 * kWarpSpanWords * 4 <= kWarpCap * 8, "bitmap + prefix must fit in s_keys");
+  const int E = (int)E64;
+  if (E == 0) {
+    if (lane == 0) { nact_out[p] = 0; nblk_out[p] = 0; pbytes_out[p] = 0; }
+    return;
+  }
+  uint32_t col[kWarpPer];
+  int rowv[kWarpPer];
+  int32_t mn = INT32_MAX, mx = INT32_MIN;
+  bool bad_range = false, bad_order = false;
+#pragma unroll
+  for (int k = 0; k < kWarpPer; ++k) {
+    const int idx = lane + 32 * k;
+    col[k] = 0;
+    rowv[k] = 0;
+    if (idx < E) {
+      const int64_t e = e0 + idx;
+      const int32_t c = ci[e];
+      const int r = row_of(s_rp, nrows, e);
+      col[k] = (uint32_t)c;
+      rowv[k] = r;
+      bad_range |= c < 0 || c >= K;
+      if (e > s_rp[r] && ci[e - 1] >= c) bad_order = true;
+      mn = min(mn, c);
+      mx = max(mx, c);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad_range) && lane == 0) atomicOr(status, ST_COL_RANGE);
+  if (__any_sync(0xffffffffu, bad_order) && lane == 0) atomicOr(status, ST_COL_ORDER);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  uint32_t qv[kWarpPer];
+  uint32_t nact = 0;
+  if ((int64_t)mx - (int64_t)mn < 32 * kWarpSpanWords) {
+    uint32_t* bm = reinterpret_cast<uint32_t*>(s_keys);
+    uint32_t* pre = bm + kWarpSpanWords;
+    constexpr int kW = kWarpSpanWords / 32;
+#pragma unroll
+    for (int i = 0; i < kW; ++i) bm[lane * kW + i] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kWarpPer; ++k)
+      if (lane + 32 * k < E) {
+        const uint32_t off = col[k] - (uint32_t)mn;
+        atomicOr(&bm[off >> 5], 1u << (off & 31));
+      }
+    __syncwarp();
+    uint32_t cnt[kW], sum = 0;
+#pragma unroll
+    for (int i = 0; i < kW; ++i) { cnt[i] = __popc(bm[lane * kW + i]); sum += cnt[i]; }
+    uint32_t run = warp_excl_scan(sum, &nact);
+#pragma unroll
+    for (int i = 0; i < kW; ++i) { pre[lane * kW + i] = run; run += cnt[i]; }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kWarpPer; ++k) {
+      const uint32_t off = col[k] - (uint32_t)mn;
+      const uint32_t w = (off >> 5) & (kWarpSpanWords - 1), b = off & 31;
+      qv[k] = pre[w] + __popc(bm[w] & ((1u << b) - 1u));
+    }
+  } else {
+    int n = 32;
+    while (n < E) n <<= 1;
+#pragma unroll
+    for (int k = 0; k < kWarpPer; ++k) {
+      const int idx = lane + 32 * k;
+      if (idx < n) s_keys[idx] = idx < E ? ((uint64_t)col[k] << 32) | (uint32_t)idx : ~0ull;
+    }
+    __syncwarp();
+    for (int kk = 2; kk <= n; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < n; i += 32) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const uint64_t a = s_keys[i], b = s_keys[ixj];
+            if ((a > b) == ((i & kk) == 0)) { s_keys[i] = b; s_keys[ixj] = a; }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    const int per = n / 32;
+    const int beg = lane * per;
+    uint32_t sum = 0;
+    for (int i = beg; i < beg + per && i < E; ++i)
+      if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++sum;
+    uint32_t run = warp_excl_scan(sum, &nact);
+    for (int i = beg; i < beg + per && i < E; ++i) {
+      if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++run;
+      s_qb[(uint32_t)s_keys[i]] = run - 1;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kWarpPer; ++k) qv[k] = lane + 32 * k < E ? s_qb[lane + 32 * k] : 0u;
+  }
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const uint32_t nblk = (nact + tk - 1) / tk;
+  const int nbricks = (int)nblk * nbk;
+  for (int i = lane; i < nbricks; i += 32) s_pat[i] = 0ull;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < kWarpPer; ++k) {
+    if (lane + 32 * k < E) {
+      const uint32_t qq = qv[k], r = (uint32_t)rowv[k];
+      const uint32_t j = qq / tk, lc = qq % tk;
+      const int bit = (int)(((r & 15) << 2) | (lc & 3));
+      uint32_t* half = reinterpret_cast<uint32_t*>(&s_pat[j * nbk + (lc >> 2) * nbrow + (r >> 4)]) + (bit >> 5);
+      atomicOr(half, 1u << (bit & 31));
+      q[e0 + lane + 32 * k] = qq;
+    }
+  }
+  __syncwarp();
+  uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
+  for (int i = lane; i < nbricks; i += 32) gp[i] = s_pat[i];
+  uint32_t bytes = 0;
+  for (uint32_t j = lane; j < nblk; j += 32) {
+    uint32_t nbr = 0, nz = 0;
+    for (int i = 0; i < nbk; ++i) { const uint64_t v = s_pat[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
+    bytes += block_bytes(nbc, nbr, nz);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+  if (lane == 0) { nact_out[p] = nact; nblk_out[p] = nblk; pbytes_out[p] = bytes; }
+}
+
+// ------------------------------------------------------------------ pass B, panels with <= kWarpCap entries
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_emit_warp(
+    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const float* __restrict__ vals, int64_t M,
+    int64_t K, int64_t nnz, int tm, int tk, int64_t P, const uint32_t* __restrict__ q,
+    const uint32_t* __restrict__ nact_in, const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff,
+    const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac, uint64_t* __restrict__ sp,
+    uint8_t* __restrict__ packed, int warp_smem_bytes) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t p = (int64_t)blockIdx.x * kWarpsPerCta + wid;
+  if (p >= P) return;
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const int64_t r0 = p * tm;
+  const int nrows = (int)min((int64_t)tm, M - r0);
+  {
+    int64_t a = rp[r0], b = rp[r0 + nrows];
+    a = a < 0 ? 0 : (a > nnz ? nnz : a);
+    b = b < 0 ? 0 : (b > nnz ? nnz : b);
+    if (b - a > kWarpCap) return;  // emitted by k_emit (CTA)
+  }
+  const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0;
+  if (nblk == 0) return;
+  uint8_t* my = dsm + (size_t)wid * warp_smem_bytes;
+  int64_t* s_rp = reinterpret_cast<int64_t*>(my);
+  uint64_t* s_vbase = reinterpret_cast<uint64_t*>(s_rp + ((tm + 2) & ~1));  // [kWarpCap / tk]
+  uint64_t* s_pt = s_vbase + kWarpCap / 16;                                // [kWarpCap / tk * nbk]
+  warp_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);
+  const uint32_t nact = nact_in[p];
+  const int64_t e0 = s_rp[0], e1 = s_rp[nrows];
+  const uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
+  for (int i = lane; i < (int)nblk * nbk; i += 32) s_pt[i] = gp[i];
+  __syncwarp();
+  // one lane per block (nblk <= kWarpCap / tk <= 32)
+  uint32_t nbr = 0, nz = 0, size = 0;
+  const uint32_t j = lane;
+  if (j < nblk) {
+    for (int i = 0; i < nbk; ++i) { const uint64_t v = s_pt[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
+    size = block_bytes(nbc, nbr, nz);
+  }
+  const uint64_t off = poff[p] + warp_excl_scan(size, nullptr);
+  if (j < nblk) {
+    sp[b0 + j] = off;
+    uint8_t* blk = packed + off;
+    const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+    uint32_t k = 0;
+    blk[0] = 0;
+    for (int bc = 0; bc < nbc; ++bc) {
+      for (int br = 0; br < nbrow; ++br) {
+        const uint64_t v = s_pt[j * nbk + bc * nbrow + br];
+        if (!v) continue;
+        blk[nbc + 1 + k] = (uint8_t)br;
+        reinterpret_cast<uint64_t*>(blk + hdr)[k] = v;
+        ++k;
+      }
+      blk[bc + 1] = (uint8_t)k;
+    }
+    for (uint32_t i = nbc + 1 + nbr; i < hdr; ++i) blk[i] = 0;
+    for (uint32_t i = hdr + 8 * nbr + 4 * nz; i < size; ++i) blk[i] = 0;
+    s_vbase[j] = off + hdr + 8 * nbr;
+  }
+  for (int64_t t = nact + lane; t < (int64_t)nblk * tk; t += 32) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
+  __syncwarp();
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    const uint32_t qq = q[e];
+    const int32_t c = ci[e];
+    const float v = vals[e];
+    if (qq >= nact) continue;
+    const int r = row_of(s_rp, nrows, e);
+    const uint32_t jb = qq / tk, lc = qq % tk;
+    ac[((int64_t)b0 + jb) * tk + lc] = (uint32_t)c;
+    const int bit = ((r & 15) << 2) | (lc & 3);
+    const int mine = (lc >> 2) * nbrow + (r >> 4);
+    const uint64_t* pt = s_pt + jb * nbk;
+    uint32_t o = 0;
+    for (int i = 0; i < mine; ++i) o += __popcll(pt[i]);
+    o += __popcll(pt[mine] & ((1ull << bit) - 1ull));
+    reinterpret_cast<float*>(packed + s_vbase[jb])[o] = v;
+  }
+}
+
+// ------------------------------------------------------------------ pass A, kWarpCap < entries <= kSmallCap
+// One CTA per listed panel ("for row_panel in rowPanels_chunk"). q[e] = rank of col_idx[e] among the
 // panel's distinct columns (ascending, R23; "active_cols = uniq(cols[...])"), nblk = ceil(nact/TK)
 // (R1), brick patterns (bit = (r % 16) * 4 + q % 4, R3) and the panel's total block bytes.
 __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restrict__ rp,
@@ -136,7 +416,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
                                                         uint32_t* __restrict__ nact_out,
                                                         uint32_t* __restrict__ nblk_out,
                                                         uint32_t* __restrict__ pbytes_out,
-                                                        uint64_t* __restrict__ gpat, uint32_t* __restrict__ biglist,
+                                                        uint64_t* __restrict__ gpat,
+                                                        const uint32_t* __restrict__ midlist,
+                                                        const uint32_t* __restrict__ nmid,
+                                                        uint32_t* __restrict__ biglist,
                                                         uint32_t* __restrict__ nbig, uint32_t* status) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ int64_t s_rp[129];
@@ -148,18 +431,16 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
   uint8_t* s_row = reinterpret_cast<uint8_t*>(s_q + kSmallCap);        // [kSmallCap]
   unsigned long long* s_pat = reinterpret_cast<unsigned long long*>(s_row + kSmallCap);  // [cap bricks]
 
-  const int64_t p = blockIdx.x;
+  const uint32_t count = *nmid;
+  for (uint32_t t = blockIdx.x; t < count; t += gridDim.x) {
+  const int64_t p = midlist[t];
   load_panel_rows(rp, M, nnz, tm, p, s_rp, status);
   const int nrows = (int)min((int64_t)tm, M - p * tm);
   const int64_t e0 = s_rp[0];
   const int E = (int)min((int64_t)kSmallCap + 1, s_rp[nrows] - e0);
   if (E > kSmallCap) {  // CTA-uniform: handled by k_count_big
     if (threadIdx.x == 0) biglist[atomicAdd(nbig, 1u)] = (uint32_t)p;
-    return;
-  }
-  if (E == 0) {
-    if (threadIdx.x == 0) { nact_out[p] = 0; nblk_out[p] = 0; pbytes_out[p] = 0; }
-    return;
+    continue;
   }
   // entries -> shared memory (local row, column)
   int32_t mn = INT32_MAX, mx = INT32_MIN;
@@ -259,6 +540,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
   uint32_t total;
   block_excl_scan<kSmallThreads>(bytes, &total, s_scan);
   if (threadIdx.x == 0) { nact_out[p] = nact; nblk_out[p] = nblk; pbytes_out[p] = total; }
+  }  // panel loop
 }
 
 // ------------------------------------------------------------------ pass A, panels with > kSmallCap entries
@@ -446,8 +728,8 @@ static void scan_excl(const uint32_t* in, int64_t n, OutT* out, uint64_t* part, 
   note_launch(3);
 }
 
-// ------------------------------------------------------------------ pass B: emit the HRPB arrays
-// One CTA per panel. Block j of panel p is global block b0 + j (b0 = blockedRowPtr[p]); its byte offset
+// ------------------------------------------------------------------ pass B (CTA), panels with > kWarpCap entries
+// One CTA per listed panel. Block j of panel p is global block b0 + j (b0 = blockedRowPtr[p]); its byte offset
 // is the panel offset plus the in-panel exclusive scan of block sizes (sizePtr). Header,
 // patterns and values follow the HRPB-v1 layout; value destination = values base + popcount of the
 // earlier bricks + popcount of the lower bits of its own brick.
@@ -458,14 +740,18 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int64_t* __restrict
                                                       const uint32_t* __restrict__ brp,
                                                       const uint64_t* __restrict__ poff,
                                                       const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac,
-                                                      uint64_t* __restrict__ sp, uint8_t* __restrict__ packed) {
+                                                      uint64_t* __restrict__ sp, uint8_t* __restrict__ packed,
+                                                      const uint32_t* __restrict__ midlist,
+                                                      const uint32_t* __restrict__ nmid) {
   __shared__ int64_t s_rp[129];
   __shared__ uint32_t s_scan[kEmitThreads / 32 + 1];
   __shared__ uint64_t s_vbase[kEmitThreads];     // byte offset of each block's values (single-chunk panels)
   __shared__ uint64_t s_pt[kEmitThreads * 4];    // patterns (single-chunk panels with nbk <= 4)
-  const int64_t p = blockIdx.x;
+  const uint32_t count = *nmid;
+  for (uint32_t tt = blockIdx.x; tt < count; tt += gridDim.x) {
+  const int64_t p = midlist[tt];
   const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0;
-  if (nblk == 0) return;
+  if (nblk == 0) continue;
   const uint32_t nact = nact_in[p];
   load_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);
   const int nrows = (int)min((int64_t)tm, M - p * tm);
@@ -546,6 +832,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int64_t* __restrict
     }
     reinterpret_cast<float*>(packed + vb)[off] = v;
   }
+  }  // panel loop
 }
 
 __global__ void k_finalize(const int64_t* __restrict__ rp, int64_t M, int64_t nnz, int64_t P,
@@ -586,7 +873,8 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   uint32_t* pbytes = cnt + 2 * (P + 1);
   uint64_t* poff = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t), s);
   uint64_t* gpat = (uint64_t*)dalloc(pat_cap * sizeof(uint64_t), s);
-  uint32_t* biglist = (uint32_t*)dalloc((P + 1) * sizeof(uint32_t), s);
+  uint32_t* biglist = (uint32_t*)dalloc(2 * (P + 1) * sizeof(uint32_t), s);  // big | mid panel lists
+  uint32_t* midlist = biglist + (P + 1);
   const int64_t nparts = ceil_div(P + 1, kScanChunk) + 1;
   uint64_t* part = (uint64_t*)dalloc(nparts * sizeof(uint64_t), s);
   uint64_t* info = (uint64_t*)dalloc(4 * sizeof(uint64_t), s);  // [3] = status word | hub count
@@ -602,7 +890,8 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   if (st == HRPB_SUCCESS) {
     uint32_t* status = reinterpret_cast<uint32_t*>(info + 3);
     uint32_t* nbig = status + 1;
-    cudaMemsetAsync(status, 0, 2 * sizeof(uint32_t), s);
+    uint32_t* nmid = reinterpret_cast<uint32_t*>(info + 2);  // info[2] is rewritten by k_finalize
+    cudaMemsetAsync(info + 2, 0, 2 * sizeof(uint64_t), s);
     const size_t count_smem =
         (size_t)kSmallCap * (8 + 4 + 4 + 1) + (size_t)ceil_div(kSmallCap, tk) * nbk * sizeof(uint64_t);
     static bool attr = false;
@@ -610,19 +899,34 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
       cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
+    const int wsm_count = (int)align_up(kWarpCap * 12 + ((tm + 2) & ~1) * 8 + (kWarpCap / tk) * nbk * 8, 16);
+    const int wsm_emit = (int)align_up(((tm + 2) & ~1) * 8 + (kWarpCap / 16) * 8 + (kWarpCap / tk) * nbk * 8, 16);
+    const unsigned wgrid = (unsigned)ceil_div(P, kWarpsPerCta);
+    static bool wattr = false;
+    if (!wattr) {
+      cudaFuncSetAttribute(k_count_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_emit_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      wattr = true;
+    }
+    const int mid_ctas = 8 * num_sms();
     if (P > 0) {  // pass A
-      k_count<<<(unsigned)P, kSmallThreads, count_smem, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
-                                                            pbytes, gpat, biglist, nbig, status);
+      k_count_warp<<<wgrid, 32 * kWarpsPerCta, (size_t)wsm_count * kWarpsPerCta, s>>>(
+          row_ptr, col_idx, M, K, nnz, tm, tk, P, q, nact, nblk, pbytes, gpat, midlist, nmid, status, wsm_count);
+      k_count<<<mid_ctas, kSmallThreads, count_smem, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
+                                                          pbytes, gpat, midlist, nmid, biglist, nbig, status);
       k_count_big<<<big_ctas, kBigThreads, 0, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk, pbytes, gpat,
                                                     biglist, nbig, bigscr, words, status);
-      note_launch(2);
+      note_launch(3);
     }
     scan_excl<uint32_t>(nblk, P, h->brp, part, s);  // B2: blockedRowPtr
     scan_excl<uint64_t>(pbytes, P, poff, part, s);  // B4 (panel level): byte offset of each panel
     if (P > 0) {                                    // pass B
-      k_emit<<<(unsigned)P, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp, poff,
-                                                  gpat, h->ac, h->sp, h->packed);
-      note_launch();
+      k_emit_warp<<<wgrid, 32 * kWarpsPerCta, (size_t)wsm_emit * kWarpsPerCta, s>>>(
+          row_ptr, col_idx, values, M, K, nnz, tm, tk, P, q, nact, h->brp, poff, gpat, h->ac, h->sp, h->packed,
+          wsm_emit);
+      k_emit<<<mid_ctas, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp, poff,
+                                               gpat, h->ac, h->sp, h->packed, midlist, nmid);
+      note_launch(2);
     }
     k_finalize<<<1, 1, 0, s>>>(row_ptr, M, nnz, P, h->brp, poff, h->sp, status, info);
     note_launch();
