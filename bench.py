@@ -131,24 +131,22 @@ def measure_tf32_peak(torch):
     return 2 * 8192 ** 3 / best / 1e12
 
 
-def cpu_baseline_oracle(rp, ci, vals, B, target_s=10.0, cap_s=30.0):
-    """Oracle CSR SpMM (FP64 accumulate, fp32 out, OpenMP over rows) on the host cores; bounded sample."""
+def cpu_baseline_oracle(rp, ci, vals, B, target_s=12.0, cap_s=30.0):
+    """Oracle CSR SpMM (FP64 accumulate, fp32 out, OpenMP over rows) on the host cores; bounded sample:
+    passes over the whole slab repeat until ~target_s seconds of CPU work have run (cap cap_s)."""
     import oracle
     M = rp.shape[0] - 1
-    probe = max(1, M // 64)
-    t = time.perf_counter()
-    _, th = oracle.csr_spmm_f32out(M, rp, ci, vals, B, 0, probe)
-    per_row = (time.perf_counter() - t) / probe
-    rows = int(min(M, max(probe, target_s / max(per_row, 1e-12))))
-    reps = 1
-    if rows == M:
-        reps = max(1, int(target_s / max(per_row * M, 1e-9)))
-        reps = min(reps, max(1, int(cap_s / max(per_row * M, 1e-9))))
+    rows = M
     out = np.empty((rows, B.shape[1]), np.float32)
+    oracle.csr_spmm_f32out(M, rp, ci, vals, B, 0, rows, out=out)  # first touch / thread start-up
+    reps, th = 0, 1
     t = time.perf_counter()
-    for _ in range(reps):
+    while True:
         _, th = oracle.csr_spmm_f32out(M, rp, ci, vals, B, 0, rows, out=out)
-    dt = time.perf_counter() - t
+        reps += 1
+        dt = time.perf_counter() - t
+        if dt >= target_s or dt * (reps + 1) / reps > cap_s:
+            break
     nnz_s = int(rp[rows] - rp[0])
     gf = 2.0 * nnz_s * B.shape[1] * reps / dt / 1e9
     return {"value": round(gf, 3), "unit": UNIT, "cores": int(th), "kind": "oracle",
