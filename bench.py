@@ -238,7 +238,7 @@ def run_ours(args, rank, world, local_rank):
     def step(evs=None):
         if evs is not None:
             evs[0].record(stream)
-        A = hp.build(rp_d, ci_d, v_d, M0, K0)
+        A = hp.build(rp_d, ci_d, v_d, M0, K0, tm=args.tm)
         if evs is not None:
             evs[1].record(stream)
         hp.spmm(A, B_d, out=C_d)
@@ -256,7 +256,7 @@ def run_ours(args, rank, world, local_rank):
     brp, ac, sp, packed_h = A.to_host()
     NB, P, packed = A.num_blocks, A.num_panels, A.packed_bytes
     sum_nact = int(np.count_nonzero(ac != K0))
-    bricks = int(packed_h[sp[:-1].astype(np.int64) + 4].astype(np.int64).sum())  # colPtr[4] = nbr per block
+    bricks = int(packed_h[sp[:-1].astype(np.int64) + 4].astype(np.int64).sum())  # colPtr[4] = nbr per block (TK=16)
     alpha = nnz / max(1, 64 * bricks)  # brick density
     A.free()
     uniq = int(np.count_nonzero(np.bincount(ci, minlength=K0)))
@@ -298,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     rp_h, ci_h, v_h, Bp_h = pin(rp), pin(ci), pin(vals), pin(B_h)
     Cp_h = torch.empty((M0, NCOL), dtype=torch.float32).pin_memory()
-    hp.build_spmm_host(rp_h, ci_h, v_h, Bp_h, M0, K0, out=Cp_h)  # warm
+    hp.build_spmm_host(rp_h, ci_h, v_h, Bp_h, M0, K0, out=Cp_h, tm=args.tm)  # warm
     e2e_steps = max(1, min(args.steps, 5))
     if world > 1:
         dist.barrier()
@@ -306,7 +306,7 @@ def run_ours(args, rank, world, local_rank):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(stream)
     for _ in range(e2e_steps):
-        hp.build_spmm_host(rp_h, ci_h, v_h, Bp_h, M0, K0, out=Cp_h)
+        hp.build_spmm_host(rp_h, ci_h, v_h, Bp_h, M0, K0, out=Cp_h, tm=args.tm)
     e.record(stream)
     torch.cuda.synchronize()
     e2e_ms = s.elapsed_time(e) / e2e_steps
@@ -337,7 +337,7 @@ def run_ours(args, rank, world, local_rank):
         tf32_peak = measure_tf32_peak(torch)
     except Exception:
         tf32_peak = None
-    exec_tflops = 2.0 * NB * 16 * 16 * (128 * ((NCOL + 127) // 128)) / (spmm_ms / 1e3) / 1e12
+    exec_tflops = 2.0 * NB * args.tm * 16 * (128 * ((NCOL + 127) // 128)) / (spmm_ms / 1e3) / 1e12
     roof = {"kernel": "hrpb::k_spmm<1>", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
             "unit": "GB/s", "frac": round(achieved / hbm, 4),
             "traffic": ncu_traffic("k_spmm", "c2a"),
@@ -365,7 +365,7 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": WORKLOAD, "nnz_per_rank": nnz, "N": NCOL, "num_blocks": NB, "panels": P,
                        "bricks": bricks, "alpha": round(alpha, 4), "sum_nact": sum_nact, "distinct_cols": uniq,
                        "parallelism": f"row-panel shards x{world}, B broadcast once (NCCL)",
-                       "step": "hrpb_build (CSR->HRPB) + hrpb_spmm",
+                       "step": "hrpb_build (CSR->HRPB) + hrpb_spmm", "TM": args.tm, "TK": 16,
                        "l2": "inputs larger than L2 (CSR 134 MB + B 512 MB per rank)",
                        "build_ms": round(build_ms, 4), "spmm_ms": round(spmm_ms, 4),
                        "spmm_only_gflops": round(flops / (spmm_ms / 1e3) / 1e9, 1),
@@ -388,6 +388,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tm", type=int, default=16, help="HRPB panel height TM (16 = paper default; 32/64 NEXT-1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank, world, local_rank = env_rank()

@@ -33,9 +33,9 @@ constexpr int kSpanWords = 512;      // bitmap ranking when the panel's column s
 constexpr int kBigThreads = 512;
 constexpr int kEmitThreads = 128;
 constexpr int kWarpCap = 256;        // entries per panel handled by one warp (no CTA barriers)
-constexpr int kWarpPer = kWarpCap / 32;
 constexpr int kWarpSpanWords = 256;  // warp bitmap ranking when the column span < 8192 (bitmap + prefix = s_keys)
 constexpr int kWarpsPerCta = 8;
+constexpr int kWarpCap2 = 1024;      // second warp pass (listed panels, bitmap ranking only)
 
 // ------------------------------------------------------------------ block-wide helpers
 template <int NT>
@@ -172,44 +172,43 @@ __device__ __forceinline__ void warp_panel_rows(const int64_t* __restrict__ rp, 
   __syncwarp();
 }
 
-// ------------------------------------------------------------------ pass A, panels with <= kWarpCap entries
-// One warp per panel, no CTA barriers: entries live in registers (kWarpPer per lane), ranks come from a
-// per-warp bitmap (column span <= 16384) or a warp bitonic sort; patterns via 32-bit shared atomics.
-// Larger panels are appended to the mid list (k_count).
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp(
-    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t M, int64_t K, int64_t nnz, int tm,
-    int tk, int64_t P, uint32_t* __restrict__ q, uint32_t* __restrict__ nact_out, uint32_t* __restrict__ nblk_out,
-    uint32_t* __restrict__ pbytes_out, uint64_t* __restrict__ gpat, uint32_t* __restrict__ midlist,
-    uint32_t* __restrict__ nmid, uint32_t* status, int warp_smem_bytes) {
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t p = (int64_t)blockIdx.x * kWarpsPerCta + wid;
-  if (p >= P) return;
-  uint8_t* my = dsm + (size_t)wid * warp_smem_bytes;
-  uint64_t* s_keys = reinterpret_cast<uint64_t*>(my);                    // [kWarpCap] / bitmap + prefix
-  uint32_t* s_qb = reinterpret_cast<uint32_t*>(s_keys + kWarpCap);       // [kWarpCap] rank by index
-  int64_t* s_rp = reinterpret_cast<int64_t*>(s_qb + kWarpCap);           // [tm + 1]
+// ------------------------------------------------------------------ pass A, warp per panel
+// One warp per panel, no CTA barriers: entries live in registers (CAP/32 per lane), ranks come from a
+// per-warp bitmap (column span < 8192) or, when SORT, a warp bitonic sort; patterns via 32-bit shared
+// atomics. Returns 0 when the panel was counted, 1 when it has more than CAP entries, 2 when its column
+// span needs the sort path and SORT is off.
+template <int CAP, bool SORT>
+__device__ __forceinline__ int count_panel_warp(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                int64_t M, int64_t K, int64_t nnz, int tm, int tk, int64_t p,
+                                                uint32_t* __restrict__ q, uint32_t* __restrict__ nact_out,
+                                                uint32_t* __restrict__ nblk_out, uint32_t* __restrict__ pbytes_out,
+                                                uint64_t* __restrict__ gpat, uint32_t* status, uint8_t* my,
+                                                int64_t& E_out) {
+  constexpr int PER = CAP / 32;
+  const int lane = threadIdx.x & 31;
+  uint64_t* s_keys = reinterpret_cast<uint64_t*>(my);                           // SORT ? [CAP] : bitmap 2 KB
+  constexpr int kKeyBytes = SORT ? CAP * 8 : 2 * kWarpSpanWords * 4;
+  uint32_t* s_qb = reinterpret_cast<uint32_t*>(my + kKeyBytes);                  // SORT ? [CAP] : none
+  int64_t* s_rp = reinterpret_cast<int64_t*>(my + kKeyBytes + (SORT ? CAP * 4 : 0));  // [tm + 1]
   unsigned long long* s_pat = reinterpret_cast<unsigned long long*>(s_rp + ((tm + 2) & ~1));
   warp_panel_rows(rp, M, nnz, tm, p, s_rp, status);
   const int nrows = (int)min((int64_t)tm, M - p * tm);
   const int64_t e0 = s_rp[0];
   const int64_t E64 = s_rp[nrows] - e0;
-  if (E64 > kWarpCap) {
-    if (lane == 0) midlist[atomicAdd(nmid, 1u)] = (uint32_t)p;
-    return;
-  }
-  static_assert(2 * kWarpSpanWords * 4 <= kWarpCap * 8, "bitmap + prefix must fit in s_keys");
+  E_out = E64;
+  if (E64 > CAP) return 1;
+  static_assert(2 * kWarpSpanWords * 4 <= kKeyBytes, "bitmap + prefix must fit in s_keys");
   const int E = (int)E64;
   if (E == 0) {
     if (lane == 0) { nact_out[p] = 0; nblk_out[p] = 0; pbytes_out[p] = 0; }
-    return;
+    return 0;
   }
-  uint32_t col[kWarpPer];
-  int rowv[kWarpPer];
+  uint32_t col[PER];
+  int rowv[PER];
   int32_t mn = INT32_MAX, mx = INT32_MIN;
   bool bad_range = false, bad_order = false;
 #pragma unroll
-  for (int k = 0; k < kWarpPer; ++k) {
+  for (int k = 0; k < PER; ++k) {
     const int idx = lane + 32 * k;
     col[k] = 0;
     rowv[k] = 0;
@@ -225,16 +224,18 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp(
       mx = max(mx, c);
     }
   }
-  if (__any_sync(0xffffffffu, bad_range) && lane == 0) atomicOr(status, ST_COL_RANGE);
-  if (__any_sync(0xffffffffu, bad_order) && lane == 0) atomicOr(status, ST_COL_ORDER);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
-  uint32_t qv[kWarpPer];
+  const bool small_span = (int64_t)mx - (int64_t)mn < 32 * kWarpSpanWords;
+  if (!SORT && !small_span) return 2;  // (warp-uniform) handled by the CTA path
+  if (__any_sync(0xffffffffu, bad_range) && lane == 0) atomicOr(status, ST_COL_RANGE);
+  if (__any_sync(0xffffffffu, bad_order) && lane == 0) atomicOr(status, ST_COL_ORDER);
+  uint32_t qv[PER];
   uint32_t nact = 0;
-  if ((int64_t)mx - (int64_t)mn < 32 * kWarpSpanWords) {
+  if (small_span) {
     uint32_t* bm = reinterpret_cast<uint32_t*>(s_keys);
     uint32_t* pre = bm + kWarpSpanWords;
     constexpr int kW = kWarpSpanWords / 32;
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp(
     for (int i = 0; i < kW; ++i) bm[lane * kW + i] = 0;
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < kWarpPer; ++k)
+    for (int k = 0; k < PER; ++k)
       if (lane + 32 * k < E) {
         const uint32_t off = col[k] - (uint32_t)mn;
         atomicOr(&bm[off >> 5], 1u << (off & 31));
@@ -256,16 +257,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp(
     for (int i = 0; i < kW; ++i) { pre[lane * kW + i] = run; run += cnt[i]; }
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < kWarpPer; ++k) {
+    for (int k = 0; k < PER; ++k) {
       const uint32_t off = col[k] - (uint32_t)mn;
       const uint32_t w = (off >> 5) & (kWarpSpanWords - 1), b = off & 31;
       qv[k] = pre[w] + __popc(bm[w] & ((1u << b) - 1u));
     }
-  } else {
+  } else if constexpr (SORT) {
     int n = 32;
     while (n < E) n <<= 1;
 #pragma unroll
-    for (int k = 0; k < kWarpPer; ++k) {
+    for (int k = 0; k < PER; ++k) {
       const int idx = lane + 32 * k;
       if (idx < n) s_keys[idx] = idx < E ? ((uint64_t)col[k] << 32) | (uint32_t)idx : ~0ull;
     }
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp(
     }
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < kWarpPer; ++k) qv[k] = lane + 32 * k < E ? s_qb[lane + 32 * k] : 0u;
+    for (int k = 0; k < PER; ++k) qv[k] = lane + 32 * k < E ? s_qb[lane + 32 * k] : 0u;
   }
   const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
   const uint32_t nblk = (nact + tk - 1) / tk;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp(
   for (int i = lane; i < nbricks; i += 32) s_pat[i] = 0ull;
   __syncwarp();
 #pragma unroll
-  for (int k = 0; k < kWarpPer; ++k) {
+  for (int k = 0; k < PER; ++k) {
     if (lane + 32 * k < E) {
       const uint32_t qq = qv[k], r = (uint32_t)rowv[k];
       const uint32_t j = qq / tk, lc = qq % tk;
@@ -324,67 +325,111 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp(
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
   if (lane == 0) { nact_out[p] = nact; nblk_out[p] = nblk; pbytes_out[p] = bytes; }
+  return 0;
 }
 
-// ------------------------------------------------------------------ pass B, panels with <= kWarpCap entries
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_emit_warp(
-    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const float* __restrict__ vals, int64_t M,
-    int64_t K, int64_t nnz, int tm, int tk, int64_t P, const uint32_t* __restrict__ q,
-    const uint32_t* __restrict__ nact_in, const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff,
-    const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac, uint64_t* __restrict__ sp,
-    uint8_t* __restrict__ packed, int warp_smem_bytes) {
+template <int CAP, bool SORT>
+__host__ __device__ constexpr int count_warp_smem(int tm, int tk) {
+  return (int)((((SORT ? CAP * 12 : 2 * kWarpSpanWords * 4) + ((tm + 2) & ~1) * 8 + (CAP / tk) * (tk / 4) * (tm / 16) * 8) +
+                15) & ~15);
+}
+
+// Warp per panel over all panels (CAP = 256, sort allowed); panels with more entries go to list L1.
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp(
+    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t M, int64_t K, int64_t nnz, int tm,
+    int tk, int64_t P, uint32_t* __restrict__ q, uint32_t* __restrict__ nact_out, uint32_t* __restrict__ nblk_out,
+    uint32_t* __restrict__ pbytes_out, uint64_t* __restrict__ gpat, uint32_t* __restrict__ l1, uint32_t* __restrict__ nl1,
+    uint32_t* status) {
   extern __shared__ __align__(16) uint8_t dsm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wid = threadIdx.x >> 5;
   const int64_t p = (int64_t)blockIdx.x * kWarpsPerCta + wid;
   if (p >= P) return;
-  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
-  const int64_t r0 = p * tm;
-  const int nrows = (int)min((int64_t)tm, M - r0);
-  {
-    int64_t a = rp[r0], b = rp[r0 + nrows];
-    a = a < 0 ? 0 : (a > nnz ? nnz : a);
-    b = b < 0 ? 0 : (b > nnz ? nnz : b);
-    if (b - a > kWarpCap) return;  // emitted by k_emit (CTA)
+  uint8_t* my = dsm + (size_t)wid * count_warp_smem<kWarpCap, true>(tm, tk);
+  int64_t E;
+  const int r = count_panel_warp<kWarpCap, true>(rp, ci, M, K, nnz, tm, tk, p, q, nact_out, nblk_out, pbytes_out,
+                                                  gpat, status, my, E);
+  if (r != 0 && (threadIdx.x & 31) == 0) l1[atomicAdd(nl1, 1u)] = (uint32_t)p;
+}
+
+// Warp per listed panel (CAP = 1024, bitmap ranking only). Not handled -> list L2 (CTA count); more than
+// kWarpCap2 entries -> also list L3 (CTA emit).
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp2(
+    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t M, int64_t K, int64_t nnz, int tm,
+    int tk, uint32_t* __restrict__ q, uint32_t* __restrict__ nact_out, uint32_t* __restrict__ nblk_out,
+    uint32_t* __restrict__ pbytes_out, uint64_t* __restrict__ gpat, const uint32_t* __restrict__ l1,
+    const uint32_t* __restrict__ nl1, uint32_t* __restrict__ l2, uint32_t* __restrict__ nl2,
+    uint32_t* __restrict__ l3, uint32_t* __restrict__ nl3, uint32_t* status) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* my = dsm + (size_t)wid * count_warp_smem<kWarpCap2, false>(tm, tk);
+  const uint32_t count = *nl1;
+  for (uint32_t t = blockIdx.x * kWarpsPerCta + wid; t < count; t += gridDim.x * kWarpsPerCta) {
+    const int64_t p = l1[t];
+    int64_t E;
+    const int r = count_panel_warp<kWarpCap2, false>(rp, ci, M, K, nnz, tm, tk, p, q, nact_out, nblk_out,
+                                                      pbytes_out, gpat, status, my, E);
+    if (lane == 0) {
+      if (r != 0) l2[atomicAdd(nl2, 1u)] = (uint32_t)p;
+      if (E > kWarpCap2) l3[atomicAdd(nl3, 1u)] = (uint32_t)p;
+    }
+    __syncwarp();
   }
+}
+
+// ------------------------------------------------------------------ pass B, warp per panel
+template <int CAP>
+__device__ __forceinline__ void emit_panel_warp(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                const float* __restrict__ vals, int64_t M, int64_t K, int64_t nnz,
+                                                int tm, int tk, int64_t p, const uint32_t* __restrict__ q,
+                                                const uint32_t* __restrict__ nact_in,
+                                                const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff,
+                                                const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac,
+                                                uint64_t* __restrict__ sp, uint8_t* __restrict__ packed, uint8_t* my) {
+  const int lane = threadIdx.x & 31;
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
   const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0;
   if (nblk == 0) return;
-  uint8_t* my = dsm + (size_t)wid * warp_smem_bytes;
   int64_t* s_rp = reinterpret_cast<int64_t*>(my);
-  uint64_t* s_vbase = reinterpret_cast<uint64_t*>(s_rp + ((tm + 2) & ~1));  // [kWarpCap / tk]
-  uint64_t* s_pt = s_vbase + kWarpCap / 16;                                // [kWarpCap / tk * nbk]
+  uint64_t* s_vbase = reinterpret_cast<uint64_t*>(s_rp + ((tm + 2) & ~1));  // [CAP / 16]
+  uint64_t* s_pt = s_vbase + CAP / 16;                                     // [CAP / tk * nbk]
   warp_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);
+  const int nrows = (int)min((int64_t)tm, M - p * tm);
   const uint32_t nact = nact_in[p];
   const int64_t e0 = s_rp[0], e1 = s_rp[nrows];
   const uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
   for (int i = lane; i < (int)nblk * nbk; i += 32) s_pt[i] = gp[i];
   __syncwarp();
-  // one lane per block (nblk <= kWarpCap / tk <= 32)
-  uint32_t nbr = 0, nz = 0, size = 0;
-  const uint32_t j = lane;
-  if (j < nblk) {
-    for (int i = 0; i < nbk; ++i) { const uint64_t v = s_pt[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
-    size = block_bytes(nbc, nbr, nz);
-  }
-  const uint64_t off = poff[p] + warp_excl_scan(size, nullptr);
-  if (j < nblk) {
-    sp[b0 + j] = off;
-    uint8_t* blk = packed + off;
-    const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
-    uint32_t k = 0;
-    blk[0] = 0;
-    for (int bc = 0; bc < nbc; ++bc) {
-      for (int br = 0; br < nbrow; ++br) {
-        const uint64_t v = s_pt[j * nbk + bc * nbrow + br];
-        if (!v) continue;
-        blk[nbc + 1 + k] = (uint8_t)br;
-        reinterpret_cast<uint64_t*>(blk + hdr)[k] = v;
-        ++k;
-      }
-      blk[bc + 1] = (uint8_t)k;
+  uint64_t carry = poff[p];
+  for (uint32_t c0 = 0; c0 < nblk; c0 += 32) {  // blocks, 32 at a time (one per lane)
+    const uint32_t j = c0 + lane;
+    uint32_t nbr = 0, nz = 0, size = 0;
+    if (j < nblk) {
+      for (int i = 0; i < nbk; ++i) { const uint64_t v = s_pt[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
+      size = block_bytes(nbc, nbr, nz);
     }
-    for (uint32_t i = nbc + 1 + nbr; i < hdr; ++i) blk[i] = 0;
-    for (uint32_t i = hdr + 8 * nbr + 4 * nz; i < size; ++i) blk[i] = 0;
-    s_vbase[j] = off + hdr + 8 * nbr;
+    uint32_t tot;
+    const uint64_t off = carry + warp_excl_scan(size, &tot);
+    if (j < nblk) {
+      sp[b0 + j] = off;
+      uint8_t* blk = packed + off;
+      const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+      uint32_t k = 0;
+      blk[0] = 0;
+      for (int bc = 0; bc < nbc; ++bc) {
+        for (int br = 0; br < nbrow; ++br) {
+          const uint64_t v = s_pt[j * nbk + bc * nbrow + br];
+          if (!v) continue;
+          blk[nbc + 1 + k] = (uint8_t)br;
+          reinterpret_cast<uint64_t*>(blk + hdr)[k] = v;
+          ++k;
+        }
+        blk[bc + 1] = (uint8_t)k;
+      }
+      for (uint32_t i = nbc + 1 + nbr; i < hdr; ++i) blk[i] = 0;
+      for (uint32_t i = hdr + 8 * nbr + 4 * nz; i < size; ++i) blk[i] = 0;
+      s_vbase[j] = off + hdr + 8 * nbr;
+    }
+    carry += tot;
   }
   for (int64_t t = nact + lane; t < (int64_t)nblk * tk; t += 32) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
   __syncwarp();
@@ -403,6 +448,56 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_emit_warp(
     for (int i = 0; i < mine; ++i) o += __popcll(pt[i]);
     o += __popcll(pt[mine] & ((1ull << bit) - 1ull));
     reinterpret_cast<float*>(packed + s_vbase[jb])[o] = v;
+  }
+  __syncwarp();
+}
+
+template <int CAP>
+__host__ __device__ constexpr int emit_warp_smem(int tm, int tk) {
+  return (int)((((tm + 2) & ~1) * 8 + (CAP / 16) * 8 + (CAP / tk) * (tk / 4) * (tm / 16) * 8 + 15) & ~15);
+}
+
+__device__ __forceinline__ int64_t panel_entries(const int64_t* __restrict__ rp, int64_t M, int64_t nnz, int tm,
+                                                 int64_t p) {
+  const int64_t r0 = p * tm;
+  const int nrows = (int)min((int64_t)tm, M - r0);
+  int64_t a = rp[r0], b = rp[r0 + nrows];
+  a = a < 0 ? 0 : (a > nnz ? nnz : a);
+  b = b < 0 ? 0 : (b > nnz ? nnz : b);
+  return b - a;
+}
+
+// all panels with <= kWarpCap entries
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_emit_warp(
+    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const float* __restrict__ vals, int64_t M,
+    int64_t K, int64_t nnz, int tm, int tk, int64_t P, const uint32_t* __restrict__ q,
+    const uint32_t* __restrict__ nact_in, const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff,
+    const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac, uint64_t* __restrict__ sp,
+    uint8_t* __restrict__ packed) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int wid = threadIdx.x >> 5;
+  const int64_t p = (int64_t)blockIdx.x * kWarpsPerCta + wid;
+  if (p >= P) return;
+  if (panel_entries(rp, M, nnz, tm, p) > kWarpCap) return;  // listed in L1 (k_emit_warp2 / k_emit)
+  emit_panel_warp<kWarpCap>(rp, ci, vals, M, K, nnz, tm, tk, p, q, nact_in, brp, poff, gpat, ac, sp, packed,
+                            dsm + (size_t)wid * emit_warp_smem<kWarpCap>(tm, tk));
+}
+
+// listed panels (L1) with <= kWarpCap2 entries
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_emit_warp2(
+    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const float* __restrict__ vals, int64_t M,
+    int64_t K, int64_t nnz, int tm, int tk, const uint32_t* __restrict__ q, const uint32_t* __restrict__ nact_in,
+    const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff, const uint64_t* __restrict__ gpat,
+    uint32_t* __restrict__ ac, uint64_t* __restrict__ sp, uint8_t* __restrict__ packed,
+    const uint32_t* __restrict__ l1, const uint32_t* __restrict__ nl1) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int wid = threadIdx.x >> 5;
+  uint8_t* my = dsm + (size_t)wid * emit_warp_smem<kWarpCap2>(tm, tk);
+  const uint32_t count = *nl1;
+  for (uint32_t t = blockIdx.x * kWarpsPerCta + wid; t < count; t += gridDim.x * kWarpsPerCta) {
+    const int64_t p = l1[t];
+    if (panel_entries(rp, M, nnz, tm, p) > kWarpCap2) continue;  // listed in L3 (k_emit)
+    emit_panel_warp<kWarpCap2>(rp, ci, vals, M, K, nnz, tm, tk, p, q, nact_in, brp, poff, gpat, ac, sp, packed, my);
   }
 }
 
@@ -873,8 +968,12 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   uint32_t* pbytes = cnt + 2 * (P + 1);
   uint64_t* poff = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t), s);
   uint64_t* gpat = (uint64_t*)dalloc(pat_cap * sizeof(uint64_t), s);
-  uint32_t* biglist = (uint32_t*)dalloc(2 * (P + 1) * sizeof(uint32_t), s);  // big | mid panel lists
-  uint32_t* midlist = biglist + (P + 1);
+  // panel lists: big (> kSmallCap, hub bitmap) | L1 (> kWarpCap) | L2 (CTA count) | L3 (CTA emit)
+  uint32_t* biglist = (uint32_t*)dalloc(4 * (P + 1) * sizeof(uint32_t), s);
+  uint32_t* l1 = biglist + (P + 1);
+  uint32_t* l2 = biglist + 2 * (P + 1);
+  uint32_t* l3 = biglist + 3 * (P + 1);
+  uint32_t* ctr = (uint32_t*)dalloc(8 * sizeof(uint32_t), s);  // nbig, nl1, nl2, nl3, status
   const int64_t nparts = ceil_div(P + 1, kScanChunk) + 1;
   uint64_t* part = (uint64_t*)dalloc(nparts * sizeof(uint64_t), s);
   uint64_t* info = (uint64_t*)dalloc(4 * sizeof(uint64_t), s);  // [3] = status word | hub count
@@ -883,50 +982,55 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   uint32_t* bigscr = (uint32_t*)dalloc((size_t)big_ctas * 2 * words * sizeof(uint32_t), s);
   hrpb_status_t st = HRPB_SUCCESS;
   if (!h->brp || !h->ac || !h->sp || !h->packed || !q || !cnt || !poff || !gpat || !biglist || !part || !info ||
-      !bigscr) {
+      !bigscr || !ctr) {
     st = HRPB_ERROR_OUT_OF_MEMORY;
   }
   uint64_t hinfo[3] = {0, 0, 0};
   if (st == HRPB_SUCCESS) {
-    uint32_t* status = reinterpret_cast<uint32_t*>(info + 3);
-    uint32_t* nbig = status + 1;
-    uint32_t* nmid = reinterpret_cast<uint32_t*>(info + 2);  // info[2] is rewritten by k_finalize
-    cudaMemsetAsync(info + 2, 0, 2 * sizeof(uint64_t), s);
+    uint32_t* nbig = ctr;
+    uint32_t* nl1 = ctr + 1;
+    uint32_t* nl2 = ctr + 2;
+    uint32_t* nl3 = ctr + 3;
+    uint32_t* status = ctr + 4;
+    cudaMemsetAsync(ctr, 0, 8 * sizeof(uint32_t), s);
     const size_t count_smem =
         (size_t)kSmallCap * (8 + 4 + 4 + 1) + (size_t)ceil_div(kSmallCap, tk) * nbk * sizeof(uint64_t);
+    const size_t wsm_c1 = (size_t)count_warp_smem<kWarpCap, true>(tm, tk) * kWarpsPerCta;
+    const size_t wsm_c2 = (size_t)count_warp_smem<kWarpCap2, false>(tm, tk) * kWarpsPerCta;
+    const size_t wsm_e1 = (size_t)emit_warp_smem<kWarpCap>(tm, tk) * kWarpsPerCta;
+    const size_t wsm_e2 = (size_t)emit_warp_smem<kWarpCap2>(tm, tk) * kWarpsPerCta;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_count_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_count_warp2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_emit_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_emit_warp2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    const int wsm_count = (int)align_up(kWarpCap * 12 + ((tm + 2) & ~1) * 8 + (kWarpCap / tk) * nbk * 8, 16);
-    const int wsm_emit = (int)align_up(((tm + 2) & ~1) * 8 + (kWarpCap / 16) * 8 + (kWarpCap / tk) * nbk * 8, 16);
     const unsigned wgrid = (unsigned)ceil_div(P, kWarpsPerCta);
-    static bool wattr = false;
-    if (!wattr) {
-      cudaFuncSetAttribute(k_count_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_emit_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      wattr = true;
-    }
     const int mid_ctas = 8 * num_sms();
-    if (P > 0) {  // pass A
-      k_count_warp<<<wgrid, 32 * kWarpsPerCta, (size_t)wsm_count * kWarpsPerCta, s>>>(
-          row_ptr, col_idx, M, K, nnz, tm, tk, P, q, nact, nblk, pbytes, gpat, midlist, nmid, status, wsm_count);
+    if (P > 0) {  // pass A: warp (<= 256) -> warp, bitmap (<= 1024) -> CTA (<= 2048) -> hub bitmap
+      k_count_warp<<<wgrid, 32 * kWarpsPerCta, wsm_c1, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, P, q, nact, nblk,
+                                                            pbytes, gpat, l1, nl1, status);
+      k_count_warp2<<<mid_ctas, 32 * kWarpsPerCta, wsm_c2, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
+                                                                pbytes, gpat, l1, nl1, l2, nl2, l3, nl3, status);
       k_count<<<mid_ctas, kSmallThreads, count_smem, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
-                                                          pbytes, gpat, midlist, nmid, biglist, nbig, status);
+                                                          pbytes, gpat, l2, nl2, biglist, nbig, status);
       k_count_big<<<big_ctas, kBigThreads, 0, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk, pbytes, gpat,
                                                     biglist, nbig, bigscr, words, status);
-      note_launch(3);
+      note_launch(4);
     }
     scan_excl<uint32_t>(nblk, P, h->brp, part, s);  // B2: blockedRowPtr
     scan_excl<uint64_t>(pbytes, P, poff, part, s);  // B4 (panel level): byte offset of each panel
     if (P > 0) {                                    // pass B
-      k_emit_warp<<<wgrid, 32 * kWarpsPerCta, (size_t)wsm_emit * kWarpsPerCta, s>>>(
-          row_ptr, col_idx, values, M, K, nnz, tm, tk, P, q, nact, h->brp, poff, gpat, h->ac, h->sp, h->packed,
-          wsm_emit);
+      k_emit_warp<<<wgrid, 32 * kWarpsPerCta, wsm_e1, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, P, q, nact,
+                                                           h->brp, poff, gpat, h->ac, h->sp, h->packed);
+      k_emit_warp2<<<mid_ctas, 32 * kWarpsPerCta, wsm_e2, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact,
+                                                               h->brp, poff, gpat, h->ac, h->sp, h->packed, l1, nl1);
       k_emit<<<mid_ctas, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp, poff,
-                                               gpat, h->ac, h->sp, h->packed, midlist, nmid);
-      note_launch(2);
+                                               gpat, h->ac, h->sp, h->packed, l3, nl3);
+      note_launch(3);
     }
     k_finalize<<<1, 1, 0, s>>>(row_ptr, M, nnz, P, h->brp, poff, h->sp, status, info);
     note_launch();
@@ -937,6 +1041,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   }
   dfree(q, s); dfree(cnt, s); dfree(poff, s); dfree(gpat, s); dfree(biglist, s); dfree(part, s); dfree(info, s);
   dfree(bigscr, s);
+  dfree(ctr, s);
   if (st == HRPB_SUCCESS && hinfo[2] != 0) st = HRPB_ERROR_INVALID_CSR;
   h->NB = (int64_t)hinfo[0];
   h->bytes = (int64_t)hinfo[1];

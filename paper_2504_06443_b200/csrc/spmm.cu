@@ -31,8 +31,6 @@ constexpr int kDecWarps = 4;                               // warps 4..7: brick 
 constexpr int kMmaWarp = kProdWarps + kDecWarps;           // warp 8: TMEM alloc + MMA issue
 constexpr int kEpiWarp0 = kMmaWarp + 1;                    // warps 9..12: epilogue
 constexpr int kSpmmThreads = 32 * (kEpiWarp0 + 4);        // 416
-constexpr int kARawBytes = 1152;   // >= 1072 (largest TM=16/TK=16 block), multiple of 128
-constexpr int kATileBytes = 1024;  // 16 x 16 fp32 decoded block
 constexpr int kMaxStages = 20;
 
 struct SpmmParams {
@@ -47,6 +45,7 @@ struct SpmmParams {
   int n0;      // first output column of this launch
   int stages;  // pipeline depth
   long long* trace;  // optional: per-block event timestamps of CTA 0 (HRPB_TRACE), [6][kTraceN]
+  int debug;         // HRPB_DEBUG bits (experiments only): 1 = skip C stores, 2 = skip decode, 4 = skip A copy wait
 };
 constexpr int kTraceN = 1024;
 // trace slots: 0 producer issue (after empty), 1 A arrived (decoder), 2 decode done, 3 B arrived (MMA),
@@ -55,15 +54,26 @@ __device__ __forceinline__ void trace_ev(const SpmmParams& p, int slot, uint32_t
   if (p.trace != nullptr && blockIdx.x == 0 && i < kTraceN) p.trace[slot * kTraceN + i] = clock64();
 }
 
-// instruction descriptor: D F32, A/B TF32, A MN-major, B K-major, N = 16, M = 128
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (0u << 16) | ((16u >> 3) << 17) |
-                            ((128u >> 4) << 24);
+// instruction descriptor: D F32, A/B TF32, A MN-major, B K-major, N = TM (panel rows), M = 128
+template <int TMV>
+__host__ __device__ constexpr uint32_t idesc_tf32() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (0u << 16) | ((uint32_t)(TMV >> 3) << 17) |
+         ((128u >> 4) << 24);
+}
 
-template <int NT>
+template <int NT, int TMV>
 struct SmemLayout {
   static constexpr int kNA = 4 * NT;                 // 32-column atoms per 4-row group
   static constexpr int kBTile = 16 * 128 * 4 * NT;  // gathered rows per stage
+  static constexpr int kNbrow = TMV / 16;            // brick rows per block
+  static constexpr int kNbk = 4 * kNbrow;            // brick slots per block (TK = 16)
+  // largest HRPB-v1 block: align8(5 + nbk) + 8 nbk + 4 TM TK, rounded to 128 B
+  static constexpr int kARawBytes = ((((5 + kNbk + 7) & ~7) + 8 * kNbk + 4 * TMV * 16) + 127) & ~127;
+  static constexpr int kATileBytes = TMV * 16 * 4;   // TM x 16 fp32 decoded block
+  static constexpr int kLbo = TMV * 16;              // bytes between 4-column K groups of the decoded tile
   static constexpr int kStage = kBTile + kARawBytes + kATileBytes;
+  static constexpr uint32_t kTmemCols = 2 * NT * TMV <= 32 ? 32 : (2 * NT * TMV <= 64 ? 64 : (2 * NT * TMV <= 128 ? 128 : (2 * NT * TMV <= 256 ? 256 : 512)));
+  static_assert(2 * NT * TMV <= 512, "two TMEM accumulator slots must fit in 512 columns");
 };
 
 __device__ __forceinline__ int64_t panel_lower_bound(const uint32_t* brp, int64_t P, uint64_t target) {
@@ -125,9 +135,10 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 
 // GM = gather mode: 0 = TMA tile::gather4 (one issuing lane per producer warp),
 //                   1 = cp.async 16-B copies by all 128 producer threads into the same swizzled layout.
-template <int NT, int GM>
+template <int NT, int GM, int TMV>
 __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant__ CUtensorMap tmB, SpmmParams prm) {
-  using L = SmemLayout<NT>;
+  using L = SmemLayout<NT, TMV>;
+  constexpr int kARawBytes = L::kARawBytes, kATileBytes = L::kATileBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = prm.stages;
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   int64_t* range = (int64_t*)(misc + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t tmem_cols = NT == 1 ? 32 : (NT == 2 ? 64 : 128);
+  const uint32_t tmem_cols = L::kTmemCols;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -296,6 +307,13 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     for (int64_t b = b_begin + dw; b < b_end; b += kDecWarps) {
       mbar_wait(&full_a[s], ph);
       if (lane == 0) trace_ev(prm, 1, (uint32_t)(b - b_begin));
+      if (prm.debug & 2) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dec[s]);
+        s += kDecWarps;
+        if (s >= S) { s -= S; ph ^= 1; }
+        continue;
+      }
       const uint8_t* blk = araw0 + (size_t)s * kARawBytes;
       float* tile = reinterpret_cast<float*>(atile0 + (size_t)s * kATileBytes);
       const uint32_t cp = *reinterpret_cast<const uint32_t*>(blk);  // colPtr[0..3]
@@ -303,26 +321,73 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       const uint32_t hdr = (5 + nbr + 7) & ~7u;
       const uint64_t* pats = reinterpret_cast<const uint64_t*>(blk + hdr);
       const float* vals = reinterpret_cast<const float*>(blk + hdr + 8 * nbr);
-      uint64_t pt[4];
+      if constexpr (L::kNbrow == 1) {
+        // TM = 16: at most one brick per brick column; all four patterns first, then the values
+        uint64_t pt[4];
 #pragma unroll
-      for (int bc = 0; bc < 4; ++bc) {  // TM = 16: at most one brick per brick column
-        const uint32_t k0 = (cp >> (8 * bc)) & 0xFF;
-        const uint32_t k1 = bc < 3 ? (cp >> (8 * (bc + 1))) & 0xFF : nbr;
-        pt[bc] = k1 > k0 ? pats[k0] : 0ull;
-      }
-      uint32_t off = 0;
-      float v0[4], v1[4];
+        for (int bc = 0; bc < 4; ++bc) {
+          const uint32_t k0 = (cp >> (8 * bc)) & 0xFF;
+          const uint32_t k1 = bc < 3 ? (cp >> (8 * (bc + 1))) & 0xFF : nbr;
+          pt[bc] = k1 > k0 ? pats[k0] : 0ull;
+        }
+        uint32_t off = 0;
+        float v0[4], v1[4];
 #pragma unroll
-      for (int bc = 0; bc < 4; ++bc) {
-        const uint32_t lo = (uint32_t)pt[bc], hi = (uint32_t)(pt[bc] >> 32);
-        v0[bc] = ((lo >> lane) & 1u) ? vals[off + __popc(lo & below)] : 0.f;
-        v1[bc] = ((hi >> lane) & 1u) ? vals[off + __popc(lo) + __popc(hi & below)] : 0.f;
-        off += __popc(lo) + __popc(hi);
-      }
+        for (int bc = 0; bc < 4; ++bc) {
+          const uint32_t lo = (uint32_t)pt[bc], hi = (uint32_t)(pt[bc] >> 32);
+          v0[bc] = ((lo >> lane) & 1u) ? vals[off + __popc(lo & below)] : 0.f;
+          v1[bc] = ((hi >> lane) & 1u) ? vals[off + __popc(lo) + __popc(hi & below)] : 0.f;
+          off += __popc(lo) + __popc(hi);
+        }
 #pragma unroll
-      for (int bc = 0; bc < 4; ++bc) {
-        tile[bc * 64 + lane] = to_tf32_rna(v0[bc]);
-        tile[bc * 64 + 32 + lane] = to_tf32_rna(v1[bc]);
+        for (int bc = 0; bc < 4; ++bc) {
+          tile[bc * 64 + lane] = to_tf32_rna(v0[bc]);
+          tile[bc * 64 + 32 + lane] = to_tf32_rna(v1[bc]);
+        }
+      } else {
+        // TM > 16: lane k < nbr owns stored brick k (pattern, slot bc*nbrow + br, value offset by warp scan);
+        // each brick is then expanded by the whole warp from shuffled metadata; absent slots get zeros.
+        uint64_t mypat = 0ull;
+        uint32_t myslot = 0, mycnt = 0;
+        if ((uint32_t)lane < nbr) {
+          mypat = pats[lane];
+          const uint32_t br = blk[5 + lane];
+          uint32_t bc = 0;
+#pragma unroll
+          for (int c = 1; c < 4; ++c) bc += (uint32_t)lane >= ((cp >> (8 * c)) & 0xFF);
+          myslot = bc * L::kNbrow + br;
+          mycnt = __popcll(mypat);
+        }
+        uint32_t myoff = mycnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, myoff, o);
+          if (lane >= o) myoff += y;
+        }
+        myoff -= mycnt;  // exclusive prefix = value offset of brick `lane`
+        uint32_t present = 0;  // bit per slot
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          if ((uint32_t)k >= nbr) break;
+          const uint32_t slot = __shfl_sync(0xffffffffu, myslot, k);
+          const uint32_t off = __shfl_sync(0xffffffffu, myoff, k);
+          const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)mypat, k);
+          const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(mypat >> 32), k);
+          const float a0 = ((lo >> lane) & 1u) ? vals[off + __popc(lo & below)] : 0.f;
+          const float a1 = ((hi >> lane) & 1u) ? vals[off + __popc(lo) + __popc(hi & below)] : 0.f;
+          const uint32_t bc = slot / L::kNbrow, br = slot % L::kNbrow;
+          tile[bc * (L::kLbo / 4) + br * 64 + lane] = to_tf32_rna(a0);
+          tile[bc * (L::kLbo / 4) + br * 64 + 32 + lane] = to_tf32_rna(a1);
+          present |= 1u << slot;
+        }
+#pragma unroll
+        for (int i = 0; i < L::kNbk; ++i) {
+          if (!((present >> i) & 1u)) {
+            const int bc = i / L::kNbrow, br = i % L::kNbrow;
+            tile[bc * (L::kLbo / 4) + br * 64 + lane] = 0.f;
+            tile[bc * (L::kLbo / 4) + br * 64 + 32 + lane] = 0.f;
+          }
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -346,7 +411,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       const uint32_t slot = pc & 1;
       mbar_wait(&tempty[slot], ((pc >> 1) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t dcol = tbase + slot * NT * 16;
+      const uint32_t dcol = tbase + slot * NT * TMV;
       for (uint32_t b = bb; b < be; ++b, ++i) {
         const int s = st;
         mbar_wait(&full_b[s], ph);
@@ -361,8 +426,8 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
 #pragma unroll
             for (int g = 0; g < 2; ++g) {
               const uint64_t ad = umma_sdesc(bt + (2 * g * L::kNA + 4 * t) * 512, 512, L::kNA * 512, 1);
-              const uint64_t bd = umma_sdesc(at + g * 512, 256, 128, 0);
-              umma_tf32(dcol + t * 16, ad, bd, kIdesc, (b > bb || g > 0) ? 1u : 0u);
+              const uint64_t bd = umma_sdesc(at + g * 2 * L::kLbo, L::kLbo, 128, 0);
+              umma_tf32(dcol + t * TMV, ad, bd, idesc_tf32<TMV>(), (b > bb || g > 0) ? 1u : 0u);
             }
           }
           umma_commit(&empty[s]);
@@ -384,8 +449,8 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     int64_t p;
     uint32_t bb, be;
     while (cursor.next(p, bb, be)) {
-      const int64_t row0 = p * 16;
-      const int nrows = (int)min((int64_t)16, M - row0);
+      const int64_t row0 = p * TMV;
+      const int nrows = (int)min((int64_t)TMV, M - row0);
       if (bb == be) {  // empty panel: zero rows (R13)
         for (int r = 0; r < nrows; ++r)
           for (int64_t c = et; c < ncols; c += 128) prm.C[(row0 + r) * N + n0 + c] = 0.f;
@@ -397,15 +462,20 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       tc_fence_after();
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        uint32_t v[16];
-        tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + slot * NT * 16 + t * 16, v);
-        tmem_ld_wait();
-        const int64_t c = 128 * t + 32 * qd + lane;
-        if (c < ncols) {
-          float* dst = prm.C + row0 * N + n0 + c;
 #pragma unroll
-          for (int r = 0; r < 16; ++r)
-            if (r < nrows) __stcs(dst + (int64_t)r * N, __uint_as_float(v[r]));
+        for (int c16 = 0; c16 < TMV / 16; ++c16) {  // 16 panel rows per tcgen05.ld
+          uint32_t v[16];
+          tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + slot * NT * TMV + t * TMV + c16 * 16, v);
+          tmem_ld_wait();
+          const int64_t c = 128 * t + 32 * qd + lane;
+          if (c < ncols) {
+            float* dst = prm.C + (row0 + 16 * c16) * N + n0 + c;
+            if (!(prm.debug & 1)) {
+#pragma unroll
+              for (int r = 0; r < 16; ++r)
+                if (16 * c16 + r < nrows) __stcs(dst + (int64_t)r * N, __uint_as_float(v[r]));
+            }
+          }
         }
       }
       tc_fence_before();
@@ -449,10 +519,10 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-template <int NT, int GM>
+template <int NT, int GM, int TMV>
 static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, const float* B, int64_t ldb, float* C,
                                int64_t N, int n0, cudaStream_t s) {
-  using L = SmemLayout<NT>;
+  using L = SmemLayout<NT, TMV>;
   const int budget = 227 * 1024 - 1024 /*alignment*/ - 512 /*barriers, misc*/;
   int stages = budget / L::kStage;
   if (stages > kMaxStages) stages = kMaxStages;
@@ -463,7 +533,7 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   const size_t smem = 1024 + (size_t)stages * L::kStage + (4 * stages + 4) * 8 + 64;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_spmm<NT, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return cuda_status(e);
     attr_set = true;
   }
@@ -473,10 +543,14 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     trace = (long long*)dalloc(6 * kTraceN * sizeof(long long), s);
     cudaMemsetAsync(trace, 0, 6 * kTraceN * sizeof(long long), s);
   }
-  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, B, h->K, ldb, n0, stages, trace};
+  static const int debug = [] {
+    const char* e = getenv("HRPB_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, B, h->K, ldb, n0, stages, trace, debug};
   int grid = num_sms();
   if ((int64_t)grid > h->P) grid = (int)(h->P > 0 ? h->P : 1);
-  k_spmm<NT, GM><<<grid, kSpmmThreads, smem, s>>>(tm, prm);
+  k_spmm<NT, GM, TMV><<<grid, kSpmmThreads, smem, s>>>(tm, prm);
   note_launch();
   if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)
     static long long host[6 * kTraceN];
@@ -498,7 +572,7 @@ hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float
     cudaError_t e = cudaMemsetAsync(C, 0, (size_t)h->M * N * sizeof(float), s);
     return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);
   }
-  if (h->tm != 16 || h->tk != 16) return HRPB_ERROR_NOT_SUPPORTED;
+  if (!(h->tm == 16 || h->tm == 32 || h->tm == 64) || h->tk != 16) return HRPB_ERROR_NOT_SUPPORTED;
   EncodeTiledFn enc = get_encode();
   if (!enc) return HRPB_ERROR_NOT_SUPPORTED;
   const float* Bt = B;
@@ -535,21 +609,28 @@ hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float
       const char* e = getenv("HRPB_GATHER");  // 0 = TMA gather4, 1 = cp.async (default)
       return e ? atoi(e) : 1;
     }();
-    if (gm == 0) {
+#define HRPB_LAUNCH(TMV_)                                                                     \
+  switch (nt) {                                                                               \
+    case 1: st = launch_nt<1, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
+    case 2: st = launch_nt<2, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
+    case 3: st = launch_nt<3, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
+    default: st = launch_nt<4, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;              \
+  }
+    if (gm == 0 && h->tm == 16) {  // TMA gather4 variant (diagnostic, TM = 16 only)
       switch (nt) {
-        case 1: st = launch_nt<1, 0>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-        case 2: st = launch_nt<2, 0>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-        case 3: st = launch_nt<3, 0>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-        default: st = launch_nt<4, 0>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+        case 1: st = launch_nt<1, 0, 16>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+        case 2: st = launch_nt<2, 0, 16>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+        case 3: st = launch_nt<3, 0, 16>(h, tm, Bt, ld, C, N, (int)n0, s); break;
+        default: st = launch_nt<4, 0, 16>(h, tm, Bt, ld, C, N, (int)n0, s); break;
       }
+    } else if (h->tm == 16) {
+      HRPB_LAUNCH(16)
+    } else if (h->tm == 32) {
+      HRPB_LAUNCH(32)
     } else {
-      switch (nt) {
-        case 1: st = launch_nt<1, 1>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-        case 2: st = launch_nt<2, 1>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-        case 3: st = launch_nt<3, 1>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-        default: st = launch_nt<4, 1>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-      }
+      HRPB_LAUNCH(64)
     }
+#undef HRPB_LAUNCH
     if (st != HRPB_SUCCESS) return st;
   }
   return HRPB_SUCCESS;

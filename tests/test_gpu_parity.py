@@ -77,9 +77,10 @@ def test_builder_edge_cases():
         assert_same_hrpb(A, oracle.csr_to_hrpb(M, K, rp, ci, v), f"edge case {i}")
 
 
+@pytest.mark.parametrize("name", ["c5", "c2a", "c2b", "c3"])
 @pytest.mark.parametrize("tm,tk", [(32, 16), (64, 16), (16, 32), (128, 16)])
-def test_builder_other_tiles(tm, tk):
-    w = synth.make("c5", scale=4)
+def test_builder_other_tiles(tm, tk, name):
+    w = synth.make(name, scale={"c5": 4, "c2a": 5, "c2b": 5, "c3": 8}[name])
     A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm, tk=tk)
     assert_same_hrpb(A, oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm, tk=tk), f"{tm}x{tk}")
 
@@ -214,3 +215,26 @@ def test_spmm_deterministic():
     c1 = hp.spmm(A, B).cpu().numpy()
     c2 = hp.spmm(A, B).cpu().numpy()
     assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
+
+
+# --------------------------------------------------------------------------- TM > 16 panels (NEXT-1)
+@pytest.mark.parametrize("tm", [32, 64])
+@pytest.mark.parametrize("N", [8, 128, 200, 512])
+def test_spmm_exact_tm(tm, N):
+    w = synth.make("c1", scale=2, N=N)
+    B = w.B()
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm)
+    assert A.tm == tm
+    check_exact(hp.spmm(A, dev(B)).cpu().numpy(), oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B),
+                f"tm={tm} N={N}")
+
+
+@pytest.mark.parametrize("tm", [32, 64])
+@pytest.mark.parametrize("name,scale,N", [("c2a", 4, 128), ("c3", 7, 256), ("c5", 3, 64)])
+def test_spmm_float_tm(tm, name, scale, N):
+    w = synth.make(name, scale=scale, N=N)
+    B = w.B()
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm)
+    C = hp.spmm(A, dev(B)).cpu().numpy()
+    Cref, S = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B, with_bound=True)
+    check_float(C, Cref, S, f"{name} tm={tm}")
