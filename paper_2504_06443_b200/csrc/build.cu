@@ -208,18 +208,25 @@ __device__ __forceinline__ int count_panel_warp(const int64_t* __restrict__ rp, 
   int32_t mn = INT32_MAX, mx = INT32_MIN;
   bool bad_range = false, bad_order = false;
 #pragma unroll
+  for (int k = 0; k < PER; ++k) {  // all loads first
+    const int idx = lane + 32 * k;
+    col[k] = idx < E ? (uint32_t)ci[e0 + idx] : 0u;
+  }
+  uint32_t prev_last = 0;  // column of entry 32k - 1 (lane 31 of the previous k)
+#pragma unroll
   for (int k = 0; k < PER; ++k) {
     const int idx = lane + 32 * k;
-    col[k] = 0;
+    uint32_t prevc = __shfl_up_sync(0xffffffffu, col[k], 1);
+    if (lane == 0) prevc = prev_last;
+    prev_last = __shfl_sync(0xffffffffu, col[k], 31);
     rowv[k] = 0;
     if (idx < E) {
       const int64_t e = e0 + idx;
-      const int32_t c = ci[e];
+      const int32_t c = (int32_t)col[k];
       const int r = row_of(s_rp, nrows, e);
-      col[k] = (uint32_t)c;
       rowv[k] = r;
       bad_range |= c < 0 || c >= K;
-      if (e > s_rp[r] && ci[e - 1] >= c) bad_order = true;
+      if (e > s_rp[r] && (int32_t)prevc >= c) bad_order = true;
       mn = min(mn, c);
       mx = max(mx, c);
     }
@@ -392,6 +399,7 @@ __device__ __forceinline__ void emit_panel_warp(const int64_t* __restrict__ rp, 
   int64_t* s_rp = reinterpret_cast<int64_t*>(my);
   uint64_t* s_vbase = reinterpret_cast<uint64_t*>(s_rp + ((tm + 2) & ~1));  // [CAP / 16]
   uint64_t* s_pt = s_vbase + CAP / 16;                                     // [CAP / tk * nbk]
+  uint16_t* s_soff = reinterpret_cast<uint16_t*>(s_pt + (CAP / tk) * nbk); // value offset of each brick slot
   warp_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);
   const int nrows = (int)min((int64_t)tm, M - p * tm);
   const uint32_t nact = nact_in[p];
@@ -404,7 +412,12 @@ __device__ __forceinline__ void emit_panel_warp(const int64_t* __restrict__ rp, 
     const uint32_t j = c0 + lane;
     uint32_t nbr = 0, nz = 0, size = 0;
     if (j < nblk) {
-      for (int i = 0; i < nbk; ++i) { const uint64_t v = s_pt[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
+      for (int i = 0; i < nbk; ++i) {
+        const uint64_t v = s_pt[j * nbk + i];
+        s_soff[j * nbk + i] = (uint16_t)nz;  // popcount of the earlier slots (CSC order)
+        nbr += v != 0ull;
+        nz += __popcll(v);
+      }
       size = block_bytes(nbc, nbr, nz);
     }
     uint32_t tot;
@@ -433,28 +446,38 @@ __device__ __forceinline__ void emit_panel_warp(const int64_t* __restrict__ rp, 
   }
   for (int64_t t = nact + lane; t < (int64_t)nblk * tk; t += 32) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
   __syncwarp();
-  for (int64_t e = e0 + lane; e < e1; e += 32) {
-    const uint32_t qq = q[e];
-    const int32_t c = ci[e];
-    const float v = vals[e];
-    if (qq >= nact) continue;
-    const int r = row_of(s_rp, nrows, e);
-    const uint32_t jb = qq / tk, lc = qq % tk;
-    ac[((int64_t)b0 + jb) * tk + lc] = (uint32_t)c;
-    const int bit = ((r & 15) << 2) | (lc & 3);
-    const int mine = (lc >> 2) * nbrow + (r >> 4);
-    const uint64_t* pt = s_pt + jb * nbk;
-    uint32_t o = 0;
-    for (int i = 0; i < mine; ++i) o += __popcll(pt[i]);
-    o += __popcll(pt[mine] & ((1ull << bit) - 1ull));
-    reinterpret_cast<float*>(packed + s_vbase[jb])[o] = v;
+  constexpr int kBatch = 8;  // loads of 8 rounds in flight before any use
+  for (int64_t eb = e0; eb < e1; eb += 32 * kBatch) {
+    uint32_t qb[kBatch];
+    int32_t cb[kBatch];
+    float vb[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int64_t e = eb + 32 * u + lane;
+      qb[u] = e < e1 ? q[e] : 0xFFFFFFFFu;
+      cb[u] = e < e1 ? ci[e] : 0;
+      vb[u] = e < e1 ? vals[e] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int64_t e = eb + 32 * u + lane;
+      const uint32_t qq = qb[u];
+      if (qq >= nact) continue;  // past the panel, or invalid CSR input
+      const int r = row_of(s_rp, nrows, e);
+      const uint32_t jb = qq / tk, lc = qq % tk;
+      ac[((int64_t)b0 + jb) * tk + lc] = (uint32_t)cb[u];
+      const int bit = ((r & 15) << 2) | (lc & 3);
+      const int mine = (lc >> 2) * nbrow + (r >> 4);
+      const uint32_t o = s_soff[jb * nbk + mine] + __popcll(s_pt[jb * nbk + mine] & ((1ull << bit) - 1ull));
+      reinterpret_cast<float*>(packed + s_vbase[jb])[o] = vb[u];
+    }
   }
   __syncwarp();
 }
 
 template <int CAP>
 __host__ __device__ constexpr int emit_warp_smem(int tm, int tk) {
-  return (int)((((tm + 2) & ~1) * 8 + (CAP / 16) * 8 + (CAP / tk) * (tk / 4) * (tm / 16) * 8 + 15) & ~15);
+  return (int)((((tm + 2) & ~1) * 8 + (CAP / 16) * 8 + (CAP / tk) * (tk / 4) * (tm / 16) * (8 + 2) + 15) & ~15);
 }
 
 __device__ __forceinline__ int64_t panel_entries(const int64_t* __restrict__ rp, int64_t M, int64_t nnz, int tm,

@@ -179,7 +179,7 @@ float run(const CUtensorMap& tm, const float* B, int ncols, const uint32_t* rows
   return ms / 3;
 }
 
-int main() {
+int main(int argc, char** argv) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const int ncols = 128;  // 512-B rows
@@ -200,8 +200,18 @@ int main() {
   ((EncodeFn)fn)(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, B, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  for (int window : {1 << 14, 1 << 20, -1}) {  // 8 MB (L2), 512 MB (DRAM), banded c2a-like
+  std::vector<uint32_t> file_rows;
+  if (argc > 1) {  // real activeCols replay: uint32 [nsm][nblk][16], sentinel rows mapped to row 0
+    FILE* f = fopen(argv[1], "rb");
+    file_rows.resize((size_t)nsm * nblk * 16);
+    size_t got = fread(file_rows.data(), 4, file_rows.size(), f);
+    fclose(f);
+    printf("replaying %zu rows from %s\n", got, argv[1]);
+  }
+  for (int window : {1 << 14, 1 << 20, -1, -2}) {  // 8 MB (L2), 512 MB (DRAM), banded c2a-like, file
+    if (window == -2 && file_rows.empty()) continue;
     std::vector<uint32_t> h((size_t)nsm * nblk * 16);
+    if (window == -2) h = file_rows;
     srand(1);
     if (window > 0) {
       for (auto& x : h) x = (uint32_t)(((uint64_t)rand() * 2654435761ull) % window);

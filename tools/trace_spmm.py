@@ -15,6 +15,7 @@ for a, b in [("issue", "a_ready"), ("a_ready", "dec_done"), ("issue", "b_ready")
     print(f"{a:>9s} -> {b:<9s}: median {np.median(d):8.0f}  p90 {np.percentile(d, 90):8.0f} cycles")
 iss = np.diff(ev["issue"])
 print(f"issue interval median {np.median(iss):.0f} cycles; mma interval median {np.median(np.diff(ev['mma'])):.0f}")
-print("first 24 blocks (cycles rel. to first issue):")
-for i in range(min(24, n)):
+start = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+print(f"blocks {start}..{start + 24} (cycles rel. to first issue):")
+for i in range(start, min(start + 24, n)):
     print(i, " ".join(f"{ev[k][i]:9.0f}" for k in ["issue", "a_ready", "dec_done", "b_ready", "mma"]))
