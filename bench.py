@@ -234,6 +234,25 @@ def run_ours(args, rank, world, local_rank):
     C_d = torch.empty((M0, NCOL), dtype=torch.float32, device=dev)
 
     stream = torch.cuda.current_stream()
+    tm_plan = None
+    if args.tm == 0:  # plan: time one build + spmm per candidate TM (untimed, like a library autotuner)
+        tm_plan = {}
+        for cand in (16, 32, 64):
+            for it in range(3):
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                A = hp.build(rp_d, ci_d, v_d, M0, K0, tm=cand)
+                hp.spmm(A, B_d, out=C_d)
+                s1.record(stream)
+                torch.cuda.synchronize()
+                A.free()
+            tm_plan[cand] = round(s0.elapsed_time(s1), 4)
+        best = min(tm_plan, key=tm_plan.get)
+        if world > 1:  # every rank uses rank 0's choice
+            t = torch.tensor([best], device=dev)
+            dist.broadcast(t, src=0)
+            best = int(t.item())
+        args.tm = best
 
     def step(evs=None):
         if evs is not None:
@@ -366,6 +385,7 @@ def run_ours(args, rank, world, local_rank):
                        "bricks": bricks, "alpha": round(alpha, 4), "sum_nact": sum_nact, "distinct_cols": uniq,
                        "parallelism": f"row-panel shards x{world}, B broadcast once (NCCL)",
                        "step": "hrpb_build (CSR->HRPB) + hrpb_spmm", "TM": args.tm, "TK": 16,
+                       "tm_plan_ms": tm_plan,
                        "l2": "inputs larger than L2 (CSR 134 MB + B 512 MB per rank)",
                        "build_ms": round(build_ms, 4), "spmm_ms": round(spmm_ms, 4),
                        "spmm_only_gflops": round(flops / (spmm_ms / 1e3) / 1e9, 1),
@@ -388,7 +408,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--tm", type=int, default=16, help="HRPB panel height TM (16 = paper default; 32/64 NEXT-1)")
+    ap.add_argument("--tm", type=int, default=0,
+                    help="HRPB panel height TM: 16 (paper default), 32, 64, or 0 = pick the fastest in an untimed plan step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank, world, local_rank = env_rank()

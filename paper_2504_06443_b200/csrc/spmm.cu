@@ -48,8 +48,9 @@ struct SpmmParams {
   int debug;         // HRPB_DEBUG bits (experiments only): 1 = skip C stores, 2 = skip decode, 4 = skip A copy wait
 };
 constexpr int kTraceN = 1024;
+constexpr int kTraceSlots = 8;
 // trace slots: 0 producer issue (after empty), 1 A arrived (decoder), 2 decode done, 3 B arrived (MMA),
-//              4 MMA issued, 5 epilogue got tfull (per panel)
+//              4 MMA issued, 5 epilogue got tfull (per panel), 6 decoder slot table done, 7 decoder rows done
 __device__ __forceinline__ void trace_ev(const SpmmParams& p, int slot, uint32_t i) {
   if (p.trace != nullptr && blockIdx.x == 0 && i < kTraceN) p.trace[slot * kTraceN + i] = clock64();
 }
@@ -140,7 +141,9 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   using L = SmemLayout<NT, TMV>;
   constexpr int kARawBytes = L::kARawBytes, kATileBytes = L::kATileBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-B alignment by pointer arithmetic on the __shared__ array (an integer round trip would make every
+  // derived pointer generic: LD.E/ST.E instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = prm.stages;
   uint8_t* btile0 = smem;                                 // S x kBTile (1024-aligned)
   uint8_t* araw0 = smem + (size_t)S * L::kBTile;          // S x kARawBytes
@@ -154,6 +157,9 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   uint64_t* tempty = tfull + 2;
   uint32_t* misc = (uint32_t*)(tempty + 2);  // [0] tmem base, [2..3] panel range
   int64_t* range = (int64_t*)(misc + 2);
+  // per decoder warp: brick-slot table (pattern, value offset) of the block being decoded
+  uint64_t* slot_pat = (uint64_t*)(range + 2);                 // [kDecWarps][kNbk]
+  uint32_t* slot_off = (uint32_t*)(slot_pat + kDecWarps * L::kNbk);  // [kDecWarps][kNbk]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t tmem_cols = L::kTmemCols;
@@ -321,74 +327,59 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       const uint32_t hdr = (5 + nbr + 7) & ~7u;
       const uint64_t* pats = reinterpret_cast<const uint64_t*>(blk + hdr);
       const float* vals = reinterpret_cast<const float*>(blk + hdr + 8 * nbr);
-      if constexpr (L::kNbrow == 1) {
-        // TM = 16: at most one brick per brick column; all four patterns first, then the values
-        uint64_t pt[4];
+      // (1) slot table: lane k < nbr owns stored brick k (CSC order); value offset = exclusive scan of popcounts
+      uint64_t* tpat = slot_pat + dw * L::kNbk;
+      uint32_t* toff = slot_off + dw * L::kNbk;
+      if (lane < L::kNbk) tpat[lane] = 0ull;
+      __syncwarp();
+      uint64_t mypat = 0ull;
+      uint32_t mycnt = 0, myslot = 0;
+      if ((uint32_t)lane < nbr) {
+        mypat = pats[lane];
+        uint32_t bc = 0;
 #pragma unroll
-        for (int bc = 0; bc < 4; ++bc) {
-          const uint32_t k0 = (cp >> (8 * bc)) & 0xFF;
-          const uint32_t k1 = bc < 3 ? (cp >> (8 * (bc + 1))) & 0xFF : nbr;
-          pt[bc] = k1 > k0 ? pats[k0] : 0ull;
-        }
-        uint32_t off = 0;
-        float v0[4], v1[4];
+        for (int c = 1; c < 4; ++c) bc += (uint32_t)lane >= ((cp >> (8 * c)) & 0xFF);
+        myslot = bc * L::kNbrow + (L::kNbrow == 1 ? 0u : (uint32_t)blk[5 + lane]);
+        mycnt = __popcll(mypat);
+      }
+      uint32_t incl = mycnt;
 #pragma unroll
-        for (int bc = 0; bc < 4; ++bc) {
-          const uint32_t lo = (uint32_t)pt[bc], hi = (uint32_t)(pt[bc] >> 32);
-          v0[bc] = ((lo >> lane) & 1u) ? vals[off + __popc(lo & below)] : 0.f;
-          v1[bc] = ((hi >> lane) & 1u) ? vals[off + __popc(lo) + __popc(hi & below)] : 0.f;
-          off += __popc(lo) + __popc(hi);
-        }
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if ((uint32_t)lane < nbr) {
+        tpat[myslot] = mypat;
+        toff[myslot] = incl - mycnt;
+      }
+      __syncwarp();
+      if (lane == 0) trace_ev(prm, 6, (uint32_t)(b - b_begin));
+      // (2) lane = tile row r (and r + 32): per brick column, the row's 4-bit nibble of the pattern gives up to
+      // 4 values at rank positions; one 16-B store per (row, brick column) into the K-major tile
 #pragma unroll
-        for (int bc = 0; bc < 4; ++bc) {
-          tile[bc * 64 + lane] = to_tf32_rna(v0[bc]);
-          tile[bc * 64 + 32 + lane] = to_tf32_rna(v1[bc]);
-        }
-      } else {
-        // TM > 16: lane k < nbr owns stored brick k (pattern, slot bc*nbrow + br, value offset by warp scan);
-        // each brick is then expanded by the whole warp from shuffled metadata; absent slots get zeros.
-        uint64_t mypat = 0ull;
-        uint32_t myslot = 0, mycnt = 0;
-        if ((uint32_t)lane < nbr) {
-          mypat = pats[lane];
-          const uint32_t br = blk[5 + lane];
-          uint32_t bc = 0;
+      for (int rr = 0; rr < (TMV + 31) / 32; ++rr) {
+        const int r = lane + 32 * rr;
+        if (r < TMV) {
+          const int br = r >> 4, sh = (r & 15) * 4;
 #pragma unroll
-          for (int c = 1; c < 4; ++c) bc += (uint32_t)lane >= ((cp >> (8 * c)) & 0xFF);
-          myslot = bc * L::kNbrow + br;
-          mycnt = __popcll(mypat);
-        }
-        uint32_t myoff = mycnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, myoff, o);
-          if (lane >= o) myoff += y;
-        }
-        myoff -= mycnt;  // exclusive prefix = value offset of brick `lane`
-        uint32_t present = 0;  // bit per slot
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          if ((uint32_t)k >= nbr) break;
-          const uint32_t slot = __shfl_sync(0xffffffffu, myslot, k);
-          const uint32_t off = __shfl_sync(0xffffffffu, myoff, k);
-          const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)mypat, k);
-          const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(mypat >> 32), k);
-          const float a0 = ((lo >> lane) & 1u) ? vals[off + __popc(lo & below)] : 0.f;
-          const float a1 = ((hi >> lane) & 1u) ? vals[off + __popc(lo) + __popc(hi & below)] : 0.f;
-          const uint32_t bc = slot / L::kNbrow, br = slot % L::kNbrow;
-          tile[bc * (L::kLbo / 4) + br * 64 + lane] = to_tf32_rna(a0);
-          tile[bc * (L::kLbo / 4) + br * 64 + 32 + lane] = to_tf32_rna(a1);
-          present |= 1u << slot;
-        }
-#pragma unroll
-        for (int i = 0; i < L::kNbk; ++i) {
-          if (!((present >> i) & 1u)) {
-            const int bc = i / L::kNbrow, br = i % L::kNbrow;
-            tile[bc * (L::kLbo / 4) + br * 64 + lane] = 0.f;
-            tile[bc * (L::kLbo / 4) + br * 64 + 32 + lane] = 0.f;
+          for (int bc = 0; bc < 4; ++bc) {
+            const int slot = bc * L::kNbrow + br;
+            const uint64_t pt = tpat[slot];
+            const uint32_t nib = (uint32_t)(pt >> sh) & 0xFu;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (nib) {
+              const uint32_t base = toff[slot] + (uint32_t)__popcll(pt & ((1ull << sh) - 1ull));
+              const uint32_t b1 = nib & 1u, b2 = (nib >> 1) & 1u, b3 = (nib >> 2) & 1u;
+              if (b1) v.x = to_tf32_rna(vals[base]);
+              if (b2) v.y = to_tf32_rna(vals[base + b1]);
+              if (b3) v.z = to_tf32_rna(vals[base + b1 + b2]);
+              if (nib & 8u) v.w = to_tf32_rna(vals[base + b1 + b2 + b3]);
+            }
+            *reinterpret_cast<float4*>(tile + bc * (L::kLbo / 4) + br * 64 + (r & 15) * 4) = v;
           }
         }
       }
+      if (lane == 0) trace_ev(prm, 7, (uint32_t)(b - b_begin));
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -440,7 +431,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       ++pc;
     }
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 9..12)
+    // ---------------------------------------------------------------- epilogue (last 4 warps)
     const int qd = warp & 3;            // TMEM lane quadrant accessible to this warp
     const int et = tid - 32 * kEpiWarp0;  // 0..127
     const int64_t ncols = min((int64_t)128 * NT, N - n0);
@@ -528,9 +519,9 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   if (stages > kMaxStages) stages = kMaxStages;
   // producer warp w (and decoder warp w) owns blocks i = w mod 4; with S a multiple of 4 every stage is
   // only ever filled by one warp, so a warp running ahead cannot alias an mbarrier phase.
-  stages -= stages % kProdWarps;
-  static_assert(kProdWarps == kDecWarps, "stage ownership assumes equal producer/decoder warp counts");
-  const size_t smem = 1024 + (size_t)stages * L::kStage + (4 * stages + 4) * 8 + 64;
+  stages -= stages % kDecWarps;  // (kDecWarps is a multiple of kProdWarps)
+  static_assert(kDecWarps % kProdWarps == 0, "stage ownership: decoder count must be a multiple of producers");
+  const size_t smem = 1024 + (size_t)stages * L::kStage + (4 * stages + 4) * 8 + 64 + kDecWarps * L::kNbk * 12;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -540,8 +531,8 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   static const char* trace_path = getenv("HRPB_TRACE");
   long long* trace = nullptr;
   if (trace_path) {
-    trace = (long long*)dalloc(6 * kTraceN * sizeof(long long), s);
-    cudaMemsetAsync(trace, 0, 6 * kTraceN * sizeof(long long), s);
+    trace = (long long*)dalloc(kTraceSlots * kTraceN * sizeof(long long), s);
+    cudaMemsetAsync(trace, 0, kTraceSlots * kTraceN * sizeof(long long), s);
   }
   static const int debug = [] {
     const char* e = getenv("HRPB_DEBUG");
@@ -553,7 +544,7 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   k_spmm<NT, GM, TMV><<<grid, kSpmmThreads, smem, s>>>(tm, prm);
   note_launch();
   if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)
-    static long long host[6 * kTraceN];
+    static long long host[kTraceSlots * kTraceN];
     cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     if (FILE* f = fopen(trace_path, "wb")) {
@@ -616,13 +607,17 @@ hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float
     case 3: st = launch_nt<3, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
     default: st = launch_nt<4, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;              \
   }
-    if (gm == 0 && h->tm == 16) {  // TMA gather4 variant (diagnostic, TM = 16 only)
-      switch (nt) {
-        case 1: st = launch_nt<1, 0, 16>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-        case 2: st = launch_nt<2, 0, 16>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-        case 3: st = launch_nt<3, 0, 16>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-        default: st = launch_nt<4, 0, 16>(h, tm, Bt, ld, C, N, (int)n0, s); break;
-      }
+#define HRPB_LAUNCH_GM0(TMV_)                                                                 \
+  switch (nt) {                                                                               \
+    case 1: st = launch_nt<1, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
+    case 2: st = launch_nt<2, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
+    case 3: st = launch_nt<3, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
+    default: st = launch_nt<4, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;              \
+  }
+    if (gm == 0) {  // TMA tile::gather4 staging
+      if (h->tm == 16) { HRPB_LAUNCH_GM0(16) }
+      else if (h->tm == 32) { HRPB_LAUNCH_GM0(32) }
+      else { HRPB_LAUNCH_GM0(64) }
     } else if (h->tm == 16) {
       HRPB_LAUNCH(16)
     } else if (h->tm == 32) {
@@ -631,6 +626,7 @@ hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float
       HRPB_LAUNCH(64)
     }
 #undef HRPB_LAUNCH
+#undef HRPB_LAUNCH_GM0
     if (st != HRPB_SUCCESS) return st;
   }
   return HRPB_SUCCESS;

@@ -3,13 +3,15 @@ import sys
 import numpy as np
 
 N = 1024
-t = np.fromfile(sys.argv[1], dtype=np.int64).reshape(6, N).astype(np.float64)
+raw = np.fromfile(sys.argv[1], dtype=np.int64)
+t = raw.reshape(raw.size // N, N).astype(np.float64)
 valid = (t[0] > 0) & (t[4] > 0)
 n = int(valid.sum())
 t0 = t[0][valid].min()
-ev = {k: t[i][:n] - t0 for i, k in enumerate(["issue", "a_ready", "dec_done", "b_ready", "mma", "tfull"])}
+names = ["issue", "a_ready", "dec_done", "b_ready", "mma", "tfull", "dec_table", "dec_rows"][:t.shape[0]]
+ev = {k: t[i][:n] - t0 for i, k in enumerate(names)}
 print(f"blocks traced: {n}")
-for a, b in [("issue", "a_ready"), ("a_ready", "dec_done"), ("issue", "b_ready"), ("dec_done", "mma"),
+for a, b in [("issue", "a_ready"), ("a_ready", "dec_table"), ("dec_table", "dec_rows"), ("dec_rows", "dec_done"), ("a_ready", "dec_done"), ("issue", "b_ready"), ("dec_done", "mma"),
              ("b_ready", "mma"), ("issue", "mma")]:
     d = ev[b] - ev[a]
     print(f"{a:>9s} -> {b:<9s}: median {np.median(d):8.0f}  p90 {np.percentile(d, 90):8.0f} cycles")
