@@ -28,10 +28,14 @@ namespace hrpb {
 
 constexpr int kProdWarps = 4;                              // warps 0..3: gather producers
 constexpr int kDecWarps = 4;                               // warps 4..7: brick decoders
-constexpr int kMmaWarp = kProdWarps + kDecWarps;           // warp 8: TMEM alloc + MMA issue
-constexpr int kEpiWarp0 = kMmaWarp + 1;                    // warps 9..12: epilogue
-constexpr int kSpmmThreads = 32 * (kEpiWarp0 + 4);        // 416
-constexpr int kMaxStages = 20;
+constexpr int kMmaWarp = kProdWarps + kDecWarps;           // warp 8: TMEM alloc; warps 8..9: MMA issue
+#ifndef HRPB_MMA_WARPS
+#define HRPB_MMA_WARPS 2
+#endif
+constexpr int kMmaWarps = HRPB_MMA_WARPS;                  // non-empty panel pc -> MMA warp 8 + pc % 2
+constexpr int kEpiWarp0 = kMmaWarp + kMmaWarps;            // warps 10..13: epilogue
+constexpr int kSpmmThreads = 32 * (kEpiWarp0 + 4);        // 448
+constexpr int kMaxStages = 24;
 
 struct SpmmParams {
   const uint32_t* brp;
@@ -45,14 +49,34 @@ struct SpmmParams {
   int n0;      // first output column of this launch
   int stages;  // pipeline depth
   long long* trace;  // optional: per-block event timestamps of CTA 0 (HRPB_TRACE), [6][kTraceN]
-  int debug;         // HRPB_DEBUG bits (experiments only): 1 = skip C stores, 2 = skip decode, 4 = skip A copy wait
+  int debug;         // HRPB_DEBUG bits (experiments only): 1 = skip C stores, 2 = skip decode, 4 = skip MMA issue,
+                     // 8 = skip A bulk copy, 16 = B gather zero-fill only (no global reads), 32 = no B cp.async at all
 };
 constexpr int kTraceN = 1024;
-constexpr int kTraceSlots = 8;
+constexpr int kTraceSlots = 9;  // slot 8: per warp of CTA 0 {cycles waiting on mbarriers, cycles total}
 // trace slots: 0 producer issue (after empty), 1 A arrived (decoder), 2 decode done, 3 B arrived (MMA),
 //              4 MMA issued, 5 epilogue got tfull (per panel), 6 decoder slot table done, 7 decoder rows done
+// Instrumentation (HRPB_TRACE timestamps, HRPB_DEBUG work-skipping bits) exists only in builds with
+// -DHRPB_INSTRUMENT=1 (tools/build_variant.py); the product kernel carries none of it: the serial MMA/decoder
+// loops are sensitive to every extra instruction.
+#ifndef HRPB_INSTRUMENT
+#define HRPB_INSTRUMENT 0
+#endif
+constexpr bool kInstr = HRPB_INSTRUMENT != 0;
+__device__ __forceinline__ bool dbg(const SpmmParams& p, int bit) { return kInstr && (p.debug & bit); }
+__device__ __forceinline__ bool tracing(const SpmmParams& p) { return kInstr && p.trace != nullptr; }
 __device__ __forceinline__ void trace_ev(const SpmmParams& p, int slot, uint32_t i) {
-  if (p.trace != nullptr && blockIdx.x == 0 && i < kTraceN) p.trace[slot * kTraceN + i] = clock64();
+  if (tracing(p) && blockIdx.x == 0 && i < kTraceN) p.trace[slot * kTraceN + i] = clock64();
+}
+// mbarrier wait that accumulates the cycles spent waiting when tracing (role busy/idle breakdown)
+__device__ __forceinline__ void mbar_wait_acc(const SpmmParams& p, uint64_t* bar, uint32_t parity, long long& acc) {
+  if (tracing(p)) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, parity);
+  }
 }
 
 // instruction descriptor: D F32, A/B TF32, A MN-major, B K-major, N = TM (panel rows), M = 128
@@ -73,7 +97,11 @@ struct SmemLayout {
   static constexpr int kATileBytes = TMV * 16 * 4;   // TM x 16 fp32 decoded block
   static constexpr int kLbo = TMV * 16;              // bytes between 4-column K groups of the decoded tile
   static constexpr int kStage = kBTile + kARawBytes + kATileBytes;
-  static constexpr uint32_t kTmemCols = 2 * NT * TMV <= 32 ? 32 : (2 * NT * TMV <= 64 ? 64 : (2 * NT * TMV <= 128 ? 128 : (2 * NT * TMV <= 256 ? 256 : 512)));
+  // TMEM accumulator slots (panels in flight between the MMA warp and the epilogue): up to 4
+  static constexpr int kSlots = 4 * NT * TMV <= 512 ? 4 : 2;
+  static_assert(kSlots % kMmaWarps == 0, "a TMEM slot must always be used by the same MMA warp");
+  static constexpr int kSlotCols = kSlots * NT * TMV;
+  static constexpr uint32_t kTmemCols = kSlotCols <= 32 ? 32 : (kSlotCols <= 64 ? 64 : (kSlotCols <= 128 ? 128 : (kSlotCols <= 256 ? 256 : 512)));
   static_assert(2 * NT * TMV <= 512, "two TMEM accumulator slots must fit in 512 columns");
 };
 
@@ -151,33 +179,37 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   uint64_t* bars = (uint64_t*)(atile0 + (size_t)S * kATileBytes);
   uint64_t* full_a = bars;
   uint64_t* full_b = bars + S;
-  uint64_t* dec = bars + 2 * S;
-  uint64_t* empty = bars + 3 * S;
-  uint64_t* tfull = bars + 4 * S;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* misc = (uint32_t*)(tempty + 2);  // [0] tmem base, [2..3] panel range
+  uint64_t* empty = bars + 2 * S;
+  uint64_t* tfull = bars + 3 * S;
+  uint64_t* tempty = tfull + 4;
+  uint32_t* misc = (uint32_t*)(tempty + 4);  // [0] tmem base, [2..3] panel range
   int64_t* range = (int64_t*)(misc + 2);
+  volatile uint32_t* mma_prog = (volatile uint32_t*)(range + 2);  // [kMmaWarps] next block each MMA warp waits for
   // per decoder warp: brick-slot table (pattern, value offset) of the block being decoded
-  uint64_t* slot_pat = (uint64_t*)(range + 2);                 // [kDecWarps][kNbk]
+  uint64_t* slot_pat = (uint64_t*)(range + 2 + kMmaWarps);     // [kDecWarps][kNbk]
   uint32_t* slot_off = (uint32_t*)(slot_pat + kDecWarps * L::kNbk);  // [kDecWarps][kNbk]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  long long wacc = 0;
+  const long long t_start = kInstr ? clock64() : 0;
   const uint32_t tmem_cols = L::kTmemCols;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_a[s], 1);
-      mbar_init(&full_b[s], GM == 0 ? 1 : 32);  // one producer warp per block
-      mbar_init(&dec[s], 1);
+      // B rows landed (one producer warp per block: 1 expect_tx arrive or 32 cp.async noinc arrivals) AND the
+      // block's A tile is decoded (+1 decoder arrival): the MMA warp waits on this single barrier per block
+      mbar_init(&full_b[s], (GM == 0 ? 1 : 32) + 1);
       mbar_init(&empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < L::kSlots; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     fence_mbar_init();
     // S1: contiguous panel range with ~equal (blocks + panels)
     const uint64_t W = (uint64_t)prm.NB + (uint64_t)prm.P;
     const uint64_t G = gridDim.x, c = blockIdx.x;
     range[0] = panel_lower_bound(prm.brp, prm.P, c * W / G);
     range[1] = c + 1 == G ? prm.P : panel_lower_bound(prm.brp, prm.P, (c + 1) * W / G);
+    for (int m = 0; m < kMmaWarps; ++m) mma_prog[m] = 0u;
     prefetch_tmap(&tmB);
   }
   if (warp == kMmaWarp) tmem_alloc(&misc[0], tmem_cols);
@@ -246,12 +278,16 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
         const int64_t b = first + 4 * j;
         if (b >= b_end) break;
         const uint64_t s0 = __shfl_sync(0xffffffffu, scur, j), s1 = __shfl_sync(0xffffffffu, scur, 8 + j);
-        mbar_wait(&empty[s], ph ^ 1);
+        mbar_wait_acc(prm, &empty[s], ph ^ 1, wacc);
         if (lane == 0) {
           trace_ev(prm, 0, (uint32_t)(b - b_begin));
           const uint32_t a_bytes = (uint32_t)(s1 - s0);
-          mbar_expect_tx(&full_a[s], a_bytes);
-          bulk_g2s(araw0 + (size_t)s * kARawBytes, pk + s0, a_bytes, &full_a[s], pol_a);
+          if (dbg(prm, 8)) {
+            mbar_arrive(&full_a[s]);
+          } else {
+            mbar_expect_tx(&full_a[s], a_bytes);
+            bulk_g2s(araw0 + (size_t)s * kARawBytes, pk + s0, a_bytes, &full_a[s], pol_a);
+          }
         }
         const uint32_t bt = bt0 + s * L::kBTile;
         const uint32_t r = acur[j];
@@ -280,8 +316,9 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
           // Lane-constant parts (offsets per row%4, column bound) are hoisted out of the block loop.
 #pragma unroll
           for (int rw = 0; rw < 16; ++rw) {
+            if (dbg(prm, 32)) break;
             const uint32_t rk = __shfl_sync(0xffffffffu, r, rw);
-            const bool real = rk < Kr;  // sentinel K -> zero fill
+            const bool real = rk < Kr && !(dbg(prm, 16));  // sentinel K -> zero fill
             const float* src = Bsrc + (int64_t)(real ? rk : 0) * ldb + 4 * lane;
             const uint32_t rowb = bt + (rw >> 2) * (L::kNA * 512) + (rw & 3) * 128;
 #pragma unroll
@@ -291,7 +328,8 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
               }
             }
           }
-          cp_async_arrive_noinc(&full_b[s]);
+          if (dbg(prm, 32)) mbar_arrive(&full_b[s]);
+          else cp_async_arrive_noinc(&full_b[s]);
         }
         s += 4;
         if (s >= S) { s -= S; ph ^= 1; }
@@ -307,15 +345,16 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     // the values, so the per-block latency is ~3 dependent shared loads.
     const int dw = warp - kProdWarps;
     const int64_t b_begin = brp[pa], b_end = brp[pb];
-    const uint32_t below = (1u << lane) - 1u;
+    const uint32_t nib_sh = (uint32_t)(lane & 15) * 4u;            // tile row r with r % 16 == lane % 16
+    const uint64_t below_row = (1ull << nib_sh) - 1ull;            // pattern bits of the rows above it
     int s = dw % S;
     uint32_t ph = (dw / S) & 1;
     for (int64_t b = b_begin + dw; b < b_end; b += kDecWarps) {
-      mbar_wait(&full_a[s], ph);
+      mbar_wait_acc(prm, &full_a[s], ph, wacc);
       if (lane == 0) trace_ev(prm, 1, (uint32_t)(b - b_begin));
-      if (prm.debug & 2) {
+      if (dbg(prm, 2)) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&dec[s]);
+        if (lane == 0) mbar_arrive(&full_b[s]);
         s += kDecWarps;
         if (s >= S) { s -= S; ph ^= 1; }
         continue;
@@ -330,7 +369,10 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       // (1) slot table: lane k < nbr owns stored brick k (CSC order); value offset = exclusive scan of popcounts
       uint64_t* tpat = slot_pat + dw * L::kNbk;
       uint32_t* toff = slot_off + dw * L::kNbk;
-      if (lane < L::kNbk) tpat[lane] = 0ull;
+      if (lane < L::kNbk) {  // absent bricks: pattern 0, offset 0 (their loads below stay in bounds)
+        tpat[lane] = 0ull;
+        toff[lane] = 0u;
+      }
       __syncwarp();
       uint64_t mypat = 0ull;
       uint32_t mycnt = 0, myslot = 0;
@@ -354,29 +396,51 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       }
       __syncwarp();
       if (lane == 0) trace_ev(prm, 6, (uint32_t)(b - b_begin));
-      // (2) lane = tile row r (and r + 32): per brick column, the row's 4-bit nibble of the pattern gives up to
-      // 4 values at rank positions; one 16-B store per (row, brick column) into the K-major tile
+      // (2) item q = lane + 32 j (j < TM/8) is (tile row r = q % TM, brick column bc = q / TM): the row's 4-bit
+      // nibble of the brick pattern selects up to 4 values at prefix-popcount ranks; one 16-B store
+      // per item into the K-major tile. Branch-free: every item's loads are issued before any is consumed, so a
+      // block costs ~3 dependent shared-memory round trips (a divergent per-item branch serialised them).
+      constexpr int kItems = TMV / 8;
+#ifndef HRPB_DEC_CHUNK
+#define HRPB_DEC_CHUNK 8
+#endif
+      constexpr int kChunk = kItems < HRPB_DEC_CHUNK ? kItems : HRPB_DEC_CHUNK;  // items in flight per lane
+      const uint32_t* __restrict__ uvals = reinterpret_cast<const uint32_t*>(vals);
 #pragma unroll
-      for (int rr = 0; rr < (TMV + 31) / 32; ++rr) {
-        const int r = lane + 32 * rr;
-        if (r < TMV) {
-          const int br = r >> 4, sh = (r & 15) * 4;
+      for (int j0 = 0; j0 < kItems; j0 += kChunk) {
+        uint64_t ipat[kChunk];
+        uint32_t ioff[kChunk];
 #pragma unroll
-          for (int bc = 0; bc < 4; ++bc) {
-            const int slot = bc * L::kNbrow + br;
-            const uint64_t pt = tpat[slot];
-            const uint32_t nib = (uint32_t)(pt >> sh) & 0xFu;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (nib) {
-              const uint32_t base = toff[slot] + (uint32_t)__popcll(pt & ((1ull << sh) - 1ull));
-              const uint32_t b1 = nib & 1u, b2 = (nib >> 1) & 1u, b3 = (nib >> 2) & 1u;
-              if (b1) v.x = to_tf32_rna(vals[base]);
-              if (b2) v.y = to_tf32_rna(vals[base + b1]);
-              if (b3) v.z = to_tf32_rna(vals[base + b1 + b2]);
-              if (nib & 8u) v.w = to_tf32_rna(vals[base + b1 + b2 + b3]);
-            }
-            *reinterpret_cast<float4*>(tile + bc * (L::kLbo / 4) + br * 64 + (r & 15) * 4) = v;
-          }
+        for (int jj = 0; jj < kChunk; ++jj) {
+          const int q = lane + 32 * (j0 + jj), r = q % TMV, bc = q / TMV;
+          const int slot = bc * L::kNbrow + (r >> 4);
+          ipat[jj] = tpat[slot];
+          ioff[jj] = toff[slot];
+        }
+        uint4 iv[kChunk];
+        uint32_t inib[kChunk];
+#pragma unroll
+        for (int jj = 0; jj < kChunk; ++jj) {
+          // row r % 16 == lane % 16 for every item of this lane: the nibble shift and the below-mask are constant
+          const uint32_t nib = (uint32_t)(ipat[jj] >> nib_sh) & 0xFu;
+          const uint32_t i0 = ioff[jj] + (uint32_t)__popcll(ipat[jj] & below_row);
+          const uint32_t i1 = i0 + (nib & 1u), i2 = i1 + ((nib >> 1) & 1u), i3 = i2 + ((nib >> 2) & 1u);
+          // unselected lanes read at most 3 words past the block's values: still inside the stage ring
+          iv[jj] = make_uint4(uvals[i0], uvals[i1], uvals[i2], uvals[i3]);
+          inib[jj] = nib;
+        }
+#pragma unroll
+        for (int jj = 0; jj < kChunk; ++jj) {
+          const int q = lane + 32 * (j0 + jj), r = q % TMV, bc = q / TMV;
+          const uint32_t nib = inib[jj];
+          // FP32 -> TF32 round-to-nearest (ties away) as integer ops, value kept only where the pattern bit is set
+          // (reading R15; cvt.rna.tf32.f32 is a ~7-instruction emulation on sm_100a). Finite A assumed (R17).
+          uint4 v;
+          v.x = (iv[jj].x + 0x1000u) & ((nib & 1u) ? 0xFFFFE000u : 0u);
+          v.y = (iv[jj].y + 0x1000u) & ((nib & 2u) ? 0xFFFFE000u : 0u);
+          v.z = (iv[jj].z + 0x1000u) & ((nib & 4u) ? 0xFFFFE000u : 0u);
+          v.w = (iv[jj].w + 0x1000u) & ((nib & 8u) ? 0xFFFFE000u : 0u);
+          *reinterpret_cast<uint4*>(tile + bc * (L::kLbo / 4) + (r >> 4) * 64 + (r & 15) * 4) = v;
         }
       }
       if (lane == 0) trace_ev(prm, 7, (uint32_t)(b - b_begin));
@@ -384,52 +448,87 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       __syncwarp();
       if (lane == 0) {
         trace_ev(prm, 2, (uint32_t)(b - b_begin));
-        mbar_arrive(&dec[s]);
+        mbar_arrive(&full_b[s]);
       }
       s += kDecWarps;
       if (s >= S) { s -= S; ph ^= 1; }
     }
-  } else if (warp == kMmaWarp) {
-    // ---------------------------------------------------------------- MMA issuer (one thread)
-    uint32_t i = 0, pc = 0, ph = 0;
-    int st = 0;
-    const uint32_t bt0 = smem_u32(btile0), at0 = smem_u32(atile0);
+  } else if (warp < kEpiWarp0) {
+    // ---------------------------------------------------------------- MMA issuers (one thread per warp)
+    // Non-empty panel pc goes to MMA warp pc % kMmaWarps and TMEM slot pc % kSlots: a single issuing warp spends
+    // several hundred cycles of dependent issue latency per block (wait, 2 MMAs, commit), so two warps overlap.
+    // Blocks of other warps' panels are skipped. A warp publishes in mma_prog the block it is about to wait for
+    // (all its earlier blocks are consumed); before a panel whose last block is i it waits until every other
+    // warp has published a block > i - S, so no stage barrier it waits on can be two phases behind (parity is
+    // unambiguous).
+    const int mw = warp - kMmaWarp;
+    const int64_t b_begin = brp[pa];
+    uint32_t pc = 0;
+    constexpr uint32_t kIdesc = idesc_tf32<TMV>();
+    // descriptors of stage 0; stage s adds s * stage bytes / 16 to the start-address field (no carry: < 256 KB)
+    const uint64_t adesc0 = umma_sdesc(smem_u32(btile0), 512, L::kNA * 512, 1);
+    const uint64_t bdesc0 = umma_sdesc(smem_u32(atile0), L::kLbo, 128, 0);
+    const uint32_t Su = (uint32_t)S;
     PanelCursor cursor(brp, pa, pb, lane);
     int64_t p;
     uint32_t bb, be;
     while (cursor.next(p, bb, be)) {
       if (bb == be) continue;
-      const uint32_t slot = pc & 1;
-      mbar_wait(&tempty[slot], ((pc >> 1) & 1) ^ 1);
+      if ((int)(pc % kMmaWarps) != mw) {
+        ++pc;
+        continue;
+      }
+      const uint32_t slot = pc % L::kSlots;
+      uint32_t i = (uint32_t)(bb - b_begin);  // block index within this CTA's range
+      uint32_t st = i % Su, ph = (i / Su) & 1u;
+      if (kMmaWarps > 1 && lane == 0) {
+        mma_prog[mw] = i;  // all of this warp's blocks before its new panel are consumed
+        const uint32_t last = i + (be - bb) - 1u;
+        if (last >= Su) {
+          const long long tg = tracing(prm) ? clock64() : 0;
+#pragma unroll
+          for (int m = 0; m < kMmaWarps; ++m)
+            if (m != mw)
+              while (mma_prog[m] <= last - Su) {
+              }
+          if (tracing(prm)) wacc += clock64() - tg;
+        }
+      }
+      __syncwarp();
+      mbar_wait_acc(prm, &tempty[slot], ((pc / L::kSlots) & 1) ^ 1, wacc);
       tc_fence_after();
       const uint32_t dcol = tbase + slot * NT * TMV;
       for (uint32_t b = bb; b < be; ++b, ++i) {
-        const int s = st;
-        mbar_wait(&full_b[s], ph);
-        if (lane == 0) trace_ev(prm, 3, i);
-        mbar_wait(&dec[s], ph);
+        const int s = (int)st;
+        if (kMmaWarps > 1 && lane == 0) mma_prog[mw] = i;
+        mbar_wait_acc(prm, &full_b[s], ph, wacc);
         tc_fence_after();
         if (lane == 0) {
+          trace_ev(prm, 3, i);
           trace_ev(prm, 4, i);
-          const uint32_t bt = bt0 + s * L::kBTile, at = at0 + s * kATileBytes;
+          if (dbg(prm, 4)) {
+            mbar_arrive(&empty[s]);
+          } else {
+            const uint64_t ad = adesc0 + (uint64_t)(st * (uint32_t)(L::kBTile >> 4));
+            const uint64_t bd = bdesc0 + (uint64_t)(st * (uint32_t)(kATileBytes >> 4));
 #pragma unroll
-          for (int t = 0; t < NT; ++t) {
+            for (int t = 0; t < NT; ++t) {
 #pragma unroll
-            for (int g = 0; g < 2; ++g) {
-              const uint64_t ad = umma_sdesc(bt + (2 * g * L::kNA + 4 * t) * 512, 512, L::kNA * 512, 1);
-              const uint64_t bd = umma_sdesc(at + g * 2 * L::kLbo, L::kLbo, 128, 0);
-              umma_tf32(dcol + t * TMV, ad, bd, idesc_tf32<TMV>(), (b > bb || g > 0) ? 1u : 0u);
+              for (int g = 0; g < 2; ++g)
+                umma_tf32(dcol + t * TMV, ad + (uint64_t)(((2 * g * L::kNA + 4 * t) * 512) >> 4),
+                          bd + (uint64_t)((g * 2 * L::kLbo) >> 4), kIdesc, (b > bb || g > 0) ? 1u : 0u);
             }
+            umma_commit(&empty[s]);
           }
-          umma_commit(&empty[s]);
         }
         __syncwarp();
-        if (++st == S) { st = 0; ph ^= 1; }
+        if (++st == Su) { st = 0; ph ^= 1; }
       }
       if (lane == 0) umma_commit(&tfull[slot]);
       __syncwarp();
       ++pc;
     }
+    if (kMmaWarps > 1 && lane == 0) mma_prog[mw] = 0xFFFFFFFFu;
   } else {
     // ---------------------------------------------------------------- epilogue (last 4 warps)
     const int qd = warp & 3;            // TMEM lane quadrant accessible to this warp
@@ -447,25 +546,27 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
           for (int64_t c = et; c < ncols; c += 128) prm.C[(row0 + r) * N + n0 + c] = 0.f;
         continue;
       }
-      const uint32_t slot = pc & 1;
-      mbar_wait(&tfull[slot], (pc >> 1) & 1);
+      const uint32_t slot = pc % L::kSlots;
+      mbar_wait_acc(prm, &tfull[slot], (pc / L::kSlots) & 1, wacc);
       if (et == 0) trace_ev(prm, 5, pc);
       tc_fence_after();
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
+        uint32_t v[TMV / 16][16];  // all panel rows of this lane's column: one tcgen05.wait per 128-column tile
 #pragma unroll
-        for (int c16 = 0; c16 < TMV / 16; ++c16) {  // 16 panel rows per tcgen05.ld
-          uint32_t v[16];
-          tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + slot * NT * TMV + t * TMV + c16 * 16, v);
-          tmem_ld_wait();
-          const int64_t c = 128 * t + 32 * qd + lane;
-          if (c < ncols) {
-            float* dst = prm.C + (row0 + 16 * c16) * N + n0 + c;
-            if (!(prm.debug & 1)) {
+        for (int c16 = 0; c16 < TMV / 16; ++c16)
+          tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + slot * NT * TMV + t * TMV + c16 * 16, v[c16]);
+        tmem_ld_wait();
+        const int64_t c = 128 * t + 32 * qd + lane;
+        if (c < ncols && !(dbg(prm, 1))) {
+          float* dst = prm.C + row0 * N + n0 + c;
+          if (nrows == TMV) {
 #pragma unroll
-              for (int r = 0; r < 16; ++r)
-                if (16 * c16 + r < nrows) __stcs(dst + (int64_t)r * N, __uint_as_float(v[r]));
-            }
+            for (int r = 0; r < TMV; ++r) __stcs(dst + (int64_t)r * N, __uint_as_float(v[r >> 4][r & 15]));
+          } else {
+#pragma unroll
+            for (int r = 0; r < TMV; ++r)
+              if (r < nrows) __stcs(dst + (int64_t)r * N, __uint_as_float(v[r >> 4][r & 15]));
           }
         }
       }
@@ -474,6 +575,10 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       if (lane == 0) mbar_arrive(&tempty[slot]);
       ++pc;
     }
+  }
+  if (tracing(prm) && blockIdx.x == 0 && lane == 0) {
+    prm.trace[8 * kTraceN + 2 * warp] = wacc;
+    prm.trace[8 * kTraceN + 2 * warp + 1] = clock64() - t_start;
   }
   tc_fence_before();
   __syncthreads();
@@ -514,28 +619,34 @@ template <int NT, int GM, int TMV>
 static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, const float* B, int64_t ldb, float* C,
                                int64_t N, int n0, cudaStream_t s) {
   using L = SmemLayout<NT, TMV>;
-  const int budget = 227 * 1024 - 1024 /*alignment*/ - 512 /*barriers, misc*/;
-  int stages = budget / L::kStage;
-  if (stages > kMaxStages) stages = kMaxStages;
   // producer warp w (and decoder warp w) owns blocks i = w mod 4; with S a multiple of 4 every stage is
   // only ever filled by one warp, so a warp running ahead cannot alias an mbarrier phase.
-  stages -= stages % kDecWarps;  // (kDecWarps is a multiple of kProdWarps)
   static_assert(kDecWarps % kProdWarps == 0, "stage ownership: decoder count must be a multiple of producers");
-  const size_t smem = 1024 + (size_t)stages * L::kStage + (4 * stages + 4) * 8 + 64 + kDecWarps * L::kNbk * 12;
+  auto smem_for = [](int st) {
+    return (size_t)1024 /*alignment*/ + (size_t)st * L::kStage + (3 * st + 8) * 8 + 64 + 8 * kMmaWarps + kDecWarps * L::kNbk * 12;
+  };
+  int stages = kMaxStages - kMaxStages % kDecWarps;
+  while (stages > kDecWarps && smem_for(stages) > 227 * 1024) stages -= kDecWarps;
+  static const int stage_cap = [] {
+    const char* e = getenv("HRPB_STAGES");  // experiments: cap the pipeline depth (multiple of 4)
+    return e ? atoi(e) : 0;
+  }();
+  if (stage_cap >= kDecWarps && stage_cap < stages) stages = stage_cap - stage_cap % kDecWarps;
+  const size_t smem = smem_for(stages);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return cuda_status(e);
     attr_set = true;
   }
-  static const char* trace_path = getenv("HRPB_TRACE");
+  static const char* trace_path = kInstr ? getenv("HRPB_TRACE") : nullptr;
   long long* trace = nullptr;
   if (trace_path) {
     trace = (long long*)dalloc(kTraceSlots * kTraceN * sizeof(long long), s);
     cudaMemsetAsync(trace, 0, kTraceSlots * kTraceN * sizeof(long long), s);
   }
   static const int debug = [] {
-    const char* e = getenv("HRPB_DEBUG");
+    const char* e = kInstr ? getenv("HRPB_DEBUG") : nullptr;
     return e ? atoi(e) : 0;
   }();
   SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, B, h->K, ldb, n0, stages, trace, debug};

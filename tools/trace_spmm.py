@@ -21,3 +21,11 @@ start = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 print(f"blocks {start}..{start + 24} (cycles rel. to first issue):")
 for i in range(start, min(start + 24, n)):
     print(i, " ".join(f"{ev[k][i]:9.0f}" for k in ["issue", "a_ready", "dec_done", "b_ready", "mma"]))
+if t.shape[0] > 8:
+    nm = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    roles = (["prod"] * 4 + ["dec"] * 4 + ["mma"] * nm + ["epi"] * 4)
+    print("per-warp mbarrier wait share (CTA 0):")
+    for w in range(len(roles)):
+        wt, tot = raw.reshape(-1, N)[8][2 * w], raw.reshape(-1, N)[8][2 * w + 1]
+        if tot > 0:
+            print(f"  warp {w:2d} {roles[w]:4s}: waiting {100.0 * wt / tot:5.1f}% of {tot} cycles")
