@@ -461,6 +461,9 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     // (all its earlier blocks are consumed); before a panel whose last block is i it waits until every other
     // warp has published a block > i - S, so no stage barrier it waits on can be two phases behind (parity is
     // unambiguous).
+    // with NT >= 3 a block is >= 6 MMAs (>= 300 tensor cycles) and one issuing warp keeps up; the skew guard
+    // would only serialise (c5 at N = 512: panels longer than the S = 4 stages)
+    constexpr int kSplit = NT <= 2 ? kMmaWarps : 1;
     const int mw = warp - kMmaWarp;
     const int64_t b_begin = brp[pa];
     uint32_t pc = 0;
@@ -474,20 +477,20 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     uint32_t bb, be;
     while (cursor.next(p, bb, be)) {
       if (bb == be) continue;
-      if ((int)(pc % kMmaWarps) != mw) {
+      if ((int)(pc % kSplit) != mw) {
         ++pc;
         continue;
       }
       const uint32_t slot = pc % L::kSlots;
       uint32_t i = (uint32_t)(bb - b_begin);  // block index within this CTA's range
       uint32_t st = i % Su, ph = (i / Su) & 1u;
-      if (kMmaWarps > 1 && lane == 0) {
+      if (kSplit > 1 && lane == 0) {
         mma_prog[mw] = i;  // all of this warp's blocks before its new panel are consumed
         const uint32_t last = i + (be - bb) - 1u;
         if (last >= Su) {
           const long long tg = tracing(prm) ? clock64() : 0;
 #pragma unroll
-          for (int m = 0; m < kMmaWarps; ++m)
+          for (int m = 0; m < kSplit; ++m)
             if (m != mw)
               while (mma_prog[m] <= last - Su) {
               }
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       const uint32_t dcol = tbase + slot * NT * TMV;
       for (uint32_t b = bb; b < be; ++b, ++i) {
         const int s = (int)st;
-        if (kMmaWarps > 1 && lane == 0) mma_prog[mw] = i;
+        if (kSplit > 1 && lane == 0) mma_prog[mw] = i;
         mbar_wait_acc(prm, &full_b[s], ph, wacc);
         tc_fence_after();
         if (lane == 0) {
