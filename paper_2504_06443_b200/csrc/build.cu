@@ -4,13 +4,17 @@
 // chunks and prefix sums; §"HRPB Sparse Matrix Data structure" defines the output.
 // B200 design: no host round trip until the end; outputs are allocated at
 // upper bounds computable from (M, nnz), so the pipeline is
-//   k_count / k_count_big  (B1 + B3 counting: per-panel sorted-unique active columns -> compacted
-//                           rank q of every entry, nact; brick patterns; block sizes; CSR validation)
-//   scan(nblk) -> blockedRowPtr (B2); scan(panel bytes) -> panel byte offsets (B4, panel level)
-//   k_emit                 (B3 + B4 + B5: activeCols with sentinel K, sizePtr, HRPB-v1 headers,
-//                           patterns, values in brick-CSC / row-major order)
+//   k_wclassify            (panels the warp path cannot take: > wcap entries or a column span wider than its
+//                           bitmap -> listed)
+//   k_count / k_count_big  (B1 + B3 counting per listed panel by a CTA / hub CTAs: ranks q of every entry,
+//                           patterns kept in scratch, nact, nblk, bytes; CSR validation)
+//   k_wbuild               (warp per panel, ticket-ordered: B1 + B3 bitmap ranking and patterns, then the
+//                           single-pass decoupled look-back scans B2 blockedRowPtr / B4 panel byte offsets over
+//                           ALL panels, then B3 + B4 + B5 emission of its panel)
+//   k_emit                 (B3 + B4 + B5 for listed panels: activeCols with sentinel K, sizePtr, HRPB-v1
+//                           headers, patterns, values in brick-CSC / row-major order)
 //   k_finalize             (NUM_BLKS, byte total, status) -> one 32-byte D2H read + sync.
-// Panel p keeps its brick patterns between the two passes in a scratch region addressed from its
+// Listed panel p keeps its brick patterns between the two passes in a scratch region addressed from its
 // first entry offset, base(p) = floor(e0 * nbk / tk) + 2 p nbk, which never overlaps the next panel's.
 #include <cstdio>
 
@@ -32,10 +36,6 @@ constexpr int kSmallCap = 2048;      // entries per panel handled in shared memo
 constexpr int kSpanWords = 512;      // bitmap ranking when the panel's column span <= 16384
 constexpr int kBigThreads = 512;
 constexpr int kEmitThreads = 128;
-constexpr int kWarpCap = 256;        // entries per panel handled by one warp (no CTA barriers)
-constexpr int kWarpSpanWords = 256;  // warp bitmap ranking when the column span < 8192 (bitmap + prefix = s_keys)
-constexpr int kWarpsPerCta = 8;
-constexpr int kWarpCap2 = 1024;      // second warp pass (listed panels, bitmap ranking only)
 
 // ------------------------------------------------------------------ block-wide helpers
 template <int NT>
@@ -172,63 +172,117 @@ __device__ __forceinline__ void warp_panel_rows(const int64_t* __restrict__ rp, 
   __syncwarp();
 }
 
-// ------------------------------------------------------------------ pass A, warp per panel
-// One warp per panel, no CTA barriers: entries live in registers (CAP/32 per lane), ranks come from a
-// per-warp bitmap (column span < 8192) or, when SORT, a warp bitonic sort; patterns via 32-bit shared
-// atomics. Returns 0 when the panel was counted, 1 when it has more than CAP entries, 2 when its column
-// span needs the sort path and SORT is off.
-template <int CAP, bool SORT>
-__device__ __forceinline__ int count_panel_warp(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                                int64_t M, int64_t K, int64_t nnz, int tm, int tk, int64_t p,
-                                                uint32_t* __restrict__ q, uint32_t* __restrict__ nact_out,
-                                                uint32_t* __restrict__ nblk_out, uint32_t* __restrict__ pbytes_out,
-                                                uint64_t* __restrict__ gpat, uint32_t* status, uint8_t* my,
-                                                int64_t& E_out) {
-  constexpr int PER = CAP / 32;
+// ------------------------------------------------------------------ warp-per-panel path (most panels)
+// One warp owns one panel with at most kWCap entries whose column span fits the kWBmWords-word bitmap
+// (c1, c2a/c2b at every TM). k_wbuild ranks, scans and emits in one pass, so no per-entry rank or per-brick
+// pattern array goes through HBM and the CSR is read once (plus L1 re-reads).
+//   ranks ("active_cols = uniq(...)", R23): bitmap over [mn, mn + span) + popcount prefix per word
+//   rows: a per-panel u8 row map in shared memory, each lane filling its own row (no per-entry search)
+//   patterns (P:L132 fill_brick_nnz_pattern; bit = (r % 16) * 4 + q % 4, R3): 32-bit shared atomicOr
+// Panels that do not fit go to the CTA / hub paths (k_count, k_count_big, k_emit), listed by k_wclassify.
+constexpr int kWCap = 1024;       // entries per panel on the warp path (TM = 128: 512, see wcap)
+constexpr int kWBmWords = 256;    // bitmap words: column span <= 8192
+constexpr int kWSlotCap = 256;    // brick slots held at once: patterns are built per chunk of blocks
+constexpr int kWWarps = 4;        // warps per CTA
+
+struct WarpLayout {  // per-warp shared memory (bytes), depends on tm/tk only
+  int slots;         // brick slots per block chunk = kWSlotCap (a chunk is kWSlotCap / nbk blocks)
+  int off_pre, off_row, off_q, off_pat, off_soff, off_vbase, bytes;
+};
+constexpr int kWSortCap = 256;  // wide-span panels with <= 256 entries: warp bitonic sort ranking
+static_assert(kWSortCap * 8 <= 2 * kWBmWords * 4, "sort keys alias the bitmap + prefix words");
+__host__ __device__ constexpr int wcap(int, int) { return kWCap; }
+__host__ __device__ inline WarpLayout warp_layout(int tm, int tk) {  // (also used by the host launcher)
+  const int nbk = (tk / HRPB_BRICK_K) * (tm / HRPB_BRICK_M);
+  WarpLayout L;
+  L.slots = kWSlotCap;
+  L.off_pre = kWBmWords * 4;
+  L.off_row = L.off_pre + kWBmWords * 4;                    // u8 row of each entry
+  L.off_q = L.off_row + kWCap;                              // u16 rank of each entry
+  L.off_pat = L.off_q + 2 * kWCap;                          // 8-B aligned
+  L.off_soff = L.off_pat + L.slots * 8;
+  L.off_vbase = (L.off_soff + L.slots * 2 + 7) & ~7;
+  L.bytes = (L.off_vbase + (kWSlotCap / nbk) * 8 + 15) & ~15;
+  return L;
+}
+
+struct WarpPanel {
+  int64_t p, e0;
+  int E, nrows;
+  int32_t mn;
+  uint32_t nact, nblk;
+  bool sorted;      // rank by warp sort (column span wider than the bitmap, E <= kWSortCap)
+  uint32_t st[4];   // row starts of rows lane + 32k (entry index relative to e0), valid for 1 <= r < nrows
+};
+
+// Loads the panel's row pointers (clamped, monotone-repaired; ST_RP_MONO on a decreasing row_ptr) into
+// per-lane registers and decides whether the warp path takes the panel: E <= kWCap and the column span
+// (first / last entries of the sorted rows) fits the bitmap. Returns false otherwise (warp-uniform).
+template <int tm, int tk>
+__device__ __forceinline__ bool warp_panel_open(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                int64_t M, int64_t nnz, int64_t p, WarpPanel& w,
+                                                uint32_t* status) {
   const int lane = threadIdx.x & 31;
-  uint64_t* s_keys = reinterpret_cast<uint64_t*>(my);                           // SORT ? [CAP] : bitmap 2 KB
-  constexpr int kKeyBytes = SORT ? CAP * 8 : 2 * kWarpSpanWords * 4;
-  uint32_t* s_qb = reinterpret_cast<uint32_t*>(my + kKeyBytes);                  // SORT ? [CAP] : none
-  int64_t* s_rp = reinterpret_cast<int64_t*>(my + kKeyBytes + (SORT ? CAP * 4 : 0));  // [tm + 1]
-  unsigned long long* s_pat = reinterpret_cast<unsigned long long*>(s_rp + ((tm + 2) & ~1));
-  warp_panel_rows(rp, M, nnz, tm, p, s_rp, status);
-  const int nrows = (int)min((int64_t)tm, M - p * tm);
-  const int64_t e0 = s_rp[0];
-  const int64_t E64 = s_rp[nrows] - e0;
-  E_out = E64;
-  if (E64 > CAP) return 1;
-  static_assert(2 * kWarpSpanWords * 4 <= kKeyBytes, "bitmap + prefix must fit in s_keys");
-  const int E = (int)E64;
-  if (E == 0) {
-    if (lane == 0) { nact_out[p] = 0; nblk_out[p] = 0; pbytes_out[p] = 0; }
-    return 0;
+  const int64_t r0 = p * tm;
+  const int nrows = (int)min((int64_t)tm, M - r0);
+  int64_t carry = INT64_MIN;
+  bool bad = false;
+  constexpr int KV = tm / 32 + 1;  // row-pointer registers per lane
+  int64_t v[KV + 1];  // rp[r0 + lane + 32k] (the last used one covers rp[r0 + nrows]); v[KV] = 0 pad
+  const int nk = nrows / 32 + 1;
+  v[KV] = 0;
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    v[k] = 0;
+    if (k >= nk) continue;  // warp-uniform
+    const int i = lane + 32 * k;
+    const bool in = i <= nrows;
+    const int64_t raw = in ? rp[r0 + i] : INT64_MAX;
+    int64_t prev = __shfl_up_sync(0xffffffffu, raw, 1);
+    if (lane == 0) prev = k == 0 ? raw : carry;
+    if (in && raw < prev) bad = true;
+    int64_t x = in ? (raw < 0 ? 0 : (raw > nnz ? nnz : raw)) : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = max(x, y);
+    }
+    if (k > 0) x = max(x, __shfl_sync(0xffffffffu, v[k - 1], 31));
+    v[k] = x;
+    carry = __shfl_sync(0xffffffffu, raw, 31);
   }
-  uint32_t col[PER];
-  int rowv[PER];
+  if (__any_sync(0xffffffffu, bad) && lane == 0 && status) atomicOr(status, ST_RP_MONO);
+  const int last_k = nrows >> 5, last_l = nrows & 31;
+  int64_t e1 = 0, e0 = 0;
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int64_t t = __shfl_sync(0xffffffffu, v[k], last_l);
+    if (k == last_k) e1 = t;
+  }
+  e0 = __shfl_sync(0xffffffffu, v[0], 0);
+  w.p = p;
+  w.e0 = e0;
+  w.nrows = nrows;
+  const int64_t E = e1 - e0;
+  w.E = (int)min(E, (int64_t)kWCap + 1);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = lane + 32 * k;
+    w.st[k] = (k < KV && r >= 1 && r < nrows) ? (uint32_t)(v[k < KV ? k : 0] - e0) : 0xFFFFFFFFu;
+  }
+  if (E > wcap(tm, tk)) return false;
+  // column span from the first and last entry of each row (rows are sorted; a violation is flagged later)
   int32_t mn = INT32_MAX, mx = INT32_MIN;
-  bool bad_range = false, bad_order = false;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {  // all loads first
-    const int idx = lane + 32 * k;
-    col[k] = idx < E ? (uint32_t)ci[e0 + idx] : 0u;
-  }
-  uint32_t prev_last = 0;  // column of entry 32k - 1 (lane 31 of the previous k)
-#pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int idx = lane + 32 * k;
-    uint32_t prevc = __shfl_up_sync(0xffffffffu, col[k], 1);
-    if (lane == 0) prevc = prev_last;
-    prev_last = __shfl_sync(0xffffffffu, col[k], 31);
-    rowv[k] = 0;
-    if (idx < E) {
-      const int64_t e = e0 + idx;
-      const int32_t c = (int32_t)col[k];
-      const int r = row_of(s_rp, nrows, e);
-      rowv[k] = r;
-      bad_range |= c < 0 || c >= K;
-      if (e > s_rp[r] && (int32_t)prevc >= c) bad_order = true;
-      mn = min(mn, c);
-      mx = max(mx, c);
+  for (int k = 0; k < KV - 1 + (tm % 32 != 0); ++k) {
+    const int r = lane + 32 * k;
+    const int64_t a = v[k];
+    const int64_t nx_same = __shfl_sync(0xffffffffu, v[k], (lane + 1) & 31);
+    const int64_t nx_next = __shfl_sync(0xffffffffu, v[k + 1], 0);
+    const int64_t b = lane == 31 ? nx_next : nx_same;  // rp[r + 1]
+    if (r < nrows && b > a) {
+      mn = min(mn, ci[a]);
+      mx = max(mx, ci[b - 1]);
     }
   }
 #pragma unroll
@@ -236,26 +290,87 @@ __device__ __forceinline__ int count_panel_warp(const int64_t* __restrict__ rp, 
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
-  const bool small_span = (int64_t)mx - (int64_t)mn < 32 * kWarpSpanWords;
-  if (!SORT && !small_span) return 2;  // (warp-uniform) handled by the CTA path
-  if (__any_sync(0xffffffffu, bad_range) && lane == 0) atomicOr(status, ST_COL_RANGE);
-  if (__any_sync(0xffffffffu, bad_order) && lane == 0) atomicOr(status, ST_COL_ORDER);
-  uint32_t qv[PER];
-  uint32_t nact = 0;
-  if (small_span) {
-    uint32_t* bm = reinterpret_cast<uint32_t*>(s_keys);
-    uint32_t* pre = bm + kWarpSpanWords;
-    constexpr int kW = kWarpSpanWords / 32;
+  w.mn = mn;
+  w.sorted = false;
+  if (E == 0) return true;
+  if ((int64_t)mx - (int64_t)mn < 32 * kWBmWords) return true;
+  w.sorted = true;
+  return E <= kWSortCap;
+}
+
+// row map: srow[i] = local row of panel entry e0 + i; lane r fills its own row's entries (row ends from the
+// neighbouring lane's start; empty rows write nothing)
+template <int tm>
+__device__ __forceinline__ void warp_row_map(const WarpPanel& w, uint8_t* srow) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int i = 0; i < kW; ++i) bm[lane * kW + i] = 0;
-    __syncwarp();
+  for (int k = 0; k < (tm + 31) / 32; ++k) {
+    if (32 * k >= w.nrows) break;  // warp-uniform
+    const int r = lane + 32 * k;
+    const uint32_t nx_same = __shfl_sync(0xffffffffu, w.st[k], (lane + 1) & 31);
+    const uint32_t nx_next = __shfl_sync(0xffffffffu, w.st[k < 3 ? k + 1 : 3], 0);
+    if (r < w.nrows) {
+      const uint32_t beg = r == 0 ? 0u : w.st[k];
+      const uint32_t end = r + 1 >= w.nrows ? (uint32_t)w.E : (lane == 31 ? nx_next : nx_same);
+      for (uint32_t e = beg; e < end; ++e) srow[e] = (uint8_t)r;
+    }
+  }
+  __syncwarp();
+}
+
+// Ranks (bitmap + prefix) and brick patterns of a warp-path panel into the warp's shared memory; validates
+// columns (ST_COL_RANGE) and in-row order (ST_COL_ORDER). Returns false if the brick slots of the
+// panel exceed the layout (then the panel is listed for the CTA path).
+template <int tm, int tk>
+__device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ ci, int64_t K, WarpPanel& w, uint8_t* my,
+                                                const WarpLayout& L, uint32_t* status) {
+  const int lane = threadIdx.x & 31;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(my);
+  uint32_t* pre = reinterpret_cast<uint32_t*>(my + L.off_pre);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(my);  // sort path (aliases bm + pre)
+  uint8_t* srow = my + L.off_row;
+  uint16_t* sq = reinterpret_cast<uint16_t*>(my + L.off_q);
+  uint32_t* pat32 = reinterpret_cast<uint32_t*>(my + L.off_pat);
+  constexpr int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  constexpr int tk_sh = tk == 16 ? 4 : 5;
+  const bool sorted = w.sorted;
+  if (!sorted) {
 #pragma unroll
-    for (int k = 0; k < PER; ++k)
-      if (lane + 32 * k < E) {
-        const uint32_t off = col[k] - (uint32_t)mn;
-        atomicOr(&bm[off >> 5], 1u << (off & 31));
-      }
-    __syncwarp();
+    for (int i = 0; i < kWBmWords / 32; ++i) bm[lane + 32 * i] = 0u;
+  }
+  warp_row_map<tm>(w, srow);
+  const int E = w.E;
+  const int32_t mn = w.mn;
+  bool bad_range = false, bad_order = false;
+  int32_t prev_c = 0;
+  int prev_r = -1;
+  for (int c0 = 0; c0 < E; c0 += 32) {  // pass 1: validation + bitmap bits (or sort keys)
+    const int i = c0 + lane;
+    const int r = i < E ? srow[i] : -2;
+    const int32_t c = i < E ? ci[w.e0 + i] : 0;
+    int32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
+    int pr = __shfl_up_sync(0xffffffffu, r, 1);
+    if (lane == 0) { pc = prev_c; pr = prev_r; }
+    prev_c = __shfl_sync(0xffffffffu, c, 31);
+    prev_r = __shfl_sync(0xffffffffu, r, 31);
+    if (i < E) {
+      const uint32_t off = (uint32_t)(c - mn);
+      if (c < 0 || c >= K) bad_range = true;
+      if (pr == r && pc >= c) bad_order = true;
+      if (sorted) keys[i] = ((uint64_t)(uint32_t)c << 32) | (uint32_t)i;
+      else if (off >= 32u * kWBmWords) bad_order = true;  // only an unsorted row can leave [mn, mx]
+      else atomicOr(&bm[off >> 5], 1u << (off & 31));
+    }
+  }
+  const bool any_range = __any_sync(0xffffffffu, bad_range), any_order = __any_sync(0xffffffffu, bad_order);
+  if (status && lane == 0) {
+    if (any_range) atomicOr(status, ST_COL_RANGE);
+    if (any_order) atomicOr(status, ST_COL_ORDER);
+  }
+  __syncwarp();
+  uint32_t nact;
+  if (!sorted) {
+    constexpr int kW = kWBmWords / 32;
     uint32_t cnt[kW], sum = 0;
 #pragma unroll
     for (int i = 0; i < kW; ++i) { cnt[i] = __popc(bm[lane * kW + i]); sum += cnt[i]; }
@@ -263,268 +378,291 @@ __device__ __forceinline__ int count_panel_warp(const int64_t* __restrict__ rp, 
 #pragma unroll
     for (int i = 0; i < kW; ++i) { pre[lane * kW + i] = run; run += cnt[i]; }
     __syncwarp();
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const uint32_t off = col[k] - (uint32_t)mn;
-      const uint32_t w = (off >> 5) & (kWarpSpanWords - 1), b = off & 31;
-      qv[k] = pre[w] + __popc(bm[w] & ((1u << b) - 1u));
+    for (int c0 = 0; c0 < E; c0 += 32) {  // ranks: popcount prefix of the lower bits (R23: ascending columns)
+      const int i = c0 + lane;
+      if (i < E) {
+        const uint32_t off = (uint32_t)(ci[w.e0 + i] - mn);
+        uint32_t qq = 0xFFFFu;
+        if (off < 32u * kWBmWords) qq = pre[off >> 5] + __popc(bm[off >> 5] & ((1u << (off & 31)) - 1u));
+        sq[i] = (uint16_t)qq;
+      }
     }
-  } else if constexpr (SORT) {
+  } else {
+    // bitonic sort of (column, entry) keys, n = next power of two >= E (<= 256), then first-occurrence scan
     int n = 32;
     while (n < E) n <<= 1;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int idx = lane + 32 * k;
-      if (idx < n) s_keys[idx] = idx < E ? ((uint64_t)col[k] << 32) | (uint32_t)idx : ~0ull;
-    }
+    for (int i = E + lane; i < n; i += 32) keys[i] = ~0ull;
     __syncwarp();
     for (int kk = 2; kk <= n; kk <<= 1) {
       for (int j = kk >> 1; j > 0; j >>= 1) {
         for (int i = lane; i < n; i += 32) {
           const int ixj = i ^ j;
           if (ixj > i) {
-            const uint64_t a = s_keys[i], b = s_keys[ixj];
-            if ((a > b) == ((i & kk) == 0)) { s_keys[i] = b; s_keys[ixj] = a; }
+            const uint64_t a = keys[i], b = keys[ixj];
+            if ((a > b) == ((i & kk) == 0)) { keys[i] = b; keys[ixj] = a; }
           }
         }
         __syncwarp();
       }
     }
-    const int per = n / 32;
-    const int beg = lane * per;
+    const int per = n / 32, beg = lane * per;
     uint32_t sum = 0;
     for (int i = beg; i < beg + per && i < E; ++i)
-      if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++sum;
+      if (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ++sum;
     uint32_t run = warp_excl_scan(sum, &nact);
     for (int i = beg; i < beg + per && i < E; ++i) {
-      if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++run;
-      s_qb[(uint32_t)s_keys[i]] = run - 1;
+      if (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ++run;
+      sq[(uint32_t)keys[i]] = (uint16_t)(run - 1);
     }
+  }
+  w.nact = nact;
+  w.nblk = (nact + tk - 1) / tk;
+  return true;
+}
+
+// Brick patterns (P:L132 fill_brick_nnz_pattern; bit = (r % 16) * 4 + q % 4, R3) of blocks [jb0, jb0 + nb) of a
+// ranked warp-path panel into the warp's slot array (slot = (j - jb0) * nbk + brick column * nbrow + brick row).
+template <int tm, int tk>
+__device__ __forceinline__ void warp_panel_patterns(const WarpPanel& w, uint8_t* my, const WarpLayout& L,
+                                                    uint32_t jb0, uint32_t nb) {
+  const int lane = threadIdx.x & 31;
+  const uint8_t* srow = my + L.off_row;
+  const uint16_t* sq = reinterpret_cast<const uint16_t*>(my + L.off_q);
+  uint32_t* pat32 = reinterpret_cast<uint32_t*>(my + L.off_pat);
+  constexpr int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  constexpr int tk_sh = tk == 16 ? 4 : 5;
+  for (int i = lane; i < 2 * (int)nb * nbk; i += 32) pat32[i] = 0u;
+  __syncwarp();
+  const uint32_t q0 = jb0 * tk, q1 = min((jb0 + nb) * tk, w.nact);
+  for (int c0 = 0; c0 < w.E; c0 += 32) {
+    const int i = c0 + lane;
+    if (i < w.E) {
+      const uint32_t qq = sq[i];
+      if (qq >= q0 && qq < q1) {
+        const int r = srow[i];
+        const uint32_t j = (qq >> tk_sh) - jb0, lc = qq & (tk - 1);
+        const int bit = ((r & 15) << 2) | (int)(lc & 3);
+        atomicOr(&pat32[2 * (j * nbk + (lc >> 2) * nbrow + (r >> 4)) + (bit >> 5)], 1u << (bit & 31));
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// Classification pre-pass: panels the warp path cannot take (more than kWCap entries, column span wider than
+// the bitmap) are flagged and listed for the CTA / hub count kernels, which run before k_wbuild.
+template <int tm, int tk>
+__global__ void __launch_bounds__(32 * kWWarps) k_wclassify(const int64_t* __restrict__ rp,
+                                                           const int32_t* __restrict__ ci, int64_t M, int64_t nnz,
+                                                           int64_t P, uint8_t* __restrict__ listed,
+                                                           uint32_t* __restrict__ list,
+                                                           uint32_t* __restrict__ nlist) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t p = (int64_t)blockIdx.x * kWWarps + wid; p < P; p += (int64_t)gridDim.x * kWWarps) {
+    WarpPanel w;
+    const bool ok = warp_panel_open<tm, tk>(rp, ci, M, nnz, p, w, nullptr);
+    if (lane == 0) {
+      listed[p] = ok ? 0 : 1;
+      if (!ok) list[atomicAdd(nlist, 1u)] = (uint32_t)p;
+    }
+  }
+}
+
+// Decoupled look-back over panels (single-pass exclusive scan, warp granularity): st[p] holds the panel's
+// aggregate (flag A) as soon as it is known, later its inclusive prefix (flag P). Panels are claimed in order
+// through a ticket, so every predecessor belongs to a warp that is running or done.
+#define kLbA (1ull << 62)
+#define kLbP (2ull << 62)
+#define kLbMask ((1ull << 62) - 1)
+__device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// One look-back over a state word carrying (blocks << 34 | bytes) (host checks both fit: blocks < 2^28,
+// bytes < 2^34). Returns the exclusive prefix of the packed pair (the fields never carry into each other).
+__device__ __forceinline__ uint64_t warp_lookback(uint64_t* st, int64_t p, uint64_t agg) {
+  const int lane = threadIdx.x & 31;
+  if (p == 0) {
+    if (lane == 0) st_relaxed_gpu(st, kLbP | agg);
     __syncwarp();
-#pragma unroll
-    for (int k = 0; k < PER; ++k) qv[k] = lane + 32 * k < E ? s_qb[lane + 32 * k] : 0u;
+    return 0;
   }
-  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
-  const uint32_t nblk = (nact + tk - 1) / tk;
-  const int nbricks = (int)nblk * nbk;
-  for (int i = lane; i < nbricks; i += 32) s_pat[i] = 0ull;
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    if (lane + 32 * k < E) {
-      const uint32_t qq = qv[k], r = (uint32_t)rowv[k];
-      const uint32_t j = qq / tk, lc = qq % tk;
-      const int bit = (int)(((r & 15) << 2) | (lc & 3));
-      uint32_t* half = reinterpret_cast<uint32_t*>(&s_pat[j * nbk + (lc >> 2) * nbrow + (r >> 4)]) + (bit >> 5);
-      atomicOr(half, 1u << (bit & 31));
-      q[e0 + lane + 32 * k] = qq;
+  if (lane == 0) st_relaxed_gpu(st + p, kLbA | agg);
+  uint64_t excl = 0;
+  int64_t j = p - 1;
+  while (true) {
+    const int64_t idx = j - lane;
+    uint64_t v = idx >= 0 ? ld_relaxed_gpu(st + idx) : kLbP;
+    while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
+      if ((v >> 62) == 0) v = ld_relaxed_gpu(st + idx);
     }
-  }
-  __syncwarp();
-  uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
-  for (int i = lane; i < nbricks; i += 32) gp[i] = s_pat[i];
-  uint32_t bytes = 0;
-  for (uint32_t j = lane; j < nblk; j += 32) {
-    uint32_t nbr = 0, nz = 0;
-    for (int i = 0; i < nbk; ++i) { const uint64_t v = s_pat[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
-    bytes += block_bytes(nbc, nbr, nz);
-  }
+    const uint32_t pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+    const int last = pm ? __ffs(pm) - 1 : 31;  // lanes 0..last contribute (lane `last` has the prefix)
+    uint64_t x = lane <= last ? (v & kLbMask) : 0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-  if (lane == 0) { nact_out[p] = nact; nblk_out[p] = nblk; pbytes_out[p] = bytes; }
-  return 0;
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    excl += x;
+    if (pm) break;
+    j -= 32;
+  }
+  if (lane == 0) st_relaxed_gpu(st + p, kLbP | (excl + agg));
+  __syncwarp();
+  return excl;
 }
 
-template <int CAP, bool SORT>
-__host__ __device__ constexpr int count_warp_smem(int tm, int tk) {
-  return (int)((((SORT ? CAP * 12 : 2 * kWarpSpanWords * 4) + ((tm + 2) & ~1) * 8 + (CAP / tk) * (tk / 4) * (tm / 16) * 8) +
-                15) & ~15);
-}
-
-// Warp per panel over all panels (CAP = 256, sort allowed); panels with more entries go to list L1.
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp(
-    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t M, int64_t K, int64_t nnz, int tm,
-    int tk, int64_t P, uint32_t* __restrict__ q, uint32_t* __restrict__ nact_out, uint32_t* __restrict__ nblk_out,
-    uint32_t* __restrict__ pbytes_out, uint64_t* __restrict__ gpat, uint32_t* __restrict__ l1, uint32_t* __restrict__ nl1,
-    uint32_t* status) {
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int wid = threadIdx.x >> 5;
-  const int64_t p = (int64_t)blockIdx.x * kWarpsPerCta + wid;
-  if (p >= P) return;
-  uint8_t* my = dsm + (size_t)wid * count_warp_smem<kWarpCap, true>(tm, tk);
-  int64_t E;
-  const int r = count_panel_warp<kWarpCap, true>(rp, ci, M, K, nnz, tm, tk, p, q, nact_out, nblk_out, pbytes_out,
-                                                  gpat, status, my, E);
-  if (r != 0 && (threadIdx.x & 31) == 0) l1[atomicAdd(nl1, 1u)] = (uint32_t)p;
-}
-
-// Warp per listed panel (CAP = 1024, bitmap ranking only). Not handled -> list L2 (CTA count); more than
-// kWarpCap2 entries -> also list L3 (CTA emit).
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_count_warp2(
-    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t M, int64_t K, int64_t nnz, int tm,
-    int tk, uint32_t* __restrict__ q, uint32_t* __restrict__ nact_out, uint32_t* __restrict__ nblk_out,
-    uint32_t* __restrict__ pbytes_out, uint64_t* __restrict__ gpat, const uint32_t* __restrict__ l1,
-    const uint32_t* __restrict__ nl1, uint32_t* __restrict__ l2, uint32_t* __restrict__ nl2,
-    uint32_t* __restrict__ l3, uint32_t* __restrict__ nl3, uint32_t* status) {
+// Fused pass for all panels: warp-path panels are ranked, their (blocks, bytes) published, the exclusive
+// prefixes (blockedRowPtr, B2; panel byte offset, B4) found by look-back, and the panel emitted:
+// sizePtr, HRPB-v1 headers + patterns + zero padding (R7), values in brick-CSC order at popcount
+// ranks, activeCols with sentinel K (R2, R6). Listed panels only take part in the scan
+// with the (nblk, bytes) their CTA / hub count produced; k_emit writes them afterwards.
+template <int tm, int tk>
+__global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                        const float* __restrict__ vals, int64_t M, int64_t K,
+                                                        int64_t nnz, int64_t P, const uint8_t* __restrict__ listed,
+                                                        const uint32_t* __restrict__ nblk_listed,
+                                                        const uint32_t* __restrict__ pbytes_listed,
+                                                        uint32_t* __restrict__ ticket, uint64_t* __restrict__ lb,
+                                                        uint32_t* __restrict__ brp,
+                                                        uint64_t* __restrict__ poff, uint32_t* __restrict__ ac,
+                                                        uint64_t* __restrict__ sp, uint8_t* __restrict__ packed,
+                                                        uint32_t* status) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* my = dsm + (size_t)wid * count_warp_smem<kWarpCap2, false>(tm, tk);
-  const uint32_t count = *nl1;
-  for (uint32_t t = blockIdx.x * kWarpsPerCta + wid; t < count; t += gridDim.x * kWarpsPerCta) {
-    const int64_t p = l1[t];
-    int64_t E;
-    const int r = count_panel_warp<kWarpCap2, false>(rp, ci, M, K, nnz, tm, tk, p, q, nact_out, nblk_out,
-                                                      pbytes_out, gpat, status, my, E);
-    if (lane == 0) {
-      if (r != 0) l2[atomicAdd(nl2, 1u)] = (uint32_t)p;
-      if (E > kWarpCap2) l3[atomicAdd(nl3, 1u)] = (uint32_t)p;
-    }
-    __syncwarp();
-  }
-}
-
-// ------------------------------------------------------------------ pass B, warp per panel
-template <int CAP>
-__device__ __forceinline__ void emit_panel_warp(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                                const float* __restrict__ vals, int64_t M, int64_t K, int64_t nnz,
-                                                int tm, int tk, int64_t p, const uint32_t* __restrict__ q,
-                                                const uint32_t* __restrict__ nact_in,
-                                                const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff,
-                                                const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac,
-                                                uint64_t* __restrict__ sp, uint8_t* __restrict__ packed, uint8_t* my) {
-  const int lane = threadIdx.x & 31;
-  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
-  const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0;
-  if (nblk == 0) return;
-  int64_t* s_rp = reinterpret_cast<int64_t*>(my);
-  uint64_t* s_vbase = reinterpret_cast<uint64_t*>(s_rp + ((tm + 2) & ~1));  // [CAP / 16]
-  uint64_t* s_pt = s_vbase + CAP / 16;                                     // [CAP / tk * nbk]
-  uint16_t* s_soff = reinterpret_cast<uint16_t*>(s_pt + (CAP / tk) * nbk); // value offset of each brick slot
-  warp_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);
-  const int nrows = (int)min((int64_t)tm, M - p * tm);
-  const uint32_t nact = nact_in[p];
-  const int64_t e0 = s_rp[0], e1 = s_rp[nrows];
-  const uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
-  for (int i = lane; i < (int)nblk * nbk; i += 32) s_pt[i] = gp[i];
-  __syncwarp();
-  uint64_t carry = poff[p];
-  for (uint32_t c0 = 0; c0 < nblk; c0 += 32) {  // blocks, 32 at a time (one per lane)
-    const uint32_t j = c0 + lane;
-    uint32_t nbr = 0, nz = 0, size = 0;
-    if (j < nblk) {
-      for (int i = 0; i < nbk; ++i) {
-        const uint64_t v = s_pt[j * nbk + i];
-        s_soff[j * nbk + i] = (uint16_t)nz;  // popcount of the earlier slots (CSC order)
-        nbr += v != 0ull;
-        nz += __popcll(v);
-      }
-      size = block_bytes(nbc, nbr, nz);
-    }
-    uint32_t tot;
-    const uint64_t off = carry + warp_excl_scan(size, &tot);
-    if (j < nblk) {
-      sp[b0 + j] = off;
-      uint8_t* blk = packed + off;
-      const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
-      uint32_t k = 0;
-      blk[0] = 0;
-      for (int bc = 0; bc < nbc; ++bc) {
-        for (int br = 0; br < nbrow; ++br) {
-          const uint64_t v = s_pt[j * nbk + bc * nbrow + br];
-          if (!v) continue;
-          blk[nbc + 1 + k] = (uint8_t)br;
-          reinterpret_cast<uint64_t*>(blk + hdr)[k] = v;
-          ++k;
+  const WarpLayout L = warp_layout(tm, tk);
+  uint8_t* my = dsm + (size_t)wid * L.bytes;
+  constexpr int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const uint8_t* srow = my + L.off_row;
+  const uint16_t* sq = reinterpret_cast<const uint16_t*>(my + L.off_q);
+  const unsigned long long* pat = reinterpret_cast<const unsigned long long*>(my + L.off_pat);
+  constexpr int tk_sh = tk == 16 ? 4 : 5;
+  uint16_t* soff = reinterpret_cast<uint16_t*>(my + L.off_soff);
+  uint64_t* vbase = reinterpret_cast<uint64_t*>(my + L.off_vbase);
+  while (true) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1u);
+    const int64_t p = (int64_t)__shfl_sync(0xffffffffu, t, 0);
+    if (p >= P) break;
+    WarpPanel w;
+    w.E = 0;
+    w.nblk = 0;
+    uint32_t bytes = 0;
+    constexpr uint32_t kChunkBlk = kWSlotCap / nbk;  // blocks whose patterns fit the slot array
+    const bool is_listed = listed[p] != 0;
+    if (is_listed) {
+      w.nblk = nblk_listed[p];
+      bytes = pbytes_listed[p];
+    } else {
+      warp_panel_open<tm, tk>(rp, ci, M, nnz, p, w, status);  // (true: the classification pass agreed)
+      if (w.E > 0) {
+        warp_panel_rank<tm, tk>(ci, K, w, my, L, status);
+        for (uint32_t jb0 = 0; jb0 < w.nblk; jb0 += kChunkBlk) {
+          const uint32_t nb = min(kChunkBlk, w.nblk - jb0);
+          warp_panel_patterns<tm, tk>(w, my, L, jb0, nb);
+          for (uint32_t j = lane; j < nb; j += 32) {
+            uint32_t nbr = 0, nz = 0;
+#pragma unroll
+            for (int i = 0; i < nbk; ++i) { const uint64_t v = pat[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
+            bytes += block_bytes(nbc, nbr, nz);
+          }
         }
-        blk[bc + 1] = (uint8_t)k;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
       }
-      for (uint32_t i = nbc + 1 + nbr; i < hdr; ++i) blk[i] = 0;
-      for (uint32_t i = hdr + 8 * nbr + 4 * nz; i < size; ++i) blk[i] = 0;
-      s_vbase[j] = off + hdr + 8 * nbr;
     }
-    carry += tot;
-  }
-  for (int64_t t = nact + lane; t < (int64_t)nblk * tk; t += 32) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
-  __syncwarp();
-  constexpr int kBatch = 8;  // loads of 8 rounds in flight before any use
-  for (int64_t eb = e0; eb < e1; eb += 32 * kBatch) {
-    uint32_t qb[kBatch];
-    int32_t cb[kBatch];
-    float vb[kBatch];
+    const uint64_t ex = warp_lookback(lb, p, ((uint64_t)w.nblk << 34) | bytes);
+    const uint32_t b0 = (uint32_t)(ex >> 34);
+    const uint64_t pbase = ex & ((1ull << 34) - 1);
+    if (lane == 0) {
+      brp[p] = b0;
+      poff[p] = pbase;
+      if (p == P - 1) { brp[P] = b0 + w.nblk; poff[P] = pbase + bytes; }
+    }
+    if (is_listed || w.E == 0) continue;
+    const uint32_t nblk = w.nblk;
+    const int E = w.E;
+    uint64_t carry = pbase;
+    for (int64_t t = w.nact + lane; t < (int64_t)nblk * tk; t += 32) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
+    for (uint32_t jb0 = 0; jb0 < nblk; jb0 += kChunkBlk) {
+      const uint32_t nbch = min(kChunkBlk, nblk - jb0);
+      if (jb0 > 0) warp_panel_patterns<tm, tk>(w, my, L, jb0, nbch);  // (chunk 0 is still in place if alone)
+      else if (nblk > kChunkBlk) warp_panel_patterns<tm, tk>(w, my, L, 0, nbch);
+      for (uint32_t c0 = 0; c0 < nbch; c0 += 32) {  // blocks: sizes, in-panel scan, headers, patterns, padding
+        const uint32_t j = c0 + lane;  // block jb0 + j of the panel
+        uint32_t nbr = 0, nz = 0, size = 0;
+        if (j < nbch) {
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const int64_t e = eb + 32 * u + lane;
-      qb[u] = e < e1 ? q[e] : 0xFFFFFFFFu;
-      cb[u] = e < e1 ? ci[e] : 0;
-      vb[u] = e < e1 ? vals[e] : 0.f;
-    }
+          for (int i = 0; i < nbk; ++i) {
+            const uint64_t v = pat[j * nbk + i];
+            soff[j * nbk + i] = (uint16_t)nz;  // values of the earlier bricks of the block (CSC slot order)
+            nbr += v != 0ull;
+            nz += __popcll(v);
+          }
+          size = block_bytes(nbc, nbr, nz);
+        }
+        uint32_t tot;
+        const uint64_t off = carry + warp_excl_scan(size, &tot);
+        if (j < nbch) {
+          sp[b0 + jb0 + j] = off;
+          uint64_t* blk = reinterpret_cast<uint64_t*>(packed + off);  // 16-B aligned
+          const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+          // header bytes: colPtr[0..nbc] (stored bricks before each brick column), rows[nbr] (brick row of each
+          // stored brick), zero pad to 8 B; assembled 8 bytes at a time
+          uint64_t acc = 0;
+          uint32_t nb = 1, k = 0, wi = 0;  // byte 0 = colPtr[0] = 0
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const int64_t e = eb + 32 * u + lane;
-      const uint32_t qq = qb[u];
-      if (qq >= nact) continue;  // past the panel, or invalid CSR input
-      const int r = row_of(s_rp, nrows, e);
-      const uint32_t jb = qq / tk, lc = qq % tk;
-      ac[((int64_t)b0 + jb) * tk + lc] = (uint32_t)cb[u];
-      const int bit = ((r & 15) << 2) | (lc & 3);
-      const int mine = (lc >> 2) * nbrow + (r >> 4);
-      const uint32_t o = s_soff[jb * nbk + mine] + __popcll(s_pt[jb * nbk + mine] & ((1ull << bit) - 1ull));
-      reinterpret_cast<float*>(packed + s_vbase[jb])[o] = vb[u];
+          for (int bc = 0; bc < nbc; ++bc) {
+#pragma unroll
+            for (int br = 0; br < nbrow; ++br) k += pat[j * nbk + bc * nbrow + br] != 0ull;
+            acc |= (uint64_t)k << (8 * (nb & 7));
+            if ((++nb & 7) == 0) { blk[wi++] = acc; acc = 0; }
+          }
+          for (int bc = 0; bc < nbc; ++bc)
+            for (int br = 0; br < nbrow; ++br) {
+              const uint64_t v = pat[j * nbk + bc * nbrow + br];
+              if (!v) continue;
+              acc |= (uint64_t)br << (8 * (nb & 7));
+              if ((++nb & 7) == 0) { blk[wi++] = acc; acc = 0; }
+            }
+          if (nb & 7) blk[wi++] = acc;
+          for (int i = 0; i < nbk; ++i) {
+            const uint64_t v = pat[j * nbk + i];
+            if (v) blk[wi++] = v;
+          }
+          uint32_t* tail = reinterpret_cast<uint32_t*>(packed + off + hdr + 8 * nbr + 4 * nz);
+          for (uint32_t t = hdr + 8 * nbr + 4 * nz; t < size; t += 4) *tail++ = 0u;
+          vbase[j] = off + hdr + 8 * nbr;
+        }
+        carry += tot;
+      }
+      __syncwarp();
+      const uint32_t q0 = jb0 * tk, q1 = min((jb0 + nbch) * tk, w.nact);
+      for (int c0 = 0; c0 < E; c0 += 32) {  // values and activeCols of this chunk's blocks
+        const int i = c0 + lane;
+        if (i < E) {
+          const uint32_t qq = sq[i];
+          if (qq >= q0 && qq < q1) {
+            const int r = srow[i];
+            const int32_t c = ci[w.e0 + i];
+            const float v = vals[w.e0 + i];
+            const uint32_t j = (qq >> tk_sh) - jb0, lc = qq & (tk - 1);
+            ac[((int64_t)b0 + jb0 + j) * tk + lc] = (uint32_t)c;
+            const int bit = ((r & 15) << 2) | (int)(lc & 3);
+            const uint32_t slot = j * nbk + (lc >> 2) * nbrow + (r >> 4);
+            const uint32_t o = soff[slot] + __popcll(pat[slot] & ((1ull << bit) - 1ull));
+            reinterpret_cast<float*>(packed + vbase[j])[o] = v;
+          }
+        }
+      }
+      __syncwarp();
     }
   }
-  __syncwarp();
 }
 
-template <int CAP>
-__host__ __device__ constexpr int emit_warp_smem(int tm, int tk) {
-  return (int)((((tm + 2) & ~1) * 8 + (CAP / 16) * 8 + (CAP / tk) * (tk / 4) * (tm / 16) * (8 + 2) + 15) & ~15);
-}
-
-__device__ __forceinline__ int64_t panel_entries(const int64_t* __restrict__ rp, int64_t M, int64_t nnz, int tm,
-                                                 int64_t p) {
-  const int64_t r0 = p * tm;
-  const int nrows = (int)min((int64_t)tm, M - r0);
-  int64_t a = rp[r0], b = rp[r0 + nrows];
-  a = a < 0 ? 0 : (a > nnz ? nnz : a);
-  b = b < 0 ? 0 : (b > nnz ? nnz : b);
-  return b - a;
-}
-
-// all panels with <= kWarpCap entries
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_emit_warp(
-    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const float* __restrict__ vals, int64_t M,
-    int64_t K, int64_t nnz, int tm, int tk, int64_t P, const uint32_t* __restrict__ q,
-    const uint32_t* __restrict__ nact_in, const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff,
-    const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac, uint64_t* __restrict__ sp,
-    uint8_t* __restrict__ packed) {
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int wid = threadIdx.x >> 5;
-  const int64_t p = (int64_t)blockIdx.x * kWarpsPerCta + wid;
-  if (p >= P) return;
-  if (panel_entries(rp, M, nnz, tm, p) > kWarpCap) return;  // listed in L1 (k_emit_warp2 / k_emit)
-  emit_panel_warp<kWarpCap>(rp, ci, vals, M, K, nnz, tm, tk, p, q, nact_in, brp, poff, gpat, ac, sp, packed,
-                            dsm + (size_t)wid * emit_warp_smem<kWarpCap>(tm, tk));
-}
-
-// listed panels (L1) with <= kWarpCap2 entries
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_emit_warp2(
-    const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const float* __restrict__ vals, int64_t M,
-    int64_t K, int64_t nnz, int tm, int tk, const uint32_t* __restrict__ q, const uint32_t* __restrict__ nact_in,
-    const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff, const uint64_t* __restrict__ gpat,
-    uint32_t* __restrict__ ac, uint64_t* __restrict__ sp, uint8_t* __restrict__ packed,
-    const uint32_t* __restrict__ l1, const uint32_t* __restrict__ nl1) {
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int wid = threadIdx.x >> 5;
-  uint8_t* my = dsm + (size_t)wid * emit_warp_smem<kWarpCap2>(tm, tk);
-  const uint32_t count = *nl1;
-  for (uint32_t t = blockIdx.x * kWarpsPerCta + wid; t < count; t += gridDim.x * kWarpsPerCta) {
-    const int64_t p = l1[t];
-    if (panel_entries(rp, M, nnz, tm, p) > kWarpCap2) continue;  // listed in L3 (k_emit)
-    emit_panel_warp<kWarpCap2>(rp, ci, vals, M, K, nnz, tm, tk, p, q, nact_in, brp, poff, gpat, ac, sp, packed, my);
-  }
-}
-
-// ------------------------------------------------------------------ pass A, kWarpCap < entries <= kSmallCap
+// ------------------------------------------------------------------ pass A (CTA), listed panels with <= kSmallCap entries
 // One CTA per listed panel ("for row_panel in rowPanels_chunk"). q[e] = rank of col_idx[e] among the
 // panel's distinct columns (ascending, R23; "active_cols = uniq(cols[...])"), nblk = ceil(nact/TK)
 // (R1), brick patterns (bit = (r % 16) * 4 + q % 4, R3) and the panel's total block bytes.
@@ -746,107 +884,7 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
   }
 }
 
-// ------------------------------------------------------------------ device-wide exclusive scan
-constexpr int kScanThreads = 256, kScanPer = 16, kScanChunk = kScanThreads * kScanPer;
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_partials(const uint32_t* __restrict__ in, int64_t n,
-                                                                uint64_t* __restrict__ part) {
-  __shared__ uint64_t sh[kScanThreads / 32];
-  int64_t base = (int64_t)blockIdx.x * kScanChunk;
-  uint64_t s = 0;
-  for (int i = 0; i < kScanPer; ++i) {
-    int64_t idx = base + (int64_t)i * kScanThreads + threadIdx.x;
-    if (idx < n) s += in[idx];
-  }
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t t = 0;
-    for (int w = 0; w < kScanThreads / 32; ++w) t += sh[w];
-    part[blockIdx.x] = t;
-  }
-}
-
-__global__ void __launch_bounds__(1024) k_scan_top(uint64_t* part, int64_t nparts) {
-  __shared__ uint64_t sh[33];
-  uint64_t carry = 0;
-  for (int64_t base = 0; base < nparts; base += 1024) {
-    int64_t i = base + threadIdx.x;
-    uint64_t v = i < nparts ? part[i] : 0, x = v;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int o = 1; o < 32; o <<= 1) {
-      uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) sh[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      uint64_t w = sh[lane];
-      for (int o = 1; o < 32; o <<= 1) {
-        uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      sh[lane] = w;
-    }
-    __syncthreads();
-    uint64_t excl = carry + (warp ? sh[warp - 1] : 0) + x - v;
-    uint64_t tot = sh[31];
-    __syncthreads();
-    if (i < nparts) part[i] = excl;
-    carry += tot;
-  }
-}
-
-template <typename OutT>
-__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* __restrict__ in, int64_t n,
-                                                            const uint64_t* __restrict__ part,
-                                                            OutT* __restrict__ out) {
-  __shared__ uint64_t sh[kScanThreads / 32 + 1];
-  int64_t base = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kScanPer;
-  uint32_t v[kScanPer];
-  uint64_t s = 0;
-#pragma unroll
-  for (int i = 0; i < kScanPer; ++i) {
-    v[i] = (base + i < n) ? in[base + i] : 0u;
-    s += v[i];
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t x = s;
-  for (int o = 1; o < 32; o <<= 1) {
-    uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) sh[warp] = x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t t = 0;
-    for (int w = 0; w < kScanThreads / 32; ++w) { uint64_t c = sh[w]; sh[w] = t; t += c; }
-  }
-  __syncthreads();
-  uint64_t run = part[blockIdx.x] + sh[warp] + x - s;
-#pragma unroll
-  for (int i = 0; i < kScanPer; ++i) {
-    if (base + i < n) out[base + i] = (OutT)run;
-    run += v[i];
-    if (base + i == n - 1) out[n] = (OutT)run;  // total at out[n]
-  }
-}
-
-template <typename OutT>
-static void scan_excl(const uint32_t* in, int64_t n, OutT* out, uint64_t* part, cudaStream_t s) {
-  if (n == 0) {
-    cudaMemsetAsync(out, 0, sizeof(OutT), s);
-    return;
-  }
-  int64_t nb = ceil_div(n, kScanChunk);
-  k_scan_partials<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, part);
-  k_scan_top<<<1, 1024, 0, s>>>(part, nb);
-  k_scan_down<OutT><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, part, out);
-  note_launch(3);
-}
-
-// ------------------------------------------------------------------ pass B (CTA), panels with > kWarpCap entries
+// ------------------------------------------------------------------ pass B (CTA), listed panels
 // One CTA per listed panel. Block j of panel p is global block b0 + j (b0 = blockedRowPtr[p]); its byte offset
 // is the panel offset plus the in-panel exclusive scan of block sizes (sizePtr). Header,
 // patterns and values follow the HRPB-v1 layout; value destination = values base + popcount of the
@@ -968,6 +1006,54 @@ __global__ void k_finalize(const int64_t* __restrict__ rp, int64_t M, int64_t nn
 }
 
 // ------------------------------------------------------------------ host orchestration
+// warp-path kernels are specialised on (TM, TK) (compile-time brick-slot loops)
+#define HRPB_WDISPATCH(CALL)                                                         \
+  do {                                                                               \
+    if (tk == 16) {                                                                  \
+      if (tm == 16) { CALL(16, 16); } else if (tm == 32) { CALL(32, 16); }           \
+      else if (tm == 64) { CALL(64, 16); } else { CALL(128, 16); }                   \
+    } else {                                                                         \
+      if (tm == 16) { CALL(16, 32); } else if (tm == 32) { CALL(32, 32); }           \
+      else if (tm == 64) { CALL(64, 32); } else { CALL(128, 32); }                   \
+    }                                                                                \
+  } while (0)
+
+template <int TM, int TK>
+static int wbuild_ctas() {  // resident CTAs of k_wbuild per SM (the ticket loop is persistent)
+  static int n = 0;
+  if (!n) {
+    const size_t smem = (size_t)warp_layout(TM, TK).bytes * kWWarps;
+    cudaFuncSetAttribute(k_wbuild<TM, TK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_wbuild<TM, TK>, 32 * kWWarps, smem);
+    if (n < 1) n = 1;
+  }
+  return n;
+}
+
+static void launch_wclassify(int tm, int tk, unsigned grid, cudaStream_t s, const int64_t* rp, const int32_t* ci,
+                             int64_t M, int64_t nnz, int64_t P, uint8_t* listed, uint32_t* list, uint32_t* nlist) {
+#define HRPB_WC(A, B) k_wclassify<A, B><<<grid, 32 * kWWarps, 0, s>>>(rp, ci, M, nnz, P, listed, list, nlist)
+  HRPB_WDISPATCH(HRPB_WC);
+#undef HRPB_WC
+}
+
+static void launch_wbuild(int tm, int tk, cudaStream_t s, const int64_t* rp, const int32_t* ci, const float* vals,
+                          int64_t M, int64_t K, int64_t nnz, int64_t P, const uint8_t* listed,
+                          const uint32_t* nblk_listed, const uint32_t* pbytes_listed, uint32_t* ticket,
+                          uint64_t* lb, uint32_t* brp, uint64_t* poff, uint32_t* ac,
+                          uint64_t* sp, uint8_t* packed, uint32_t* status) {
+  const size_t smem = (size_t)warp_layout(tm, tk).bytes * kWWarps;
+#define HRPB_WB(A, B)                                                                                          \
+  {                                                                                                            \
+    const int64_t want = ceil_div(P, kWWarps), have = (int64_t)wbuild_ctas<A, B>() * num_sms();                \
+    k_wbuild<A, B><<<(unsigned)(want < have ? want : have), 32 * kWWarps, smem, s>>>(                          \
+        rp, ci, vals, M, K, nnz, P, listed, nblk_listed, pbytes_listed, ticket, lb, brp, poff,                \
+        ac, sp, packed, status);                                                                               \
+  }
+  HRPB_WDISPATCH(HRPB_WB);
+#undef HRPB_WB
+}
+
 hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
                          const float* values, int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h) {
   const int64_t P = ceil_div(M, tm);
@@ -991,69 +1077,56 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   uint32_t* pbytes = cnt + 2 * (P + 1);
   uint64_t* poff = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t), s);
   uint64_t* gpat = (uint64_t*)dalloc(pat_cap * sizeof(uint64_t), s);
-  // panel lists: big (> kSmallCap, hub bitmap) | L1 (> kWarpCap) | L2 (CTA count) | L3 (CTA emit)
-  uint32_t* biglist = (uint32_t*)dalloc(4 * (P + 1) * sizeof(uint32_t), s);
+  // panel lists: big (> kSmallCap entries, hub bitmap) | L1 (not on the warp path: CTA count + CTA emit)
+  uint32_t* biglist = (uint32_t*)dalloc(2 * (P + 1) * sizeof(uint32_t), s);
   uint32_t* l1 = biglist + (P + 1);
-  uint32_t* l2 = biglist + 2 * (P + 1);
-  uint32_t* l3 = biglist + 3 * (P + 1);
-  uint32_t* ctr = (uint32_t*)dalloc(8 * sizeof(uint32_t), s);  // nbig, nl1, nl2, nl3, status
-  const int64_t nparts = ceil_div(P + 1, kScanChunk) + 1;
-  uint64_t* part = (uint64_t*)dalloc(nparts * sizeof(uint64_t), s);
+  uint32_t* ctr = (uint32_t*)dalloc(8 * sizeof(uint32_t), s);  // nbig, nl1, ticket, -, status
+  uint64_t* lb = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t), s);  // look-back states (blocks << 34 | bytes)
+  uint8_t* listed = (uint8_t*)dalloc(P + 1, s);
   uint64_t* info = (uint64_t*)dalloc(4 * sizeof(uint64_t), s);  // [3] = status word | hub count
   const int big_ctas = num_sms();
   const int64_t words = ceil_div(K, 32) + 2;
   uint32_t* bigscr = (uint32_t*)dalloc((size_t)big_ctas * 2 * words * sizeof(uint32_t), s);
   hrpb_status_t st = HRPB_SUCCESS;
-  if (!h->brp || !h->ac || !h->sp || !h->packed || !q || !cnt || !poff || !gpat || !biglist || !part || !info ||
-      !bigscr || !ctr) {
+  // the fused look-back packs (blocks, bytes) into 62 bits
+  if (nb_cap >= (1ll << 28) || bytes_cap >= (1ll << 34)) {
+    st = HRPB_ERROR_NOT_SUPPORTED;
+  } else if (!h->brp || !h->ac || !h->sp || !h->packed || !q || !cnt || !poff || !gpat || !biglist || !info ||
+             !bigscr || !ctr || !lb || !listed) {
     st = HRPB_ERROR_OUT_OF_MEMORY;
   }
   uint64_t hinfo[3] = {0, 0, 0};
   if (st == HRPB_SUCCESS) {
     uint32_t* nbig = ctr;
     uint32_t* nl1 = ctr + 1;
-    uint32_t* nl2 = ctr + 2;
-    uint32_t* nl3 = ctr + 3;
+    uint32_t* ticket = ctr + 2;
     uint32_t* status = ctr + 4;
     cudaMemsetAsync(ctr, 0, 8 * sizeof(uint32_t), s);
     const size_t count_smem =
         (size_t)kSmallCap * (8 + 4 + 4 + 1) + (size_t)ceil_div(kSmallCap, tk) * nbk * sizeof(uint64_t);
-    const size_t wsm_c1 = (size_t)count_warp_smem<kWarpCap, true>(tm, tk) * kWarpsPerCta;
-    const size_t wsm_c2 = (size_t)count_warp_smem<kWarpCap2, false>(tm, tk) * kWarpsPerCta;
-    const size_t wsm_e1 = (size_t)emit_warp_smem<kWarpCap>(tm, tk) * kWarpsPerCta;
-    const size_t wsm_e2 = (size_t)emit_warp_smem<kWarpCap2>(tm, tk) * kWarpsPerCta;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_count_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_count_warp2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_emit_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_emit_warp2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    const unsigned wgrid = (unsigned)ceil_div(P, kWarpsPerCta);
+    const unsigned wgrid = (unsigned)ceil_div(P, kWWarps);
     const int mid_ctas = 8 * num_sms();
-    if (P > 0) {  // pass A: warp (<= 256) -> warp, bitmap (<= 1024) -> CTA (<= 2048) -> hub bitmap
-      k_count_warp<<<wgrid, 32 * kWarpsPerCta, wsm_c1, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, P, q, nact, nblk,
-                                                            pbytes, gpat, l1, nl1, status);
-      k_count_warp2<<<mid_ctas, 32 * kWarpsPerCta, wsm_c2, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
-                                                                pbytes, gpat, l1, nl1, l2, nl2, l3, nl3, status);
+    cudaMemsetAsync(lb, 0, (P + 1) * sizeof(uint64_t), s);
+    cudaMemsetAsync(h->brp, 0, sizeof(uint32_t), s);  // P == 0: blockedRowPtr = {0}
+    cudaMemsetAsync(poff, 0, sizeof(uint64_t), s);
+    if (P > 0) {
+      // classification; listed panels counted by a CTA (<= kSmallCap entries) or the hub bitmap kernel
+      launch_wclassify(tm, tk, wgrid, s, row_ptr, col_idx, M, nnz, P, listed, l1, nl1);
       k_count<<<mid_ctas, kSmallThreads, count_smem, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
-                                                          pbytes, gpat, l2, nl2, biglist, nbig, status);
+                                                          pbytes, gpat, l1, nl1, biglist, nbig, status);
       k_count_big<<<big_ctas, kBigThreads, 0, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk, pbytes, gpat,
                                                     biglist, nbig, bigscr, words, status);
-      note_launch(4);
-    }
-    scan_excl<uint32_t>(nblk, P, h->brp, part, s);  // B2: blockedRowPtr
-    scan_excl<uint64_t>(pbytes, P, poff, part, s);  // B4 (panel level): byte offset of each panel
-    if (P > 0) {                                    // pass B
-      k_emit_warp<<<wgrid, 32 * kWarpsPerCta, wsm_e1, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, P, q, nact,
-                                                           h->brp, poff, gpat, h->ac, h->sp, h->packed);
-      k_emit_warp2<<<mid_ctas, 32 * kWarpsPerCta, wsm_e2, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact,
-                                                               h->brp, poff, gpat, h->ac, h->sp, h->packed, l1, nl1);
+      // B1-B5 for warp-path panels + the single-pass scans B2 / B4 for all panels
+      launch_wbuild(tm, tk, s, row_ptr, col_idx, values, M, K, nnz, P, listed, nblk, pbytes, ticket, lb, h->brp,
+                    poff, h->ac, h->sp, h->packed, status);
       k_emit<<<mid_ctas, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp, poff,
-                                               gpat, h->ac, h->sp, h->packed, l3, nl3);
-      note_launch(3);
+                                               gpat, h->ac, h->sp, h->packed, l1, nl1);
+      note_launch(5);
     }
     k_finalize<<<1, 1, 0, s>>>(row_ptr, M, nnz, P, h->brp, poff, h->sp, status, info);
     note_launch();
@@ -1062,9 +1135,9 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) st = cuda_status(e);
   }
-  dfree(q, s); dfree(cnt, s); dfree(poff, s); dfree(gpat, s); dfree(biglist, s); dfree(part, s); dfree(info, s);
+  dfree(q, s); dfree(cnt, s); dfree(poff, s); dfree(gpat, s); dfree(biglist, s); dfree(info, s);
   dfree(bigscr, s);
-  dfree(ctr, s);
+  dfree(ctr, s); dfree(lb, s); dfree(listed, s);
   if (st == HRPB_SUCCESS && hinfo[2] != 0) st = HRPB_ERROR_INVALID_CSR;
   h->NB = (int64_t)hinfo[0];
   h->bytes = (int64_t)hinfo[1];
