@@ -352,14 +352,15 @@ def run_ours(args, rank, world, local_rank):
     compulsory = meta_bytes + 4 * NCOL * uniq + 4 * M0 * NCOL
     gathered = meta_bytes + 4 * NCOL * sum_nact + 4 * M0 * NCOL
     achieved = compulsory / (spmm_ms / 1e3) / 1e9
+    build_bytes = 8 * (M0 + 1) + 8 * nnz + packed + NB * 16 * 4 + (NB + 1) * 8 + (P + 1) * 4
     try:
         tf32_peak = measure_tf32_peak(torch)
     except Exception:
         tf32_peak = None
     exec_tflops = 2.0 * NB * args.tm * 16 * (128 * ((NCOL + 127) // 128)) / (spmm_ms / 1e3) / 1e12
-    roof = {"kernel": "hrpb::k_spmm<1>", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+    roof = {"kernel": f"hrpb::k_spmm<NT=1, TM={args.tm}>", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
             "unit": "GB/s", "frac": round(achieved / hbm, 4),
-            "traffic": ncu_traffic("k_spmm", "c2a"),
+            "traffic": ncu_traffic(f"k_spmm_tm{args.tm}", "c2a"),
             "algorithmic_bytes_per_launch": int(compulsory),
             "bytes_definition": "packedBlocks + activeCols + blockedRowPtr + sizePtr + 4*N*(distinct columns) "
                                 "+ 4*M*N (compulsory; DESIGN.md §Roofline)",
@@ -367,6 +368,13 @@ def run_ours(args, rank, world, local_rank):
             "gathered_gbs": round(gathered / (spmm_ms / 1e3) / 1e9, 1),
             "kernel_ms": round(spmm_ms, 4), "share_of_step": round(spmm_ms / ms, 3),
             "peak_source": peak_src,
+            "build_phase": {"ms": round(build_ms, 4),
+                            "algorithmic_bytes": int(build_bytes),
+                            "achieved_gbs": round(build_bytes / (build_ms / 1e3) / 1e9, 1),
+                            "frac": round(build_bytes / (build_ms / 1e3) / 1e9 / hbm, 4),
+                            "bytes_definition": "CSR read (8(M+1) + 8 nnz) + HRPB written (packedBlocks + "
+                                                "activeCols + sizePtr + blockedRowPtr); phase = all builder "
+                                                "kernels + the status read-back"},
             "tf32": {"executed_tflops": round(exec_tflops, 2),
                      "peak_tflops_measured": round(tf32_peak, 1) if tf32_peak else None,
                      "frac": round(exec_tflops / tf32_peak, 4) if tf32_peak else None}}

@@ -1,6 +1,8 @@
 """Summarise ncu --set full reports into a markdown table + the per-kernel DRAM traffic JSON bench.py reads.
 
-usage: python tools/ncu_summary.py OUT_MD WORKLOAD_TAG REP [REP ...]
+usage: python tools/ncu_summary.py OUT_MD WORKLOAD_TAG REP [REP ...] [--traffic]
+(--traffic also records each kernel's DRAM bytes per launch in profiles/ncu_traffic.json; k_spmm is keyed by
+ its TM template argument, k_spmm_tm<TM>, because bench.py picks TM per run)
 """
 import csv
 import io
@@ -39,7 +41,9 @@ def read(rep):
 
 
 def main():
-    out_md, tag, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+    args = [a for a in sys.argv[1:] if a != "--traffic"]
+    write_traffic = "--traffic" in sys.argv
+    out_md, tag, reps = args[0], args[1], args[2:]
     rows = [d for rep in reps for d in read(rep)]
     lines = ["| kernel | time us | DRAM read MB | DRAM write MB | DRAM % | L2 % | L2 hit % | L1 % | SM % | tensor % | warps % | regs | grid x block |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
@@ -55,12 +59,16 @@ def main():
                      f"{g('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed'):.2f} | "
                      f"{g('sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} | {g('launch__registers_per_thread'):.0f} | "
                      f"{g('launch__grid_size'):.0f} x {g('launch__block_size'):.0f} |")
-        name = d["kernel"].replace("void ", "").split("::")[-1].split("<")[0].strip()
+        full = d["kernel"].replace("void ", "").split("::")[-1]
+        name = full.split("<")[0].strip()
+        if name == "k_spmm" and "<" in full:  # k_spmm<NT, GM, TM>
+            name += "_tm" + full.split("<")[1].rstrip(">").split(",")[-1].strip()
         traffic[name] = {"workload": tag,
                          "dram_bytes_per_launch": int(g("dram__bytes_read.sum") + g("dram__bytes_write.sum")),
                          "ncu_time_us": round(g("gpu__time_duration.sum") * 1e6, 2)}
     open(out_md, "a").write("\n".join(lines) + "\n")
-    json.dump(traffic, open(traffic_path, "w"), indent=1)
+    if write_traffic:
+        json.dump(traffic, open(traffic_path, "w"), indent=1)
     print("\n".join(lines))
 
 
