@@ -92,8 +92,11 @@ hrpb_status_t hrpb_spmm(const hrpb_t A, const float* B, float* C, int64_t M, int
 
 /*
  * hrpb_build_spmm_host — the whole hot path from HOST buffers (end-to-end entry point):
- * H2D copies of the CSR and B, hrpb_build, hrpb_spmm, D2H copy of C, all on `stream`, returning
- * after C is in host memory. Host buffers should be pinned for full PCIe bandwidth.
+ * H2D copies of the CSR and B, hrpb_build, hrpb_spmm, D2H copy of C, returning after C is in host memory.
+ * Pipelined: the CSR and then B (in 32 row chunks) are copied on a library-owned copy stream, the build runs on
+ * `stream` once the CSR is in, C is computed in 16 panel chunks — each starting as soon as the B rows up to its
+ * largest active column have arrived — and each chunk is copied back on a second library stream while later B
+ * chunks are still in flight. Host buffers should be pinned for full (and overlapped) PCIe bandwidth.
  * Arguments as for hrpb_build / hrpb_spmm, with host pointers.
  */
 hrpb_status_t hrpb_build_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr_h,

@@ -126,32 +126,96 @@ hrpb_status_t hrpb_build_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz,
   hrpb_status_t st = check_device();
   if (st != HRPB_SUCCESS) return st;
   cudaStream_t s = (cudaStream_t)stream;
+  // Pipeline: copy engine H2D: CSR, then B in row chunks; the build runs as soon as the CSR is in;
+  // C is produced in panel chunks, chunk c starting once the B rows up to its largest active column have
+  // arrived; its rows go back D2H on a third stream while later B chunks still stream in (PCIe is full duplex).
+  static cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking);
+  });
+  constexpr int kBChunks = 32, kCChunks = 16;
+  cudaEvent_t ev[2 + kBChunks + kCChunks];
+  for (auto& x : ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  cudaEvent_t ev_in = ev[0], ev_done = ev[1], *ev_b = ev + 2, *ev_c = ev + 2 + kBChunks;
   int64_t* rp = (int64_t*)dalloc((M + 1) * sizeof(int64_t), s);
   int32_t* ci = (int32_t*)dalloc((nnz + 1) * sizeof(int32_t), s);
   float* v = (float*)dalloc((nnz + 1) * sizeof(float), s);
   float* B = (float*)dalloc((size_t)K * N * sizeof(float) + 16, s);
   float* C = (float*)dalloc((size_t)M * N * sizeof(float) + 16, s);
+  int* maxcol = (int*)dalloc(kCChunks * sizeof(int), s);
+  int maxcol_h[kCChunks];
   hrpb_t A = nullptr;
-  if (!rp || !ci || !v || !B || !C) st = HRPB_ERROR_OUT_OF_MEMORY;
+  if (!rp || !ci || !v || !B || !C || !maxcol) st = HRPB_ERROR_OUT_OF_MEMORY;
   cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t x) {
+    if (x != cudaSuccess && e == cudaSuccess) e = x;
+  };
+  const int64_t brows = (K + kBChunks - 1) / kBChunks;  // B rows per H2D chunk
   if (st == HRPB_SUCCESS) {
-    e = cudaMemcpyAsync(rp, row_ptr_h, (M + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(ci, col_idx_h, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(v, values_h, nnz * sizeof(float), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && K * N)
-      e = cudaMemcpyAsync(B, B_h, (size_t)K * N * sizeof(float), cudaMemcpyHostToDevice, s);
+    ok(cudaEventRecord(ev_in, s));  // the allocations above are ordered on s
+    ok(cudaStreamWaitEvent(s_h2d, ev_in, 0));
+    ok(cudaMemcpyAsync(rp, row_ptr_h, (M + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s_h2d));
+    if (nnz) ok(cudaMemcpyAsync(ci, col_idx_h, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s_h2d));
+    if (nnz) ok(cudaMemcpyAsync(v, values_h, nnz * sizeof(float), cudaMemcpyHostToDevice, s_h2d));
+    ok(cudaEventRecord(ev_in, s_h2d));
+    for (int j = 0; j < kBChunks; ++j) {
+      const int64_t r0 = j * brows, r1 = (j + 1) * brows < K ? (j + 1) * brows : K;
+      if (r1 > r0 && N > 0)
+        ok(cudaMemcpyAsync(B + r0 * N, B_h + r0 * N, (size_t)(r1 - r0) * N * sizeof(float), cudaMemcpyHostToDevice,
+                           s_h2d));
+      ok(cudaEventRecord(ev_b[j], s_h2d));
+    }
+    ok(cudaStreamWaitEvent(s, ev_in, 0));
     if (e != cudaSuccess) st = cuda_status(e);
   }
-  if (st == HRPB_SUCCESS) st = hrpb_build(M, K, nnz, rp, ci, v, cfg, stream, &A);
-  if (st == HRPB_SUCCESS) st = hrpb_spmm(A, B, C, M, K, N, stream);
-  if (st == HRPB_SUCCESS && M * N) {
-    e = cudaMemcpyAsync(C_h, C, (size_t)M * N * sizeof(float), cudaMemcpyDeviceToHost, s);
+  if (st == HRPB_SUCCESS) st = hrpb_build(M, K, nnz, rp, ci, v, cfg, stream, &A);  // (syncs s, not the copies)
+  const int64_t P = A ? A->P : 0;
+  const int64_t per = (P + kCChunks - 1) / kCChunks > 0 ? (P + kCChunks - 1) / kCChunks : 1;
+  if (st == HRPB_SUCCESS && M > 0 && N > 0) st = chunk_maxcol(A, per, kCChunks, maxcol, s);
+  if (st == HRPB_SUCCESS && M > 0 && N > 0) {
+    ok(cudaMemcpyAsync(maxcol_h, maxcol, sizeof(maxcol_h), cudaMemcpyDeviceToHost, s));
+    ok(cudaStreamSynchronize(s));
     if (e != cudaSuccess) st = cuda_status(e);
   }
+  if (st == HRPB_SUCCESS && M > 0 && N > 0) {
+    if (N % 4 != 0) {  // padded-B path of the kernel: whole-matrix launch after all of B
+      ok(cudaStreamWaitEvent(s, ev_b[kBChunks - 1], 0));
+      st = hrpb_spmm(A, B, C, M, K, N, stream);
+      ok(cudaEventRecord(ev_c[0], s));
+      ok(cudaStreamWaitEvent(s_d2h, ev_c[0], 0));
+      ok(cudaMemcpyAsync(C_h, C, (size_t)M * N * sizeof(float), cudaMemcpyDeviceToHost, s_d2h));
+    } else {
+      int waited = -1;
+      for (int c = 0; c < kCChunks && st == HRPB_SUCCESS; ++c) {
+        const int64_t p0 = c * per, p1 = (c + 1) * per < P ? (c + 1) * per : P;
+        if (p1 <= p0) break;
+        const int need = maxcol_h[c] < 0 ? -1 : (int)(maxcol_h[c] / brows);  // last B chunk this C chunk reads
+        if (need > waited) {
+          ok(cudaStreamWaitEvent(s, ev_b[need], 0));
+          waited = need;
+        }
+        st = spmm_range_impl(A, B, N, C, N, p0, p1, s);
+        ok(cudaEventRecord(ev_c[c], s));
+        const int64_t r0 = p0 * A->tm, r1 = p1 * A->tm < M ? p1 * A->tm : M;
+        ok(cudaStreamWaitEvent(s_d2h, ev_c[c], 0));
+        ok(cudaMemcpyAsync(C_h + r0 * N, C + r0 * N, (size_t)(r1 - r0) * N * sizeof(float), cudaMemcpyDeviceToHost,
+                           s_d2h));
+      }
+    }
+    if (e != cudaSuccess && st == HRPB_SUCCESS) st = cuda_status(e);
+  }
+  // every stream drains before the buffers are released on s
+  cudaEventRecord(ev_done, s_h2d);
+  cudaStreamWaitEvent(s, ev_done, 0);
+  cudaEventRecord(ev_done, s_d2h);
+  cudaStreamWaitEvent(s, ev_done, 0);
   hrpb_free(A);
-  dfree(rp, s); dfree(ci, s); dfree(v, s); dfree(B, s); dfree(C, s);
-  e = cudaStreamSynchronize(s);
-  if (st == HRPB_SUCCESS && e != cudaSuccess) st = cuda_status(e);
+  dfree(rp, s); dfree(ci, s); dfree(v, s); dfree(B, s); dfree(C, s); dfree(maxcol, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (st == HRPB_SUCCESS && e2 != cudaSuccess) st = cuda_status(e2);
+  for (auto& x : ev) cudaEventDestroy(x);
   return st;
 }
 

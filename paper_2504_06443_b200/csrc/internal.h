@@ -30,6 +30,11 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
                          const float* values, int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h);
 
 hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, cudaStream_t s);
+// C rows of panels [p_lo, p_hi) only (the pipelined host entry point)
+hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, int64_t p_lo,
+                              int64_t p_hi, cudaStream_t s);
+// dev_out[c] = largest real active column of panels [c * per, (c + 1) * per), -1 if none
+hrpb_status_t chunk_maxcol(const hrpb_handle* h, int64_t per, int nchunks, int* dev_out, cudaStream_t s);
 
 int num_sms();
 

@@ -44,6 +44,7 @@ struct SpmmParams {
   const uint8_t* packed;
   float* C;
   int64_t M, N, P, NB;
+  int64_t p_lo, p_hi;  // panel range of this launch (the whole matrix, or one chunk of the pipelined host path)
   const float* B;  // row-major K x ldb (cp.async gather mode)
   int64_t K, ldb;
   int n0;      // first output column of this launch
@@ -105,9 +106,8 @@ struct SmemLayout {
   static_assert(2 * NT * TMV <= 512, "two TMEM accumulator slots must fit in 512 columns");
 };
 
-__device__ __forceinline__ int64_t panel_lower_bound(const uint32_t* brp, int64_t P, uint64_t target) {
-  // first p in [0, P] with brp[p] + p >= target (brp[p] + p strictly increasing)
-  int64_t lo = 0, hi = P;
+__device__ __forceinline__ int64_t panel_lower_bound(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t target) {
+  // first p in [lo, hi] with brp[p] + p >= target (brp[p] + p strictly increasing)
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
     if ((uint64_t)brp[mid] + (uint64_t)mid >= target) hi = mid;
@@ -204,11 +204,12 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     }
     for (int i = 0; i < L::kSlots; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     fence_mbar_init();
-    // S1: contiguous panel range with ~equal (blocks + panels)
-    const uint64_t W = (uint64_t)prm.NB + (uint64_t)prm.P;
+    // S1: contiguous panel range with ~equal (blocks + panels) inside [p_lo, p_hi)
+    const uint64_t base = (uint64_t)prm.brp[prm.p_lo] + (uint64_t)prm.p_lo;
+    const uint64_t W = (uint64_t)prm.brp[prm.p_hi] + (uint64_t)prm.p_hi - base;
     const uint64_t G = gridDim.x, c = blockIdx.x;
-    range[0] = panel_lower_bound(prm.brp, prm.P, c * W / G);
-    range[1] = c + 1 == G ? prm.P : panel_lower_bound(prm.brp, prm.P, (c + 1) * W / G);
+    range[0] = panel_lower_bound(prm.brp, prm.p_lo, prm.p_hi, base + c * W / G);
+    range[1] = c + 1 == G ? prm.p_hi : panel_lower_bound(prm.brp, prm.p_lo, prm.p_hi, base + (c + 1) * W / G);
     for (int m = 0; m < kMmaWarps; ++m) mma_prog[m] = 0u;
     prefetch_tmap(&tmB);
   }
@@ -620,7 +621,7 @@ static EncodeTiledFn get_encode() {
 
 template <int NT, int GM, int TMV>
 static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, const float* B, int64_t ldb, float* C,
-                               int64_t N, int n0, cudaStream_t s) {
+                               int64_t N, int n0, int64_t p_lo, int64_t p_hi, cudaStream_t s) {
   using L = SmemLayout<NT, TMV>;
   // producer warp w (and decoder warp w) owns blocks i = w mod 4; with S a multiple of 4 every stage is
   // only ever filled by one warp, so a warp running ahead cannot alias an mbarrier phase.
@@ -652,9 +653,10 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     const char* e = kInstr ? getenv("HRPB_DEBUG") : nullptr;
     return e ? atoi(e) : 0;
   }();
-  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, B, h->K, ldb, n0, stages, trace, debug};
+  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, p_lo, p_hi, B, h->K, ldb, n0, stages,
+                 trace, debug};
   int grid = num_sms();
-  if ((int64_t)grid > h->P) grid = (int)(h->P > 0 ? h->P : 1);
+  if ((int64_t)grid > p_hi - p_lo) grid = (int)(p_hi > p_lo ? p_hi - p_lo : 1);
   k_spmm<NT, GM, TMV><<<grid, kSpmmThreads, smem, s>>>(tm, prm);
   note_launch();
   if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)
@@ -672,9 +674,15 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
 }
 
 hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, cudaStream_t s) {
-  if (N == 0 || h->M == 0) return HRPB_SUCCESS;
-  if (h->NB == 0) {  // A has no entries: C = 0
-    cudaError_t e = cudaMemsetAsync(C, 0, (size_t)h->M * N * sizeof(float), s);
+  return spmm_range_impl(h, B, ldb, C, N, 0, h->P, s);
+}
+
+hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, int64_t p_lo,
+                              int64_t p_hi, cudaStream_t s) {
+  if (N == 0 || h->M == 0 || p_hi <= p_lo) return HRPB_SUCCESS;
+  if (h->NB == 0) {  // A has no entries: C = 0 (rows of the range)
+    const int64_t r0 = p_lo * h->tm, r1 = p_hi * h->tm < h->M ? p_hi * h->tm : h->M;
+    cudaError_t e = cudaMemsetAsync(C + r0 * N, 0, (size_t)(r1 - r0) * N * sizeof(float), s);
     return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);
   }
   if (!(h->tm == 16 || h->tm == 32 || h->tm == 64) || h->tk != 16) return HRPB_ERROR_NOT_SUPPORTED;
@@ -716,17 +724,17 @@ hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float
     }();
 #define HRPB_LAUNCH(TMV_)                                                                     \
   switch (nt) {                                                                               \
-    case 1: st = launch_nt<1, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
-    case 2: st = launch_nt<2, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
-    case 3: st = launch_nt<3, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
-    default: st = launch_nt<4, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;              \
+    case 1: st = launch_nt<1, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, p_lo, p_hi, s); break;               \
+    case 2: st = launch_nt<2, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, p_lo, p_hi, s); break;               \
+    case 3: st = launch_nt<3, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, p_lo, p_hi, s); break;               \
+    default: st = launch_nt<4, 1, TMV_>(h, tm, Bt, ld, C, N, (int)n0, p_lo, p_hi, s); break;              \
   }
 #define HRPB_LAUNCH_GM0(TMV_)                                                                 \
   switch (nt) {                                                                               \
-    case 1: st = launch_nt<1, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
-    case 2: st = launch_nt<2, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
-    case 3: st = launch_nt<3, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;               \
-    default: st = launch_nt<4, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, s); break;              \
+    case 1: st = launch_nt<1, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, p_lo, p_hi, s); break;               \
+    case 2: st = launch_nt<2, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, p_lo, p_hi, s); break;               \
+    case 3: st = launch_nt<3, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, p_lo, p_hi, s); break;               \
+    default: st = launch_nt<4, 0, TMV_>(h, tm, Bt, ld, C, N, (int)n0, p_lo, p_hi, s); break;              \
   }
     if (gm == 0) {  // TMA tile::gather4 staging
       if (h->tm == 16) { HRPB_LAUNCH_GM0(16) }
@@ -744,6 +752,34 @@ hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float
     if (st != HRPB_SUCCESS) return st;
   }
   return HRPB_SUCCESS;
+}
+
+// Largest real active column of every panel of each chunk (chunk c = panels [c * per, (c + 1) * per)); the
+// pipelined host entry point starts a chunk's SpMM once B rows up to that column have arrived.
+__global__ void k_chunk_maxcol(const uint32_t* __restrict__ brp, const uint32_t* __restrict__ ac, int64_t P, int tk,
+                               uint32_t K, int64_t per, int* __restrict__ out) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b0 = brp[p], b1 = brp[p + 1];
+    if (b1 == b0) continue;
+    int mx = -1;
+    for (int64_t t = b1 * tk - 1; t >= b0 * tk && t >= b1 * tk - tk; --t) {  // sentinels only in the last block
+      const uint32_t c = ac[t];
+      if (c < K) { mx = (int)c; break; }
+    }
+    if (mx >= 0) atomicMax(&out[p / per], mx);
+  }
+}
+
+hrpb_status_t chunk_maxcol(const hrpb_handle* h, int64_t per, int nchunks, int* dev_out, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(dev_out, 0xFF, nchunks * sizeof(int), s);  // -1: chunk needs no B row
+  if (e != cudaSuccess) return cuda_status(e);
+  if (h->P > 0 && h->NB > 0) {
+    k_chunk_maxcol<<<(unsigned)ceil_div(h->P, 256) < 4096 ? (unsigned)ceil_div(h->P, 256) : 4096u, 256, 0, s>>>(
+        h->brp, h->ac, h->P, h->tk, (uint32_t)h->K, per, dev_out);
+    note_launch();
+  }
+  e = cudaGetLastError();
+  return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);
 }
 
 }  // namespace hrpb
