@@ -1,0 +1,659 @@
+// spmm_kernel.cuh — the hrpb_spmm_sm100 kernel template: C = A.B with A in HRPB.
+//
+// Paper kernel (Alg. "cuTeSpMM kernel design"; prose P:L244-282): one thread block
+// per row panel, warps along N, SM_A/SM_B staging, per-brick pattern decode with prefix popcounts
+// (P:L207-219), Ampere mma.sync m16n8k4 TF32 accumulating in registers.
+//
+// B200 design:
+//  * persistent CTAs (one per SM), each owning a contiguous panel range balanced on
+//    (blocks + panels) (S1);
+//  * warp 0: TMA producer — cp.async.bulk of the packed block bytes (S2) and
+//    cp.async.bulk.tensor.2d.tile::gather4 of the 16 B rows named by activeCols into an
+//    MN-major SWIZZLE_128B_BASE32B tile (S3); sentinel column K is out of bounds -> zero fill;
+//  * warp 1: decoder — lane l expands bits l and l+32 of every brick (prefix popcounts)
+//    into a zero-filled K-major TF32 tile (cvt.rna on A, reading R15) (S2);
+//  * warp 2: one thread issues tcgen05.mma.kind::tf32 computing the transposed product
+//    D[n, r] += sum_k Bg[k, n] * A[r, k]  (M = 128 dense columns, N = TM = 16 panel rows, K = 8 x 2),
+//    accumulating a whole panel in TMEM (double-buffered across panels) (S4);
+//  * warps 3..6: epilogue — tcgen05.ld 32x32b, coalesced 128-B row stores of C (S5);
+//  * mbarrier rings: full_a/full_b (TMA), dec (decoder), empty (tcgen05.commit), tfull/tempty.
+#pragma once
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace hrpb {
+
+constexpr int kProdWarps = 4;                              // warps 0..3: gather producers
+constexpr int kDecWarps = 4;                               // warps 4..7: brick decoders
+constexpr int kMmaWarp = kProdWarps + kDecWarps;           // warp 8: TMEM alloc; warps 8..9: MMA issue
+#ifndef HRPB_MMA_WARPS
+#define HRPB_MMA_WARPS 2
+#endif
+constexpr int kMmaWarps = HRPB_MMA_WARPS;                  // non-empty panel pc -> MMA warp 8 + pc % 2
+constexpr int kEpiWarp0 = kMmaWarp + kMmaWarps;            // warps 10..13: epilogue
+constexpr int kSpmmThreads = 32 * (kEpiWarp0 + 4);        // 448
+constexpr int kMaxStages = 24;
+
+struct SpmmParams {
+  const uint32_t* brp;
+  const uint32_t* ac;
+  const uint64_t* sp;
+  const uint8_t* packed;
+  float* C;
+  int64_t M, N, P, NB;
+  int64_t p_lo, p_hi;  // panel range of this launch (the whole matrix, or one chunk of the pipelined host path)
+  const float* B;  // row-major K x ldb (cp.async gather mode)
+  int64_t K, ldb;
+  int n0;      // first output column of this launch
+  int stages;  // pipeline depth
+  long long* trace;  // optional: per-block event timestamps of CTA 0 (HRPB_TRACE), [6][kTraceN]
+  int debug;         // HRPB_DEBUG bits (experiments only): 1 = skip C stores, 2 = skip decode, 4 = skip MMA issue,
+                     // 8 = skip A bulk copy, 16 = B gather zero-fill only (no global reads), 32 = no B cp.async at all
+};
+constexpr int kTraceN = 1024;
+constexpr int kTraceSlots = 9;  // slot 8: per warp of CTA 0 {cycles waiting on mbarriers, cycles total}
+// trace slots: 0 producer issue (after empty), 1 A arrived (decoder), 2 decode done, 3 B arrived (MMA),
+//              4 MMA issued, 5 epilogue got tfull (per panel), 6 decoder slot table done, 7 decoder rows done
+// Instrumentation (HRPB_TRACE timestamps, HRPB_DEBUG work-skipping bits) exists only in builds with
+// -DHRPB_INSTRUMENT=1 (tools/build_variant.py); the product kernel carries none of it: the serial MMA/decoder
+// loops are sensitive to every extra instruction.
+#ifndef HRPB_INSTRUMENT
+#define HRPB_INSTRUMENT 0
+#endif
+constexpr bool kInstr = HRPB_INSTRUMENT != 0;
+__device__ __forceinline__ bool dbg(const SpmmParams& p, int bit) { return kInstr && (p.debug & bit); }
+__device__ __forceinline__ bool tracing(const SpmmParams& p) { return kInstr && p.trace != nullptr; }
+__device__ __forceinline__ void trace_ev(const SpmmParams& p, int slot, uint32_t i) {
+  if (tracing(p) && blockIdx.x == 0 && i < kTraceN) p.trace[slot * kTraceN + i] = clock64();
+}
+// mbarrier wait that accumulates the cycles spent waiting when tracing (role busy/idle breakdown)
+__device__ __forceinline__ void mbar_wait_acc(const SpmmParams& p, uint64_t* bar, uint32_t parity, long long& acc) {
+  if (tracing(p)) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, parity);
+  }
+}
+
+// instruction descriptor: D F32, A/B TF32, A MN-major, B K-major, N = TM (panel rows), M = 128
+template <int TMV>
+__host__ __device__ constexpr uint32_t idesc_tf32() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (0u << 16) | ((uint32_t)(TMV >> 3) << 17) |
+         ((128u >> 4) << 24);
+}
+
+template <int NT, int TMV, int TKV>
+struct SmemLayout {
+  static constexpr int kNA = 4 * NT;                 // 32-column atoms per 4-row group
+  static constexpr int kBTile = TKV * 128 * 4 * NT;  // gathered rows per stage
+  static constexpr int kNbc = TKV / 4;               // brick columns per block
+  static constexpr int kNbrow = TMV / 16;            // brick rows per block
+  static constexpr int kNbk = kNbc * kNbrow;         // brick slots per block
+  static_assert(kNbk <= 32, "the decoder's slot table gives one lane per brick slot");
+  // largest HRPB-v1 block: align8(5 + nbk) + 8 nbk + 4 TM TK, rounded to 128 B
+  static constexpr int kARawBytes = ((((kNbc + 1 + kNbk + 7) & ~7) + 8 * kNbk + 4 * TMV * TKV) + 127) & ~127;
+  static constexpr int kATileBytes = TMV * TKV * 4;  // TM x TK fp32 decoded block
+  static constexpr int kLbo = TMV * 16;              // bytes between 4-column K groups of the decoded tile
+  static constexpr int kStage = kBTile + kARawBytes + kATileBytes;
+  // TMEM accumulator slots (panels in flight between the MMA warp and the epilogue): up to 4
+  static constexpr int kSlots = 4 * NT * TMV <= 512 ? 4 : 2;
+  static_assert(kSlots % kMmaWarps == 0, "a TMEM slot must always be used by the same MMA warp");
+  static constexpr int kSlotCols = kSlots * NT * TMV;
+  static constexpr uint32_t kTmemCols = kSlotCols <= 32 ? 32 : (kSlotCols <= 64 ? 64 : (kSlotCols <= 128 ? 128 : (kSlotCols <= 256 ? 256 : 512)));
+  static_assert(2 * NT * TMV <= 512, "two TMEM accumulator slots must fit in 512 columns");
+};
+
+__device__ __forceinline__ int64_t panel_lower_bound(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t target) {
+  // first p in [lo, hi] with brp[p] + p >= target (brp[p] + p strictly increasing)
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if ((uint64_t)brp[mid] + (uint64_t)mid >= target) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+// Warp-cooperative iteration over panels [pa, pb): blockedRowPtr is fetched 32 panels per coalesced
+// load, one chunk ahead. All 32 lanes must call next() convergently; it returns false at the end.
+struct PanelCursor {
+  const uint32_t* brp;
+  int64_t pb, base, j;
+  int cnt;
+  uint32_t cur, cur_last, nxt, nxt_last;
+  int lane;
+  __device__ void load(int64_t b0, uint32_t& v, uint32_t& last) {
+    const int64_t idx = b0 + lane;
+    v = idx <= pb ? __ldg(brp + idx) : 0u;
+    last = __ldg(brp + (b0 + 32 <= pb ? b0 + 32 : pb));
+  }
+  __device__ PanelCursor(const uint32_t* brp_, int64_t pa, int64_t pb_, int lane_)
+      : brp(brp_), pb(pb_), base(pa), j(-1), lane(lane_) {
+    cnt = (int)min((int64_t)32, pb - pa);
+    if (pa < pb) load(pa, cur, cur_last);
+    if (pa + 32 < pb) load(pa + 32, nxt, nxt_last);
+  }
+  // advances to the next panel; p = panel id, bb/be = its block range
+  __device__ bool next(int64_t& p, uint32_t& bb, uint32_t& be) {
+    if (base >= pb) return false;
+    if (++j == cnt) {
+      base += 32;
+      if (base >= pb) return false;
+      cur = nxt;
+      cur_last = nxt_last;
+      cnt = (int)min((int64_t)32, pb - base);
+      j = 0;
+      if (base + 32 < pb) load(base + 32, nxt, nxt_last);
+    }
+    p = base + j;
+    bb = __shfl_sync(0xffffffffu, cur, (int)j);
+    const uint32_t nx = __shfl_sync(0xffffffffu, cur, (int)(j + 1) & 31);
+    be = j + 1 < 32 ? nx : cur_last;
+    return true;
+  }
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// GM = gather mode: 0 = TMA tile::gather4 (one issuing lane per producer warp),
+//                   1 = cp.async 16-B copies by all 128 producer threads into the same swizzled layout.
+template <int NT, int GM, int TMV, int TKV>
+__global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant__ CUtensorMap tmB, SpmmParams prm) {
+  using L = SmemLayout<NT, TMV, TKV>;
+  static_assert(GM == 1 || TKV == 16, "TMA gather4 staging is written for TK = 16");
+  constexpr int kARawBytes = L::kARawBytes, kATileBytes = L::kATileBytes;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B alignment by pointer arithmetic on the __shared__ array (an integer round trip would make every
+  // derived pointer generic: LD.E/ST.E instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int S = prm.stages;
+  uint8_t* btile0 = smem;                                 // S x kBTile (1024-aligned)
+  uint8_t* araw0 = smem + (size_t)S * L::kBTile;          // S x kARawBytes
+  uint8_t* atile0 = araw0 + (size_t)S * kARawBytes;       // S x kATileBytes
+  uint64_t* bars = (uint64_t*)(atile0 + (size_t)S * kATileBytes);
+  uint64_t* full_a = bars;
+  uint64_t* full_b = bars + S;
+  uint64_t* empty = bars + 2 * S;
+  uint64_t* tfull = bars + 3 * S;
+  uint64_t* tempty = tfull + 4;
+  uint32_t* misc = (uint32_t*)(tempty + 4);  // [0] tmem base, [2..3] panel range
+  int64_t* range = (int64_t*)(misc + 2);
+  volatile uint32_t* mma_prog = (volatile uint32_t*)(range + 2);  // [kMmaWarps] next block each MMA warp waits for
+  // per decoder warp: brick-slot table (pattern, value offset) of the block being decoded
+  uint64_t* slot_pat = (uint64_t*)(range + 2 + kMmaWarps);     // [kDecWarps][kNbk]
+  uint32_t* slot_off = (uint32_t*)(slot_pat + kDecWarps * L::kNbk);  // [kDecWarps][kNbk]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  long long wacc = 0;
+  const long long t_start = kInstr ? clock64() : 0;
+  const uint32_t tmem_cols = L::kTmemCols;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_a[s], 1);
+      // B rows landed (one producer warp per block: 1 expect_tx arrive or 32 cp.async noinc arrivals) AND the
+      // block's A tile is decoded (+1 decoder arrival): the MMA warp waits on this single barrier per block
+      mbar_init(&full_b[s], (GM == 0 ? 1 : 32) + 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < L::kSlots; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    fence_mbar_init();
+    // S1: contiguous panel range with ~equal (blocks + panels) inside [p_lo, p_hi)
+    const uint64_t base = (uint64_t)prm.brp[prm.p_lo] + (uint64_t)prm.p_lo;
+    const uint64_t W = (uint64_t)prm.brp[prm.p_hi] + (uint64_t)prm.p_hi - base;
+    const uint64_t G = gridDim.x, c = blockIdx.x;
+    range[0] = panel_lower_bound(prm.brp, prm.p_lo, prm.p_hi, base + c * W / G);
+    range[1] = c + 1 == G ? prm.p_hi : panel_lower_bound(prm.brp, prm.p_lo, prm.p_hi, base + (c + 1) * W / G);
+    for (int m = 0; m < kMmaWarps; ++m) mma_prog[m] = 0u;
+    prefetch_tmap(&tmB);
+  }
+  if (warp == kMmaWarp) tmem_alloc(&misc[0], tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = misc[0];
+  const int64_t pa = range[0], pb = range[1];
+  const uint32_t* __restrict__ brp = prm.brp;
+  const int n0 = prm.n0;
+  const int64_t N = prm.N, M = prm.M;
+
+  if (warp < kProdWarps) {
+    // ---------------------------------------------------------------- producers (warps 0..3)
+    // Warp w stages blocks i = w, w+4, ... (the i-th block of this CTA uses stage i % S): the packed
+    // block bytes (S2, one bulk copy) and its 16 gathered B rows (S3). One cp.async instruction moves one
+    // contiguous 512-B row segment (lane = 16-B chunk); lanes 0..15 prefetch the block's activeCols 8 blocks
+    // ahead and the row index is broadcast by shuffle.
+    const uint64_t pol_a = policy_evict_first();
+    const int na_eff = (int)min((int64_t)L::kNA, ceil_div(N - n0, 32));  // 32-col atoms with a column < N
+    const int64_t b_begin = brp[pa], b_end = brp[pb];
+    const int pw = warp;
+    const uint32_t Kr = (uint32_t)prm.K;
+    const int64_t ldb = prm.ldb;
+    const float* __restrict__ Bsrc = prm.B + n0;
+    const uint32_t* __restrict__ acp = prm.ac;
+    const uint64_t* __restrict__ spp = prm.sp;
+    const uint8_t* __restrict__ pk = prm.packed;
+    const int row = lane & (TKV - 1);
+    const uint32_t bt0 = smem_u32(btile0);
+    // per-lane prefetch ring: block b_begin + pw + 4*(j + 8*chunk)
+    constexpr int kPf = 8;
+    uint32_t acur[kPf], anxt[kPf];
+    uint64_t scur = 0, snxt = 0;  // lane j < 8 (and j+8 < 16 for the +1) holds sp of block j of the chunk
+    auto prefetch = [&](int64_t first, uint32_t (&ar)[kPf], uint64_t& sv) {
+#pragma unroll
+      for (int j = 0; j < kPf; ++j) {
+        const int64_t bl = first + 4 * j;
+        ar[j] = bl < b_end ? __ldg(acp + bl * TKV + row) : Kr;
+      }
+      const int64_t bl = first + 4 * (lane & 7);
+      sv = 0;
+      if (lane < 16 && bl < b_end) sv = __ldg(spp + bl + (lane >> 3));
+    };
+    // lane-constant destination offsets (per 128-column tile t and row % 4) and column bounds
+    uint32_t doff[NT][4];
+    bool col_ok[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int c = lane + 32 * t;  // 16-B chunk along N
+      const int at = c >> 3;
+      const uint32_t g = (c >> 1) & 3;
+#pragma unroll
+      for (int rq = 0; rq < 4; ++rq) doff[t][rq] = at * 512 + ((g ^ rq) << 5) + ((c & 1) << 4);
+      col_ok[t] = (n0 + 4 * c) < N && at < na_eff;
+    }
+    int s = pw % S;
+    uint32_t ph = (pw / S) & 1;
+    int64_t first = b_begin + pw;
+    if (first < b_end) prefetch(first, acur, scur);
+    while (first < b_end) {
+      const int64_t nfirst = first + 4 * kPf;
+      if (nfirst < b_end) prefetch(nfirst, anxt, snxt);
+#pragma unroll
+      for (int j = 0; j < kPf; ++j) {
+        const int64_t b = first + 4 * j;
+        if (b >= b_end) break;
+        const uint64_t s0 = __shfl_sync(0xffffffffu, scur, j), s1 = __shfl_sync(0xffffffffu, scur, 8 + j);
+        mbar_wait_acc(prm, &empty[s], ph ^ 1, wacc);
+        if (lane == 0) {
+          trace_ev(prm, 0, (uint32_t)(b - b_begin));
+          const uint32_t a_bytes = (uint32_t)(s1 - s0);
+          if (dbg(prm, 8)) {
+            mbar_arrive(&full_a[s]);
+          } else {
+            mbar_expect_tx(&full_a[s], a_bytes);
+            bulk_g2s(araw0 + (size_t)s * kARawBytes, pk + s0, a_bytes, &full_a[s], pol_a);
+          }
+        }
+        const uint32_t bt = bt0 + s * L::kBTile;
+        const uint32_t r = acur[j];
+        if constexpr (GM == 0) {
+          const uint32_t r0 = __shfl_sync(0xffffffffu, r, 0), r1 = __shfl_sync(0xffffffffu, r, 1);
+          const uint32_t r2 = __shfl_sync(0xffffffffu, r, 2), r3 = __shfl_sync(0xffffffffu, r, 3);
+          const uint32_t r4 = __shfl_sync(0xffffffffu, r, 4), r5 = __shfl_sync(0xffffffffu, r, 5);
+          const uint32_t r6 = __shfl_sync(0xffffffffu, r, 6), r7 = __shfl_sync(0xffffffffu, r, 7);
+          const uint32_t r8 = __shfl_sync(0xffffffffu, r, 8), r9 = __shfl_sync(0xffffffffu, r, 9);
+          const uint32_t ra = __shfl_sync(0xffffffffu, r, 10), rb = __shfl_sync(0xffffffffu, r, 11);
+          const uint32_t rc = __shfl_sync(0xffffffffu, r, 12), rd = __shfl_sync(0xffffffffu, r, 13);
+          const uint32_t re = __shfl_sync(0xffffffffu, r, 14), rf = __shfl_sync(0xffffffffu, r, 15);
+          if (lane == 0) {
+            mbar_expect_tx(&full_b[s], 16u * 128u * (uint32_t)na_eff);
+            uint8_t* btg = btile0 + (size_t)s * L::kBTile;
+            const uint32_t rr[16] = {r0, r1, r2, r3, r4, r5, r6, r7, r8, r9, ra, rb, rc, rd, re, rf};
+#pragma unroll
+            for (int g4 = 0; g4 < 4; ++g4)
+              for (int a = 0; a < na_eff; ++a)
+                tma_gather4(btg + (g4 * L::kNA + a) * 512, &tmB, n0 + 32 * a, (int32_t)rr[4 * g4],
+                            (int32_t)rr[4 * g4 + 1], (int32_t)rr[4 * g4 + 2], (int32_t)rr[4 * g4 + 3], &full_b[s]);
+          }
+        } else {
+          // lane copies 16-B chunk c = lane + 32 t (along N) of each of the 16 rows; destination in the UMMA
+          // SWIZZLE_128B_BASE32B MN-major atom: 4 rows x 128 B, 32-B granule g stored at g ^ (row % 4).
+          // Lane-constant parts (offsets per row%4, column bound) are hoisted out of the block loop.
+#pragma unroll
+          for (int rw = 0; rw < TKV; ++rw) {
+            if (dbg(prm, 32)) break;
+            const uint32_t rk = __shfl_sync(0xffffffffu, r, rw);
+            const bool real = rk < Kr && !(dbg(prm, 16));  // sentinel K -> zero fill
+            const float* src = Bsrc + (int64_t)(real ? rk : 0) * ldb + 4 * lane;
+            const uint32_t rowb = bt + (rw >> 2) * (L::kNA * 512) + (rw & 3) * 128;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              if (t * 4 < na_eff) {
+                cp_async16(rowb + doff[t][rw & 3], src + 128 * t, (real && col_ok[t]) ? 16u : 0u);
+              }
+            }
+          }
+          if (dbg(prm, 32)) mbar_arrive(&full_b[s]);
+          else cp_async_arrive_noinc(&full_b[s]);
+        }
+        s += 4;
+        if (s >= S) { s -= S; ph ^= 1; }
+      }
+#pragma unroll
+      for (int j = 0; j < kPf; ++j) acur[j] = anxt[j];
+      scur = snxt;
+      first = nfirst;
+    }
+  } else if (warp < kMmaWarp) {
+    // ---------------------------------------------------------------- decoders (block i -> warp 4 + i % 4)
+    // Lane l expands bits l and l+32 of each brick. All four patterns are loaded first, then
+    // the values, so the per-block latency is ~3 dependent shared loads.
+    const int dw = warp - kProdWarps;
+    const int64_t b_begin = brp[pa], b_end = brp[pb];
+    const uint32_t nib_sh = (uint32_t)(lane & 15) * 4u;            // tile row r with r % 16 == lane % 16
+    const uint64_t below_row = (1ull << nib_sh) - 1ull;            // pattern bits of the rows above it
+    int s = dw % S;
+    uint32_t ph = (dw / S) & 1;
+    for (int64_t b = b_begin + dw; b < b_end; b += kDecWarps) {
+      mbar_wait_acc(prm, &full_a[s], ph, wacc);
+      if (lane == 0) trace_ev(prm, 1, (uint32_t)(b - b_begin));
+      if (dbg(prm, 2)) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_b[s]);
+        s += kDecWarps;
+        if (s >= S) { s -= S; ph ^= 1; }
+        continue;
+      }
+      const uint8_t* blk = araw0 + (size_t)s * kARawBytes;
+      float* tile = reinterpret_cast<float*>(atile0 + (size_t)s * kATileBytes);
+      const uint64_t cp = *reinterpret_cast<const uint64_t*>(blk);  // colPtr[0..7] (bytes)
+      const uint32_t nbr = blk[L::kNbc];                            // colPtr[nbc] = stored bricks
+      const uint32_t hdr = (L::kNbc + 1 + nbr + 7) & ~7u;
+      const uint64_t* pats = reinterpret_cast<const uint64_t*>(blk + hdr);
+      const float* vals = reinterpret_cast<const float*>(blk + hdr + 8 * nbr);
+      // (1) slot table: lane k < nbr owns stored brick k (CSC order); value offset = exclusive scan of popcounts
+      uint64_t* tpat = slot_pat + dw * L::kNbk;
+      uint32_t* toff = slot_off + dw * L::kNbk;
+      if (lane < L::kNbk) {  // absent bricks: pattern 0, offset 0 (their loads below stay in bounds)
+        tpat[lane] = 0ull;
+        toff[lane] = 0u;
+      }
+      __syncwarp();
+      uint64_t mypat = 0ull;
+      uint32_t mycnt = 0, myslot = 0;
+      if ((uint32_t)lane < nbr) {
+        mypat = pats[lane];
+        uint32_t bc = 0;
+#pragma unroll
+        for (int c = 1; c < L::kNbc; ++c) bc += (uint32_t)lane >= (uint32_t)((cp >> (8 * c)) & 0xFF);
+        myslot = bc * L::kNbrow + (L::kNbrow == 1 ? 0u : (uint32_t)blk[L::kNbc + 1 + lane]);
+        mycnt = __popcll(mypat);
+      }
+      uint32_t incl = mycnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if ((uint32_t)lane < nbr) {
+        tpat[myslot] = mypat;
+        toff[myslot] = incl - mycnt;
+      }
+      __syncwarp();
+      if (lane == 0) trace_ev(prm, 6, (uint32_t)(b - b_begin));
+      // (2) item q = lane + 32 j (j < TM/8) is (tile row r = q % TM, brick column bc = q / TM): the row's 4-bit
+      // nibble of the brick pattern selects up to 4 values at prefix-popcount ranks; one 16-B store
+      // per item into the K-major tile. Branch-free: every item's loads are issued before any is consumed, so a
+      // block costs ~3 dependent shared-memory round trips (a divergent per-item branch serialised them).
+      constexpr int kItems = TMV * L::kNbc / 32;
+#ifndef HRPB_DEC_CHUNK
+#define HRPB_DEC_CHUNK 8
+#endif
+      constexpr int kChunk = kItems < HRPB_DEC_CHUNK ? kItems : HRPB_DEC_CHUNK;  // items in flight per lane
+      const uint32_t* __restrict__ uvals = reinterpret_cast<const uint32_t*>(vals);
+#pragma unroll
+      for (int j0 = 0; j0 < kItems; j0 += kChunk) {
+        uint64_t ipat[kChunk];
+        uint32_t ioff[kChunk];
+#pragma unroll
+        for (int jj = 0; jj < kChunk; ++jj) {
+          const int q = lane + 32 * (j0 + jj), r = q % TMV, bc = q / TMV;
+          const int slot = bc * L::kNbrow + (r >> 4);
+          ipat[jj] = tpat[slot];
+          ioff[jj] = toff[slot];
+        }
+        uint4 iv[kChunk];
+        uint32_t inib[kChunk];
+#pragma unroll
+        for (int jj = 0; jj < kChunk; ++jj) {
+          // row r % 16 == lane % 16 for every item of this lane: the nibble shift and the below-mask are constant
+          const uint32_t nib = (uint32_t)(ipat[jj] >> nib_sh) & 0xFu;
+          const uint32_t i0 = ioff[jj] + (uint32_t)__popcll(ipat[jj] & below_row);
+          const uint32_t i1 = i0 + (nib & 1u), i2 = i1 + ((nib >> 1) & 1u), i3 = i2 + ((nib >> 2) & 1u);
+          // unselected lanes read at most 3 words past the block's values: still inside the stage ring
+          iv[jj] = make_uint4(uvals[i0], uvals[i1], uvals[i2], uvals[i3]);
+          inib[jj] = nib;
+        }
+#pragma unroll
+        for (int jj = 0; jj < kChunk; ++jj) {
+          const int q = lane + 32 * (j0 + jj), r = q % TMV, bc = q / TMV;
+          const uint32_t nib = inib[jj];
+          // FP32 -> TF32 round-to-nearest (ties away) as integer ops, value kept only where the pattern bit is set
+          // (reading R15; cvt.rna.tf32.f32 is a ~7-instruction emulation on sm_100a). Finite A assumed (R17).
+          uint4 v;
+          v.x = (iv[jj].x + 0x1000u) & ((nib & 1u) ? 0xFFFFE000u : 0u);
+          v.y = (iv[jj].y + 0x1000u) & ((nib & 2u) ? 0xFFFFE000u : 0u);
+          v.z = (iv[jj].z + 0x1000u) & ((nib & 4u) ? 0xFFFFE000u : 0u);
+          v.w = (iv[jj].w + 0x1000u) & ((nib & 8u) ? 0xFFFFE000u : 0u);
+          *reinterpret_cast<uint4*>(tile + bc * (L::kLbo / 4) + (r >> 4) * 64 + (r & 15) * 4) = v;
+        }
+      }
+      if (lane == 0) trace_ev(prm, 7, (uint32_t)(b - b_begin));
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        trace_ev(prm, 2, (uint32_t)(b - b_begin));
+        mbar_arrive(&full_b[s]);
+      }
+      s += kDecWarps;
+      if (s >= S) { s -= S; ph ^= 1; }
+    }
+  } else if (warp < kEpiWarp0) {
+    // ---------------------------------------------------------------- MMA issuers (one thread per warp)
+    // Non-empty panel pc goes to MMA warp pc % kMmaWarps and TMEM slot pc % kSlots: a single issuing warp spends
+    // several hundred cycles of dependent issue latency per block (wait, 2 MMAs, commit), so two warps overlap.
+    // Blocks of other warps' panels are skipped. A warp publishes in mma_prog the block it is about to wait for
+    // (all its earlier blocks are consumed); before a panel whose last block is i it waits until every other
+    // warp has published a block > i - S, so no stage barrier it waits on can be two phases behind (parity is
+    // unambiguous).
+    // with NT >= 3 a block is >= 6 MMAs (>= 300 tensor cycles) and one issuing warp keeps up; the skew guard
+    // would only serialise (c5 at N = 512: panels longer than the S = 4 stages)
+    constexpr int kSplit = NT <= 2 ? kMmaWarps : 1;
+    const int mw = warp - kMmaWarp;
+    const int64_t b_begin = brp[pa];
+    uint32_t pc = 0;
+    constexpr uint32_t kIdesc = idesc_tf32<TMV>();
+    // descriptors of stage 0; stage s adds s * stage bytes / 16 to the start-address field (no carry: < 256 KB)
+    const uint64_t adesc0 = umma_sdesc(smem_u32(btile0), 512, L::kNA * 512, 1);
+    const uint64_t bdesc0 = umma_sdesc(smem_u32(atile0), L::kLbo, 128, 0);
+    const uint32_t Su = (uint32_t)S;
+    PanelCursor cursor(brp, pa, pb, lane);
+    int64_t p;
+    uint32_t bb, be;
+    while (cursor.next(p, bb, be)) {
+      if (bb == be) continue;
+      if ((int)(pc % kSplit) != mw) {
+        ++pc;
+        continue;
+      }
+      const uint32_t slot = pc % L::kSlots;
+      uint32_t i = (uint32_t)(bb - b_begin);  // block index within this CTA's range
+      uint32_t st = i % Su, ph = (i / Su) & 1u;
+      if (kSplit > 1 && lane == 0) {
+        mma_prog[mw] = i;  // all of this warp's blocks before its new panel are consumed
+        const uint32_t last = i + (be - bb) - 1u;
+        if (last >= Su) {
+          const long long tg = tracing(prm) ? clock64() : 0;
+#pragma unroll
+          for (int m = 0; m < kSplit; ++m)
+            if (m != mw)
+              while (mma_prog[m] <= last - Su) {
+              }
+          if (tracing(prm)) wacc += clock64() - tg;
+        }
+      }
+      __syncwarp();
+      mbar_wait_acc(prm, &tempty[slot], ((pc / L::kSlots) & 1) ^ 1, wacc);
+      tc_fence_after();
+      const uint32_t dcol = tbase + slot * NT * TMV;
+      for (uint32_t b = bb; b < be; ++b, ++i) {
+        const int s = (int)st;
+        if (kSplit > 1 && lane == 0) mma_prog[mw] = i;
+        mbar_wait_acc(prm, &full_b[s], ph, wacc);
+        tc_fence_after();
+        if (lane == 0) {
+          trace_ev(prm, 3, i);
+          trace_ev(prm, 4, i);
+          if (dbg(prm, 4)) {
+            mbar_arrive(&empty[s]);
+          } else {
+            const uint64_t ad = adesc0 + (uint64_t)(st * (uint32_t)(L::kBTile >> 4));
+            const uint64_t bd = bdesc0 + (uint64_t)(st * (uint32_t)(kATileBytes >> 4));
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+#pragma unroll
+              for (int g = 0; g < TKV / 8; ++g)
+                umma_tf32(dcol + t * TMV, ad + (uint64_t)(((2 * g * L::kNA + 4 * t) * 512) >> 4),
+                          bd + (uint64_t)((g * 2 * L::kLbo) >> 4), kIdesc, (b > bb || g > 0) ? 1u : 0u);
+            }
+            umma_commit(&empty[s]);
+          }
+        }
+        __syncwarp();
+        if (++st == Su) { st = 0; ph ^= 1; }
+      }
+      if (lane == 0) umma_commit(&tfull[slot]);
+      __syncwarp();
+      ++pc;
+    }
+    if (kMmaWarps > 1 && lane == 0) mma_prog[mw] = 0xFFFFFFFFu;
+  } else {
+    // ---------------------------------------------------------------- epilogue (last 4 warps)
+    const int qd = warp & 3;            // TMEM lane quadrant accessible to this warp
+    const int et = tid - 32 * kEpiWarp0;  // 0..127
+    const int64_t ncols = min((int64_t)128 * NT, N - n0);
+    uint32_t pc = 0;
+    PanelCursor cursor(brp, pa, pb, lane);
+    int64_t p;
+    uint32_t bb, be;
+    while (cursor.next(p, bb, be)) {
+      const int64_t row0 = p * TMV;
+      const int nrows = (int)min((int64_t)TMV, M - row0);
+      if (bb == be) {  // empty panel: zero rows (R13)
+        for (int r = 0; r < nrows; ++r)
+          for (int64_t c = et; c < ncols; c += 128) prm.C[(row0 + r) * N + n0 + c] = 0.f;
+        continue;
+      }
+      const uint32_t slot = pc % L::kSlots;
+      mbar_wait_acc(prm, &tfull[slot], (pc / L::kSlots) & 1, wacc);
+      if (et == 0) trace_ev(prm, 5, pc);
+      tc_fence_after();
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        uint32_t v[TMV / 16][16];  // all panel rows of this lane's column: one tcgen05.wait per 128-column tile
+#pragma unroll
+        for (int c16 = 0; c16 < TMV / 16; ++c16)
+          tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + slot * NT * TMV + t * TMV + c16 * 16, v[c16]);
+        tmem_ld_wait();
+        const int64_t c = 128 * t + 32 * qd + lane;
+        if (c < ncols && !(dbg(prm, 1))) {
+          float* dst = prm.C + row0 * N + n0 + c;
+          if (nrows == TMV) {
+#pragma unroll
+            for (int r = 0; r < TMV; ++r) __stcs(dst + (int64_t)r * N, __uint_as_float(v[r >> 4][r & 15]));
+          } else {
+#pragma unroll
+            for (int r = 0; r < TMV; ++r)
+              if (r < nrows) __stcs(dst + (int64_t)r * N, __uint_as_float(v[r >> 4][r & 15]));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[slot]);
+      ++pc;
+    }
+  }
+  if (tracing(prm) && blockIdx.x == 0 && lane == 0) {
+    prm.trace[8 * kTraceN + 2 * warp] = wacc;
+    prm.trace[8 * kTraceN + 2 * warp + 1] = clock64() - t_start;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc(tbase, tmem_cols);
+  }
+}
+
+template <int NT, int GM, int TMV, int TKV>
+static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, const float* B, int64_t ldb, float* C,
+                               int64_t N, int n0, int64_t p_lo, int64_t p_hi, cudaStream_t s) {
+  using L = SmemLayout<NT, TMV, TKV>;
+  // producer warp w (and decoder warp w) owns blocks i = w mod 4; with S a multiple of 4 every stage is
+  // only ever filled by one warp, so a warp running ahead cannot alias an mbarrier phase.
+  static_assert(kDecWarps % kProdWarps == 0, "stage ownership: decoder count must be a multiple of producers");
+  auto smem_for = [](int st) {
+    return (size_t)1024 /*alignment*/ + (size_t)st * L::kStage + (3 * st + 8) * 8 + 64 + 8 * kMmaWarps + kDecWarps * L::kNbk * 12;
+  };
+  int stages = kMaxStages - kMaxStages % kDecWarps;
+  while (stages > kDecWarps && smem_for(stages) > 227 * 1024) stages -= kDecWarps;
+  static const int stage_cap = [] {
+    const char* e = getenv("HRPB_STAGES");  // experiments: cap the pipeline depth (multiple of 4)
+    return e ? atoi(e) : 0;
+  }();
+  if (stage_cap >= kDecWarps && stage_cap < stages) stages = stage_cap - stage_cap % kDecWarps;
+  const size_t smem = smem_for(stages);
+  if (smem > 227 * 1024) return HRPB_ERROR_NOT_SUPPORTED;  // (not reachable with the instantiated NT / TM / TK)
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV, TKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return cuda_status(e);
+    attr_set = true;
+  }
+  static const char* trace_path = kInstr ? getenv("HRPB_TRACE") : nullptr;
+  long long* trace = nullptr;
+  if (trace_path) {
+    trace = (long long*)dalloc(kTraceSlots * kTraceN * sizeof(long long), s);
+    cudaMemsetAsync(trace, 0, kTraceSlots * kTraceN * sizeof(long long), s);
+  }
+  static const int debug = [] {
+    const char* e = kInstr ? getenv("HRPB_DEBUG") : nullptr;
+    return e ? atoi(e) : 0;
+  }();
+  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, p_lo, p_hi, B, h->K, ldb, n0, stages,
+                 trace, debug};
+  int grid = num_sms();
+  if ((int64_t)grid > p_hi - p_lo) grid = (int)(p_hi > p_lo ? p_hi - p_lo : 1);
+  k_spmm<NT, GM, TMV, TKV><<<grid, kSpmmThreads, smem, s>>>(tm, prm);
+  note_launch();
+  if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)
+    static long long host[kTraceSlots * kTraceN];
+    cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (FILE* f = fopen(trace_path, "wb")) {
+      fwrite(host, sizeof(host), 1, f);
+      fclose(f);
+    }
+    dfree(trace, s);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);
+}
+
+// one translation unit per TK instantiates its kernels (parallel compilation): spmm_tk16.cu, spmm_tk32.cu
+template <int TKV>
+hrpb_status_t spmm_dispatch(const hrpb_handle* h, const CUtensorMap& tm, const float* Bt, int64_t ld, float* C,
+                            int64_t N, int n0, int nt, int gm, int64_t p_lo, int64_t p_hi, cudaStream_t s);
+
+}  // namespace hrpb

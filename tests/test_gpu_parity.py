@@ -218,23 +218,23 @@ def test_spmm_deterministic():
 
 
 # --------------------------------------------------------------------------- TM > 16 panels (NEXT-1)
-@pytest.mark.parametrize("tm", [32, 64])
+@pytest.mark.parametrize("tm,tk", [(32, 16), (64, 16), (16, 32), (32, 32), (64, 32)])
 @pytest.mark.parametrize("N", [8, 128, 200, 512])
-def test_spmm_exact_tm(tm, N):
+def test_spmm_exact_tm(tm, tk, N):
     w = synth.make("c1", scale=2, N=N)
     B = w.B()
-    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm)
-    assert A.tm == tm
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm, tk=tk)
+    assert A.tm == tm and A.tk == tk
     check_exact(hp.spmm(A, dev(B)).cpu().numpy(), oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B),
-                f"tm={tm} N={N}")
+                f"tm={tm} tk={tk} N={N}")
 
 
-@pytest.mark.parametrize("tm", [32, 64])
+@pytest.mark.parametrize("tm,tk", [(32, 16), (64, 16), (16, 32), (64, 32)])
 @pytest.mark.parametrize("name,scale,N", [("c2a", 4, 128), ("c3", 7, 256), ("c5", 3, 64)])
-def test_spmm_float_tm(tm, name, scale, N):
+def test_spmm_float_tm(tm, tk, name, scale, N):
     w = synth.make(name, scale=scale, N=N)
     B = w.B()
-    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm)
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm, tk=tk)
     C = hp.spmm(A, dev(B)).cpu().numpy()
     Cref, S = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B, with_bound=True)
-    check_float(C, Cref, S, f"{name} tm={tm}")
+    check_float(C, Cref, S, f"{name} tm={tm} tk={tk}")

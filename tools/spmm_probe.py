@@ -36,7 +36,8 @@ def main():
         del sys.argv[1:3]
     spec = sys.argv[1]
     name, N = (spec.split(":") + [None])[:2]
-    tms = [int(x) for x in sys.argv[2:]] or [16]
+    # TM or TMxTK (e.g. 64x32)
+    tms = [tuple(int(y) for y in x.split("x")) if "x" in x else (int(x), 16) for x in sys.argv[2:]] or [(16, 16)]
     w = synth.make(name, N=int(N) if N else None)
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     rp, ci, va = dev(w.row_ptr), dev(w.col_idx), dev(w.vals)
@@ -44,16 +45,16 @@ def main():
     C = torch.empty((w.M, w.N), dtype=torch.float32, device="cuda")
     flops = 2.0 * w.nnz * w.N
     distinct = int(np.unique(w.col_idx).size)
-    for tm in tms:
-        A = hp.build(rp, ci, va, w.M, w.K, tm=tm)
-        bms = timed(lambda: hp.build(rp, ci, va, w.M, w.K, tm=tm).free(), 5)
+    for tm, tk in tms:
+        A = hp.build(rp, ci, va, w.M, w.K, tm=tm, tk=tk)
+        bms = timed(lambda: hp.build(rp, ci, va, w.M, w.K, tm=tm, tk=tk).free(), 5)
         sms = timed(lambda: hp.spmm(A, B, out=C), 10)
         _, ac, _, _ = A.to_host()
         sum_nact = int((ac < w.K).sum())
         meta = A.packed_bytes + 4 * ac.size + 4 * (A.num_panels + 1) + 8 * (A.num_blocks + 1)
         gath = meta + 4 * w.N * sum_nact + 4 * w.M * w.N
         comp = meta + 4 * w.N * distinct + 4 * w.M * w.N
-        print(f"{name} N={w.N} nnz={w.nnz} TM={tm} NB={A.num_blocks} build {bms:.3f} ms  spmm {sms:.3f} ms  "
+        print(f"{name} N={w.N} nnz={w.nnz} TM={tm} TK={tk} NB={A.num_blocks} build {bms:.3f} ms  spmm {sms:.3f} ms  "
               f"{flops / sms / 1e6:.0f} GF/s spmm-only, {flops / (sms + bms) / 1e6:.0f} GF/s step  "
               f"gathered {gath / sms / 1e6:.0f} GB/s  compulsory {comp / sms / 1e6:.0f} GB/s", flush=True)
         A.free()
