@@ -37,6 +37,7 @@ constexpr int kMmaWarps = HRPB_MMA_WARPS;                  // non-empty panel pc
 constexpr int kEpiWarp0 = kMmaWarp + kMmaWarps;            // warps 10..13: epilogue
 constexpr int kSpmmThreads = 32 * (kEpiWarp0 + 4);        // 448
 constexpr int kMaxStages = 24;
+constexpr int kPfRing = 8;  // producer look-ahead in own blocks (x4 producer warps = 32 blocks)
 
 struct SpmmParams {
   const uint32_t* brp;
@@ -192,6 +193,8 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   // per decoder warp: brick-slot table (pattern, value offset) of the block being decoded
   uint64_t* slot_pat = (uint64_t*)(range + 2 + kMmaWarps);     // [kDecWarps][kNbk]
   uint32_t* slot_off = (uint32_t*)(slot_pat + kDecWarps * L::kNbk);  // [kDecWarps][kNbk]
+  // per producer warp: ring of kPfRing own blocks {sizePtr[b], sizePtr[b + 1], activeCols[b * TK .. + TK)}
+  uint32_t* pring = (uint32_t*)(((uintptr_t)(slot_off + kDecWarps * L::kNbk) + 15) & ~(uintptr_t)15);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   long long wacc = 0;
@@ -245,19 +248,26 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     const uint8_t* __restrict__ pk = prm.packed;
     const int row = lane & (TKV - 1);
     const uint32_t bt0 = smem_u32(btile0);
-    // per-lane prefetch ring: block b_begin + pw + 4*(j + 8*chunk)
-    constexpr int kPf = 8;
-    uint32_t acur[kPf], anxt[kPf];
-    uint64_t scur = 0, snxt = 0;  // lane j < 8 (and j+8 < 16 for the +1) holds sp of block j of the chunk
-    auto prefetch = [&](int64_t first, uint32_t (&ar)[kPf], uint64_t& sv) {
-#pragma unroll
-      for (int j = 0; j < kPf; ++j) {
-        const int64_t bl = first + 4 * j;
-        ar[j] = bl < b_end ? __ldg(acp + bl * TKV + row) : Kr;
+    const uint32_t ldb32 = (uint32_t)ldb;                       // (N < 2^31)
+    const float* __restrict__ Blane = Bsrc + 4 * lane;
+    // Look-ahead ring in shared memory, filled with cp.async (4-B activeCols rows, 8-B sizePtr pairs) kPfRing own
+    // blocks ahead and committed as one cp.async group per block: waiting for the group of block b
+    // (wait_group kPfRing - 1) never waits on a load issued in the same iteration, and a register ring would
+    // stall on the moves of its in-flight loads. The block loop is not unrolled (code size: the kernel's roles
+    // share the instruction cache).
+    constexpr int kSlotW = TKV + 4;  // words per ring slot: sp pair (4 words) + TK rows
+    uint32_t* myring = pring + pw * kPfRing * kSlotW;
+    auto fetch = [&](int64_t bl, int q) {  // stage block bl's look-ahead data into ring slot q (all lanes call)
+      uint32_t* slot = myring + q * kSlotW;
+      if (bl < b_end) {
+        if (lane < TKV)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot + 4 + lane)),
+                       "l"(acp + bl * TKV + lane) : "memory");
+        if (lane < 2)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(slot + 2 * lane)),
+                       "l"(spp + bl + lane) : "memory");
       }
-      const int64_t bl = first + 4 * (lane & 7);
-      sv = 0;
-      if (lane < 16 && bl < b_end) sv = __ldg(spp + bl + (lane >> 3));
+      asm volatile("cp.async.commit_group;" ::: "memory");
     };
     // lane-constant destination offsets (per 128-column tile t and row % 4) and column bounds
     uint32_t doff[NT][4];
@@ -273,76 +283,67 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     }
     int s = pw % S;
     uint32_t ph = (pw / S) & 1;
-    int64_t first = b_begin + pw;
-    if (first < b_end) prefetch(first, acur, scur);
-    while (first < b_end) {
-      const int64_t nfirst = first + 4 * kPf;
-      if (nfirst < b_end) prefetch(nfirst, anxt, snxt);
+    int64_t b = b_begin + pw;
 #pragma unroll
-      for (int j = 0; j < kPf; ++j) {
-        const int64_t b = first + 4 * j;
-        if (b >= b_end) break;
-        const uint64_t s0 = __shfl_sync(0xffffffffu, scur, j), s1 = __shfl_sync(0xffffffffu, scur, 8 + j);
-        mbar_wait_acc(prm, &empty[s], ph ^ 1, wacc);
-        if (lane == 0) {
-          trace_ev(prm, 0, (uint32_t)(b - b_begin));
-          const uint32_t a_bytes = (uint32_t)(s1 - s0);
-          if (dbg(prm, 8)) {
-            mbar_arrive(&full_a[s]);
-          } else {
-            mbar_expect_tx(&full_a[s], a_bytes);
-            bulk_g2s(araw0 + (size_t)s * kARawBytes, pk + s0, a_bytes, &full_a[s], pol_a);
-          }
-        }
-        const uint32_t bt = bt0 + s * L::kBTile;
-        const uint32_t r = acur[j];
-        if constexpr (GM == 0) {
-          const uint32_t r0 = __shfl_sync(0xffffffffu, r, 0), r1 = __shfl_sync(0xffffffffu, r, 1);
-          const uint32_t r2 = __shfl_sync(0xffffffffu, r, 2), r3 = __shfl_sync(0xffffffffu, r, 3);
-          const uint32_t r4 = __shfl_sync(0xffffffffu, r, 4), r5 = __shfl_sync(0xffffffffu, r, 5);
-          const uint32_t r6 = __shfl_sync(0xffffffffu, r, 6), r7 = __shfl_sync(0xffffffffu, r, 7);
-          const uint32_t r8 = __shfl_sync(0xffffffffu, r, 8), r9 = __shfl_sync(0xffffffffu, r, 9);
-          const uint32_t ra = __shfl_sync(0xffffffffu, r, 10), rb = __shfl_sync(0xffffffffu, r, 11);
-          const uint32_t rc = __shfl_sync(0xffffffffu, r, 12), rd = __shfl_sync(0xffffffffu, r, 13);
-          const uint32_t re = __shfl_sync(0xffffffffu, r, 14), rf = __shfl_sync(0xffffffffu, r, 15);
-          if (lane == 0) {
-            mbar_expect_tx(&full_b[s], 16u * 128u * (uint32_t)na_eff);
-            uint8_t* btg = btile0 + (size_t)s * L::kBTile;
-            const uint32_t rr[16] = {r0, r1, r2, r3, r4, r5, r6, r7, r8, r9, ra, rb, rc, rd, re, rf};
-#pragma unroll
-            for (int g4 = 0; g4 < 4; ++g4)
-              for (int a = 0; a < na_eff; ++a)
-                tma_gather4(btg + (g4 * L::kNA + a) * 512, &tmB, n0 + 32 * a, (int32_t)rr[4 * g4],
-                            (int32_t)rr[4 * g4 + 1], (int32_t)rr[4 * g4 + 2], (int32_t)rr[4 * g4 + 3], &full_b[s]);
-          }
+    for (int q = 0; q < kPfRing; ++q) fetch(b + 4 * q, q);
+    int q = 0;
+#pragma unroll 1
+    for (; b < b_end; b += 4) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(kPfRing - 1) : "memory");
+      __syncwarp();
+      const uint32_t* slot = myring + q * kSlotW;
+      mbar_wait_acc(prm, &empty[s], ph ^ 1, wacc);
+      if (lane == 0) {
+        trace_ev(prm, 0, (uint32_t)(b - b_begin));
+        const uint64_t s0 = *reinterpret_cast<const uint64_t*>(slot), s1 = *reinterpret_cast<const uint64_t*>(slot + 2);
+        const uint32_t a_bytes = (uint32_t)(s1 - s0);
+        if (dbg(prm, 8)) {
+          mbar_arrive(&full_a[s]);
         } else {
-          // lane copies 16-B chunk c = lane + 32 t (along N) of each of the 16 rows; destination in the UMMA
-          // SWIZZLE_128B_BASE32B MN-major atom: 4 rows x 128 B, 32-B granule g stored at g ^ (row % 4).
-          // Lane-constant parts (offsets per row%4, column bound) are hoisted out of the block loop.
-#pragma unroll
-          for (int rw = 0; rw < TKV; ++rw) {
-            if (dbg(prm, 32)) break;
-            const uint32_t rk = __shfl_sync(0xffffffffu, r, rw);
-            const bool real = rk < Kr && !(dbg(prm, 16));  // sentinel K -> zero fill
-            const float* src = Bsrc + (int64_t)(real ? rk : 0) * ldb + 4 * lane;
-            const uint32_t rowb = bt + (rw >> 2) * (L::kNA * 512) + (rw & 3) * 128;
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-              if (t * 4 < na_eff) {
-                cp_async16(rowb + doff[t][rw & 3], src + 128 * t, (real && col_ok[t]) ? 16u : 0u);
-              }
-            }
-          }
-          if (dbg(prm, 32)) mbar_arrive(&full_b[s]);
-          else cp_async_arrive_noinc(&full_b[s]);
+          mbar_expect_tx(&full_a[s], a_bytes);
+          bulk_g2s(araw0 + (size_t)s * kARawBytes, pk + s0, a_bytes, &full_a[s], pol_a);
         }
-        s += 4;
-        if (s >= S) { s -= S; ph ^= 1; }
       }
+      const uint32_t bt = bt0 + s * L::kBTile;
+      uint32_t rr[TKV];
 #pragma unroll
-      for (int j = 0; j < kPf; ++j) acur[j] = anxt[j];
-      scur = snxt;
-      first = nfirst;
+      for (int k4 = 0; k4 < TKV / 4; ++k4) {
+        const uint4 v4 = *reinterpret_cast<const uint4*>(slot + 4 + 4 * k4);
+        rr[4 * k4] = v4.x; rr[4 * k4 + 1] = v4.y; rr[4 * k4 + 2] = v4.z; rr[4 * k4 + 3] = v4.w;
+      }
+      if constexpr (GM == 0) {
+        if (lane == 0) {
+          mbar_expect_tx(&full_b[s], 16u * 128u * (uint32_t)na_eff);
+          uint8_t* btg = btile0 + (size_t)s * L::kBTile;
+#pragma unroll
+          for (int g4 = 0; g4 < 4; ++g4)
+            for (int a = 0; a < na_eff; ++a)
+              tma_gather4(btg + (g4 * L::kNA + a) * 512, &tmB, n0 + 32 * a, (int32_t)rr[4 * g4],
+                          (int32_t)rr[4 * g4 + 1], (int32_t)rr[4 * g4 + 2], (int32_t)rr[4 * g4 + 3], &full_b[s]);
+        }
+      } else {
+        // lane copies 16-B chunk c = lane + 32 t (along N) of each of the TK rows; destination in the UMMA
+        // SWIZZLE_128B_BASE32B MN-major atom: 4 rows x 128 B, 32-B granule g stored at g ^ (row % 4).
+#pragma unroll
+        for (int rw = 0; rw < TKV; ++rw) {
+          if (dbg(prm, 32)) break;
+          const uint32_t rk = rr[rw];
+          const bool real = rk < Kr && !(dbg(prm, 16));  // sentinel K -> zero fill (src-size 0)
+          const float* src = Blane + (uint64_t)(real ? rk : 0u) * ldb32;
+          const uint32_t rowb = bt + (rw >> 2) * (L::kNA * 512) + (rw & 3) * 128;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (t * 4 < na_eff) cp_async16(rowb + doff[t][rw & 3], src + 128 * t, (real && col_ok[t]) ? 16u : 0u);
+          }
+        }
+        if (dbg(prm, 32)) mbar_arrive(&full_b[s]);
+        else cp_async_arrive_noinc(&full_b[s]);
+      }
+      __syncwarp();  // every lane has read slot q before it is refilled
+      fetch(b + 4 * kPfRing, q);
+      q = q + 1 == kPfRing ? 0 : q + 1;
+      s += 4;
+      if (s >= S) { s -= S; ph ^= 1; }
     }
   } else if (warp < kMmaWarp) {
     // ---------------------------------------------------------------- decoders (block i -> warp 4 + i % 4)
@@ -604,7 +605,8 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   // only ever filled by one warp, so a warp running ahead cannot alias an mbarrier phase.
   static_assert(kDecWarps % kProdWarps == 0, "stage ownership: decoder count must be a multiple of producers");
   auto smem_for = [](int st) {
-    return (size_t)1024 /*alignment*/ + (size_t)st * L::kStage + (3 * st + 8) * 8 + 64 + 8 * kMmaWarps + kDecWarps * L::kNbk * 12;
+    return (size_t)1024 /*alignment*/ + (size_t)st * L::kStage + (3 * st + 8) * 8 + 64 + 8 * kMmaWarps +
+           kDecWarps * L::kNbk * 12 + 16 + kProdWarps * kPfRing * (TKV + 4) * 4;
   };
   int stages = kMaxStages - kMaxStages % kDecWarps;
   while (stages > kDecWarps && smem_for(stages) > 227 * 1024) stages -= kDecWarps;
