@@ -330,9 +330,6 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ ci, 
   uint64_t* keys = reinterpret_cast<uint64_t*>(my);  // sort path (aliases bm + pre)
   uint8_t* srow = my + L.off_row;
   uint16_t* sq = reinterpret_cast<uint16_t*>(my + L.off_q);
-  uint32_t* pat32 = reinterpret_cast<uint32_t*>(my + L.off_pat);
-  constexpr int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
-  constexpr int tk_sh = tk == 16 ? 4 : 5;
   const bool sorted = w.sorted;
   if (!sorted) {
 #pragma unroll
@@ -357,9 +354,15 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ ci, 
       const uint32_t off = (uint32_t)(c - mn);
       if (c < 0 || c >= K) bad_range = true;
       if (pr == r && pc >= c) bad_order = true;
-      if (sorted) keys[i] = ((uint64_t)(uint32_t)c << 32) | (uint32_t)i;
-      else if (off >= 32u * kWBmWords) bad_order = true;  // only an unsorted row can leave [mn, mx]
-      else atomicOr(&bm[off >> 5], 1u << (off & 31));
+      if (sorted) {
+        keys[i] = ((uint64_t)(uint32_t)c << 32) | (uint32_t)i;
+      } else if (off >= 32u * kWBmWords) {
+        bad_order = true;  // only an unsorted row can leave [mn, mx]
+        sq[i] = 0xFFFFu;
+      } else {
+        atomicOr(&bm[off >> 5], 1u << (off & 31));
+        sq[i] = (uint16_t)off;  // column offset, turned into the rank below (no second global load)
+      }
     }
   }
   const bool any_range = __any_sync(0xffffffffu, bad_range), any_order = __any_sync(0xffffffffu, bad_order);
@@ -381,7 +384,7 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ ci, 
     for (int c0 = 0; c0 < E; c0 += 32) {  // ranks: popcount prefix of the lower bits (R23: ascending columns)
       const int i = c0 + lane;
       if (i < E) {
-        const uint32_t off = (uint32_t)(ci[w.e0 + i] - mn);
+        const uint32_t off = sq[i];
         uint32_t qq = 0xFFFFu;
         if (off < 32u * kWBmWords) qq = pre[off >> 5] + __popc(bm[off >> 5] & ((1u << (off & 31)) - 1u));
         sq[i] = (uint16_t)qq;
@@ -586,6 +589,25 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
     const int E = w.E;
     uint64_t carry = pbase;
     for (int64_t t = w.nact + lane; t < (int64_t)nblk * tk; t += 32) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
+    // activeCols (R6, R23): the panel's distinct columns in ascending order, from the ranking structures
+    uint32_t* acp = ac + (int64_t)b0 * tk;
+    if (!w.sorted) {
+      const uint32_t* bm = reinterpret_cast<const uint32_t*>(my);
+      const uint32_t* pre = reinterpret_cast<const uint32_t*>(my + L.off_pre);
+#pragma unroll
+      for (int k = 0; k < kWBmWords / 32; ++k) {
+        const int wd = lane + 32 * k;
+        uint32_t bits = bm[wd], rank = pre[wd];
+        while (bits) {
+          const int bit = __ffs(bits) - 1;
+          acp[rank++] = (uint32_t)(w.mn + 32 * wd + bit);
+          bits &= bits - 1;
+        }
+      }
+    } else {
+      const uint64_t* keys = reinterpret_cast<const uint64_t*>(my);
+      for (int i = lane; i < w.E; i += 32) acp[sq[(uint32_t)keys[i]]] = (uint32_t)(keys[i] >> 32);
+    }
     for (uint32_t jb0 = 0; jb0 < nblk; jb0 += kChunkBlk) {
       const uint32_t nbch = min(kChunkBlk, nblk - jb0);
       if (jb0 > 0) warp_panel_patterns<tm, tk>(w, my, L, jb0, nbch);  // (chunk 0 is still in place if alone)
@@ -646,10 +668,8 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
           const uint32_t qq = sq[i];
           if (qq >= q0 && qq < q1) {
             const int r = srow[i];
-            const int32_t c = ci[w.e0 + i];
             const float v = vals[w.e0 + i];
             const uint32_t j = (qq >> tk_sh) - jb0, lc = qq & (tk - 1);
-            ac[((int64_t)b0 + jb0 + j) * tk + lc] = (uint32_t)c;
             const int bit = ((r & 15) << 2) | (int)(lc & 3);
             const uint32_t slot = j * nbk + (lc >> 2) * nbrow + (r >> 4);
             const uint32_t o = soff[slot] + __popcll(pat[slot] & ((1ull << bit) - 1ull));
