@@ -187,22 +187,24 @@ constexpr int kWWarps = 4;        // warps per CTA
 
 struct WarpLayout {  // per-warp shared memory (bytes), depends on tm/tk only
   int slots;         // brick slots per block chunk = kWSlotCap (a chunk is kWSlotCap / nbk blocks)
-  int off_pre, off_row, off_q, off_pat, off_soff, off_vbase, bytes;
+  int off_pre, off_row, off_q, off_pat, off_soff, off_vbase, off_stage, bytes;
 };
 constexpr int kWSortCap = 256;  // wide-span panels with <= 256 entries: warp bitonic sort ranking
 static_assert(kWSortCap * 8 <= 2 * kWBmWords * 4, "sort keys alias the bitmap + prefix words");
-__host__ __device__ constexpr int wcap(int, int) { return kWCap; }
+__host__ __device__ constexpr int wcap(int tm, int) { return tm == 16 ? kWCap / 2 : kWCap; }
 __host__ __device__ inline WarpLayout warp_layout(int tm, int tk) {  // (also used by the host launcher)
   const int nbk = (tk / HRPB_BRICK_K) * (tm / HRPB_BRICK_M);
   WarpLayout L;
+  const int cap = wcap(tm, tk);
   L.slots = kWSlotCap;
   L.off_pre = kWBmWords * 4;
   L.off_row = L.off_pre + kWBmWords * 4;                    // u8 row of each entry
-  L.off_q = L.off_row + kWCap;                              // u16 rank of each entry
-  L.off_pat = L.off_q + 2 * kWCap;                          // 8-B aligned
+  L.off_q = L.off_row + cap;                                // u16 rank of each entry
+  L.off_pat = (L.off_q + 2 * cap + 7) & ~7;
   L.off_soff = L.off_pat + L.slots * 8;
   L.off_vbase = (L.off_soff + L.slots * 2 + 7) & ~7;
-  L.bytes = (L.off_vbase + (kWSlotCap / nbk) * 8 + 15) & ~15;
+  L.off_stage = (L.off_vbase + (kWSlotCap / nbk) * 8 + 15) & ~15;  // staged col_idx, later the values
+  L.bytes = L.off_stage + 4 * (cap + 8);
   return L;
 }
 
@@ -219,9 +221,8 @@ struct WarpPanel {
 // per-lane registers and decides whether the warp path takes the panel: E <= kWCap and the column span
 // (first / last entries of the sorted rows) fits the bitmap. Returns false otherwise (warp-uniform).
 template <int tm, int tk>
-__device__ __forceinline__ bool warp_panel_open(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                                int64_t M, int64_t nnz, int64_t p, WarpPanel& w,
-                                                uint32_t* status) {
+__device__ __forceinline__ bool warp_panel_rows(const int64_t* __restrict__ rp, int64_t M, int64_t nnz, int64_t p,
+                                                WarpPanel& w, uint32_t* status) {
   const int lane = threadIdx.x & 31;
   const int64_t r0 = p * tm;
   const int nrows = (int)min((int64_t)tm, M - r0);
@@ -270,19 +271,28 @@ __device__ __forceinline__ bool warp_panel_open(const int64_t* __restrict__ rp, 
     const int r = lane + 32 * k;
     w.st[k] = (k < KV && r >= 1 && r < nrows) ? (uint32_t)(v[k < KV ? k : 0] - e0) : 0xFFFFFFFFu;
   }
-  if (E > wcap(tm, tk)) return false;
-  // column span from the first and last entry of each row (rows are sorted; a violation is flagged later)
+  return E <= wcap(tm, tk);
+}
+
+// Column span of a panel from the first and last entry of each (sorted) row; col(i) returns the column of panel
+// entry e0 + i. Decides the ranking method (bitmap, or warp sort for small wide panels) and whether the warp
+// path takes the panel at all.
+template <int tm, typename GetCol>
+__device__ __forceinline__ bool warp_panel_span(WarpPanel& w, GetCol col) {
+  const int lane = threadIdx.x & 31;
   int32_t mn = INT32_MAX, mx = INT32_MIN;
 #pragma unroll
-  for (int k = 0; k < KV - 1 + (tm % 32 != 0); ++k) {
+  for (int k = 0; k < (tm + 31) / 32; ++k) {
     const int r = lane + 32 * k;
-    const int64_t a = v[k];
-    const int64_t nx_same = __shfl_sync(0xffffffffu, v[k], (lane + 1) & 31);
-    const int64_t nx_next = __shfl_sync(0xffffffffu, v[k + 1], 0);
-    const int64_t b = lane == 31 ? nx_next : nx_same;  // rp[r + 1]
-    if (r < nrows && b > a) {
-      mn = min(mn, ci[a]);
-      mx = max(mx, ci[b - 1]);
+    const uint32_t nx_same = __shfl_sync(0xffffffffu, w.st[k], (lane + 1) & 31);
+    const uint32_t nx_next = __shfl_sync(0xffffffffu, w.st[k < 3 ? k + 1 : 3], 0);
+    if (r < w.nrows) {
+      const uint32_t beg = r == 0 ? 0u : w.st[k];
+      const uint32_t end = r + 1 >= w.nrows ? (uint32_t)w.E : (lane == 31 ? nx_next : nx_same);
+      if (end > beg) {
+        mn = min(mn, col(beg));
+        mx = max(mx, col(end - 1));
+      }
     }
   }
 #pragma unroll
@@ -292,10 +302,50 @@ __device__ __forceinline__ bool warp_panel_open(const int64_t* __restrict__ rp, 
   }
   w.mn = mn;
   w.sorted = false;
-  if (E == 0) return true;
+  if (w.E == 0) return true;
   if ((int64_t)mx - (int64_t)mn < 32 * kWBmWords) return true;
   w.sorted = true;
-  return E <= kWSortCap;
+  return w.E <= kWSortCap;
+}
+
+template <int tm, int tk>
+__device__ __forceinline__ bool warp_panel_open(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                int64_t M, int64_t nnz, int64_t p, WarpPanel& w,
+                                                uint32_t* status) {
+  if (!warp_panel_rows<tm, tk>(rp, M, nnz, p, w, status)) return false;
+  const int64_t e0 = w.e0;
+  return warp_panel_span<tm>(w, [&](uint32_t i) { return ci[e0 + i]; });
+}
+
+// Stages 4-byte elements [e0, e0 + E) of a CSR array into shared memory with cp.async (one latency for the
+// whole panel): 16-B copies from the 16-B aligned window around e0 (src-size clamps at nnz) when the array base
+// is 16-B aligned, else 4-B copies. Commits one cp.async group; returns the offset of e0 in the window.
+__device__ __forceinline__ int warp_stage(const void* __restrict__ base, int64_t nnz, int64_t e0, int E, uint8_t* dst,
+                                          bool al16) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(base);
+  int shift = 0;
+  if (al16) {
+    shift = (int)(e0 & 3);
+    const int64_t a0 = e0 - shift;
+    const int nch = (shift + E + 3) >> 2;
+    for (int c = lane; c < nch; c += 32) {
+      const int64_t idx = a0 + 4 * c;
+      const uint32_t bytes = idx + 4 <= nnz ? 16u : (idx < nnz ? (uint32_t)(nnz - idx) * 4u : 0u);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + 16 * c)),
+                   "l"(src + (idx < nnz ? idx : 0)), "r"(bytes) : "memory");
+    }
+  } else {
+    for (int i = lane; i < E; i += 32)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + 4 * i)), "l"(src + e0 + i)
+                   : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  return shift;
+}
+__device__ __forceinline__ void warp_stage_wait() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
 }
 
 // row map: srow[i] = local row of panel entry e0 + i; lane r fills its own row's entries (row ends from the
@@ -322,8 +372,8 @@ __device__ __forceinline__ void warp_row_map(const WarpPanel& w, uint8_t* srow) 
 // columns (ST_COL_RANGE) and in-row order (ST_COL_ORDER). Returns false if the brick slots of the
 // panel exceed the layout (then the panel is listed for the CTA path).
 template <int tm, int tk>
-__device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ ci, int64_t K, WarpPanel& w, uint8_t* my,
-                                                const WarpLayout& L, uint32_t* status) {
+__device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ scol, int64_t K, WarpPanel& w,
+                                                uint8_t* my, const WarpLayout& L, uint32_t* status) {
   const int lane = threadIdx.x & 31;
   uint32_t* bm = reinterpret_cast<uint32_t*>(my);
   uint32_t* pre = reinterpret_cast<uint32_t*>(my + L.off_pre);
@@ -344,7 +394,7 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ ci, 
   for (int c0 = 0; c0 < E; c0 += 32) {  // pass 1: validation + bitmap bits (or sort keys)
     const int i = c0 + lane;
     const int r = i < E ? srow[i] : -2;
-    const int32_t c = i < E ? ci[w.e0 + i] : 0;
+    const int32_t c = i < E ? scol[i] : 0;
     int32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
     int pr = __shfl_up_sync(0xffffffffu, r, 1);
     if (lane == 0) { pc = prev_c; pr = prev_r; }
@@ -544,6 +594,8 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
   constexpr int tk_sh = tk == 16 ? 4 : 5;
   uint16_t* soff = reinterpret_cast<uint16_t*>(my + L.off_soff);
   uint64_t* vbase = reinterpret_cast<uint64_t*>(my + L.off_vbase);
+  // 16-B cp.async staging needs 16-B aligned col_idx / values arrays
+  const bool al16 = ((reinterpret_cast<uintptr_t>(ci) | reinterpret_cast<uintptr_t>(vals)) & 15) == 0;
   while (true) {
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(ticket, 1u);
@@ -553,15 +605,22 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
     w.E = 0;
     w.nblk = 0;
     uint32_t bytes = 0;
+    int vsh = 0;
     constexpr uint32_t kChunkBlk = kWSlotCap / nbk;  // blocks whose patterns fit the slot array
     const bool is_listed = listed[p] != 0;
     if (is_listed) {
       w.nblk = nblk_listed[p];
       bytes = pbytes_listed[p];
     } else {
-      warp_panel_open<tm, tk>(rp, ci, M, nnz, p, w, status);  // (true: the classification pass agreed)
+      warp_panel_rows<tm, tk>(rp, M, nnz, p, w, status);  // (true: the classification pass agreed)
       if (w.E > 0) {
-        warp_panel_rank<tm, tk>(ci, K, w, my, L, status);
+        const int sh = warp_stage(ci, nnz, w.e0, w.E, my + L.off_stage, al16);
+        warp_stage_wait();
+        const int32_t* scol = reinterpret_cast<const int32_t*>(my + L.off_stage) + sh;
+        warp_panel_span<tm>(w, [&](uint32_t i) { return scol[i]; });
+        warp_panel_rank<tm, tk>(scol, K, w, my, L, status);
+        __syncwarp();  // the staged columns are dead: the values go into the same window, landing meanwhile
+        vsh = warp_stage(vals, nnz, w.e0, w.E, my + L.off_stage, al16);
         for (uint32_t jb0 = 0; jb0 < w.nblk; jb0 += kChunkBlk) {
           const uint32_t nb = min(kChunkBlk, w.nblk - jb0);
           warp_panel_patterns<tm, tk>(w, my, L, jb0, nb);
@@ -588,6 +647,8 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
     const uint32_t nblk = w.nblk;
     const int E = w.E;
     uint64_t carry = pbase;
+    warp_stage_wait();
+    const float* sval = reinterpret_cast<const float*>(my + L.off_stage) + vsh;
     for (int64_t t = w.nact + lane; t < (int64_t)nblk * tk; t += 32) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
     // activeCols (R6, R23): the panel's distinct columns in ascending order, from the ranking structures
     uint32_t* acp = ac + (int64_t)b0 * tk;
@@ -668,7 +729,7 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
           const uint32_t qq = sq[i];
           if (qq >= q0 && qq < q1) {
             const int r = srow[i];
-            const float v = vals[w.e0 + i];
+            const float v = sval[i];
             const uint32_t j = (qq >> tk_sh) - jb0, lc = qq & (tk - 1);
             const int bit = ((r & 15) << 2) | (int)(lc & 3);
             const uint32_t slot = j * nbk + (lc >> 2) * nbrow + (r >> 4);
