@@ -62,7 +62,7 @@ def main():
         full = d["kernel"].replace("void ", "").split("::")[-1]
         name = full.split("<")[0].strip()
         if name == "k_spmm" and "<" in full:  # k_spmm<NT, GM, TM>
-            name += "_tm" + full.split("<")[1].rstrip(">").split(",")[-1].strip()
+            name += "_tm" + full.split("<")[1].rstrip(">").split(",")[2].strip()  # k_spmm<NT, GM, TM, TK>
         traffic[name] = {"workload": tag,
                          "dram_bytes_per_launch": int(g("dram__bytes_read.sum") + g("dram__bytes_write.sum")),
                          "ncu_time_us": round(g("gpu__time_duration.sum") * 1e6, 2)}
