@@ -238,3 +238,24 @@ def test_spmm_float_tm(tm, tk, name, scale, N):
     C = hp.spmm(A, dev(B)).cpu().numpy()
     Cref, S = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B, with_bound=True)
     check_float(C, Cref, S, f"{name} tm={tm} tk={tk}")
+
+
+# --------------------------------------------------------------------------- pipelined host entry point
+@pytest.mark.parametrize("name,scale,N,tm,tk", [
+    ("c2a", 6, 128, 64, 16),   # banded: C chunks start while later B chunks are still in flight
+    ("c2a", 6, 100, 16, 16),   # N % 4 != 0: whole-matrix fallback after all of B
+    ("c3", 8, 64, 32, 32),     # power law, TK = 32, hub columns anywhere in B
+    ("c1", 3, 8, 16, 16),      # fewer panels than C chunks
+])
+def test_host_entry_pipelined_exact(name, scale, N, tm, tk):
+    w = synth.make(name, scale=scale, N=N, mode=synth.EXACT)
+    B = w.B()
+    C = hp.build_spmm_host(w.row_ptr, w.col_idx, w.vals, B, w.M, w.K, tm=tm, tk=tk)
+    check_exact(C, oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B), f"host {name} N={N} {tm}x{tk}")
+
+
+def test_host_entry_empty_and_zero_rows():
+    M, K, N = 300, 200, 16
+    rp = np.zeros(M + 1, np.int64)
+    C = hp.build_spmm_host(rp, np.zeros(0, np.int32), np.zeros(0, np.float32), np.ones((K, N), np.float32), M, K)
+    assert C.shape == (M, N) and not C.any()
