@@ -75,7 +75,6 @@ static void release(hrpb_handle* h) {
   dfree(h->ac, s);
   dfree(h->sp, s);
   dfree(h->packed, s);
-  dfree(h->bpad, s);
   delete h;
 }
 

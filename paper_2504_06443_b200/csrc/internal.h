@@ -13,9 +13,6 @@ struct hrpb_handle {
   uint64_t* sp;     // [NB_cap + 1]
   uint8_t* packed;  // [bytes_cap]
   cudaStream_t stream;  // build stream (frees are ordered on it)
-  // lazily sized SpMM workspace (padded B copy when N % 4 != 0)
-  float* bpad;
-  size_t bpad_bytes;
 };
 
 namespace hrpb {

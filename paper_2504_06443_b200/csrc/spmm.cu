@@ -46,23 +46,27 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
   if (!(h->tm == 16 || h->tm == 32 || h->tm == 64) || !(h->tk == 16 || h->tk == 32)) return HRPB_ERROR_NOT_SUPPORTED;
   EncodeTiledFn enc = get_encode();
   if (!enc) return HRPB_ERROR_NOT_SUPPORTED;
+  // per-call scratch, stream-ordered on s (a handle may serve concurrent calls on different streams): the padded
+  // B copy when its rows are not 16-B aligned, and the split-panel workspace of the S1 fix-up
   const float* Bt = B;
   int64_t ld = ldb;
+  float* bpad = nullptr;
   if ((reinterpret_cast<uintptr_t>(B) & 15) || (ld * 4) % 16) {
     const int64_t ldp = align_up(N, 4);
-    const size_t need = (size_t)h->K * ldp * sizeof(float);
-    hrpb_handle* hm = const_cast<hrpb_handle*>(h);
-    if (hm->bpad_bytes < need) {
-      if (hm->bpad) dfree(hm->bpad, s);
-      hm->bpad = (float*)dalloc(need, s);
-      hm->bpad_bytes = hm->bpad ? need : 0;
-      if (!hm->bpad) return HRPB_ERROR_OUT_OF_MEMORY;
-    }
-    k_pad_rows<<<4 * num_sms(), 256, 0, s>>>(B, h->K, N, ldb, hm->bpad, ldp);
+    bpad = (float*)dalloc((size_t)h->K * ldp * sizeof(float), s);
+    if (!bpad) return HRPB_ERROR_OUT_OF_MEMORY;
+    k_pad_rows<<<4 * num_sms(), 256, 0, s>>>(B, h->K, N, ldb, bpad, ldp);
     note_launch();
-    Bt = hm->bpad;
+    Bt = bpad;
     ld = ldp;
   }
+  const size_t ws_bytes = (size_t)num_sms() * 2 * 64 * 512 * sizeof(float);  // grid x 2 tiles x TM x 128 NT
+  float* ws = (float*)dalloc(ws_bytes + 64, s);
+  if (!ws) {
+    dfree(bpad, s);
+    return HRPB_ERROR_OUT_OF_MEMORY;
+  }
+  Scratch scr{ws, reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ws) + ws_bytes), next_epoch()};
   CUtensorMap tm;
   cuuint64_t gdim[2] = {(cuuint64_t)N, (cuuint64_t)h->K};
   cuuint64_t gstr[1] = {(cuuint64_t)ld * 4};
@@ -81,10 +85,16 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
       const char* e = getenv("HRPB_GATHER");  // 0 = TMA gather4 (TK = 16 only), 1 = cp.async (default)
       return e ? atoi(e) : 1;
     }();
-    if (h->tk == 16) st = spmm_dispatch<16>(h, tm, Bt, ld, C, N, (int)n0, nt, gm, p_lo, p_hi, s);
-    else st = spmm_dispatch<32>(h, tm, Bt, ld, C, N, (int)n0, nt, 1, p_lo, p_hi, s);
-    if (st != HRPB_SUCCESS) return st;
+    if (h->tk == 16) st = spmm_dispatch<16>(h, tm, Bt, ld, C, N, (int)n0, nt, gm, p_lo, p_hi, scr, s);
+    else st = spmm_dispatch<32>(h, tm, Bt, ld, C, N, (int)n0, nt, 1, p_lo, p_hi, scr, s);
+    if (st != HRPB_SUCCESS) {
+      dfree(ws, s);
+      dfree(bpad, s);
+      return st;
+    }
   }
+  dfree(ws, s);
+  dfree(bpad, s);
   return HRPB_SUCCESS;
 }
 

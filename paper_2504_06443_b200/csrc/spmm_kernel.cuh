@@ -18,6 +18,7 @@
 //  * warps 3..6: epilogue — tcgen05.ld 32x32b, coalesced 128-B row stores of C (S5);
 //  * mbarrier rings: full_a/full_b (TMA), dec (decoder), empty (tcgen05.commit), tfull/tempty.
 #pragma once
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -39,6 +40,17 @@ constexpr int kSpmmThreads = 32 * (kEpiWarp0 + 4);        // 448
 constexpr int kMaxStages = 24;
 constexpr int kPfRing = 8;  // producer look-ahead in own blocks (x4 producer warps = 32 blocks)
 
+// per-call scratch of hrpb_spmm: split-panel workspace, its flag word and this call's epoch
+struct Scratch {
+  float* ws;
+  uint64_t* flag;
+  uint64_t epoch;
+};
+inline uint64_t next_epoch() {
+  static std::atomic<uint64_t> e{0};
+  return ++e;
+}
+
 struct SpmmParams {
   const uint32_t* brp;
   const uint32_t* ac;
@@ -47,6 +59,9 @@ struct SpmmParams {
   float* C;
   int64_t M, N, P, NB;
   int64_t p_lo, p_hi;  // panel range of this launch (the whole matrix, or one chunk of the pipelined host path)
+  float* ws;           // split-panel partial tiles [G][2][TM][128 NT]
+  uint64_t* split_flag;  // set to `epoch` by any CTA that writes a partial tile (k_spmm_fixup runs only then)
+  uint64_t epoch;
   const float* B;  // row-major K x ldb (cp.async gather mode)
   int64_t K, ldb;
   int n0;      // first output column of this launch
@@ -120,6 +135,108 @@ __device__ __forceinline__ int64_t panel_lower_bound(const uint32_t* brp, int64_
   return lo;
 }
 
+// S1 work assignment. Work units: panel p owns units [brp[p] + p, brp[p+1] + p + 1) — one per block plus one for
+// its epilogue (so empty panels cost one unit). CTA c of G takes units [t_c, t_c+1) with t_c = c W / G snapped up
+// to the next panel start unless the panel containing it is "big" (more than half a CTA's share): such a panel
+// is split between CTAs, each accumulating its blocks into a workspace tile, and k_spmm_fixup adds the partial
+// tiles in CTA order (deterministic) into C.
+__device__ __forceinline__ int64_t panel_of_unit(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t t) {
+  // first p in [lo, hi) with brp[p + 1] + p + 1 > t (hi if none); binary search (one thread)
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((uint64_t)brp[mid + 1] + (uint64_t)mid + 1 > t) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ int64_t warp_panel_of_unit(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t t) {
+  // the same by a whole warp: 32-way search, ~log32(P) dependent loads instead of log2(P). Invariant: the answer
+  // is in [lo, hi] (hi = none in [lo, hi)).
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t idx = lo + lane * step;
+    const bool pred = idx < hi && (uint64_t)brp[idx + 1] + (uint64_t)idx + 1 > t;
+    const uint32_t m = __ballot_sync(0xffffffffu, pred);
+    if (!m) {  // every probe <= t: the answer is past the last probe inside [lo, hi)
+      const int64_t kmax = min((int64_t)31, (hi - 1 - lo) / step);
+      lo = lo + kmax * step + 1;
+      continue;
+    }
+    const int k = __ffs(m) - 1;  // f(lo + k step) > t, and f(lo + (k - 1) step) <= t when k > 0
+    if (k == 0) return lo;
+    const int64_t l0 = lo;
+    lo = l0 + (int64_t)(k - 1) * step + 1;
+    hi = l0 + (int64_t)k * step;  // (itself a candidate: "none in [lo, hi)" means hi)
+  }
+  const int64_t idx = lo + lane;
+  const bool pred = idx < hi && (uint64_t)brp[idx + 1] + (uint64_t)idx + 1 > t;
+  const uint32_t m = __ballot_sync(0xffffffffu, pred);
+  return m ? lo + __ffs(m) - 1 : hi;
+}
+// boundary t_c and the panel containing unit t_c (p_hi if t_c is the end); FIND = (brp, lo, hi, t) -> panel
+template <typename FIND>
+__device__ __forceinline__ uint64_t work_boundary(const uint32_t* brp, int64_t p_lo, int64_t p_hi, uint64_t c,
+                                                  uint64_t G, int64_t& pt, FIND find) {
+  const uint64_t base = (uint64_t)brp[p_lo] + (uint64_t)p_lo;
+  const uint64_t W = (uint64_t)brp[p_hi] + (uint64_t)p_hi - base;
+  if (c == 0) {
+    pt = p_lo;
+    return base;
+  }
+  if (c >= G) {
+    pt = p_hi;
+    return base + W;
+  }
+  const uint64_t t = base + c * W / G;
+  const int64_t p = find(brp, p_lo, p_hi, t);
+  pt = p;
+  if (p >= p_hi) return base + W;
+  const uint64_t start = (uint64_t)brp[p] + (uint64_t)p, end = (uint64_t)brp[p + 1] + (uint64_t)p + 1;
+  if (t == start) return t;
+  if ((end - start) * 2 * G > W) return t;  // big panel: split here
+  pt = p + 1;                               // small panel: round up to the next panel start
+  return end;
+}
+struct CtaWork {
+  int64_t pa, pb;      // panels [pa, pb) touched by this CTA (pb - 1 = pl, the panel of its last unit)
+  uint32_t bB, bE;     // its flat block range
+  bool first_full, last_full;  // owns all units of pa / of pb - 1
+};
+template <typename FIND>
+__device__ __forceinline__ CtaWork cta_work(const uint32_t* brp, int64_t p_lo, int64_t p_hi, uint64_t c, uint64_t G,
+                                            FIND find) {
+  CtaWork w;
+  int64_t p0, p1;
+  const uint64_t t0 = work_boundary(brp, p_lo, p_hi, c, G, p0, find);
+  const uint64_t t1 = work_boundary(brp, p_lo, p_hi, c + 1, G, p1, find);
+  if (t1 <= t0) {
+    w.pa = w.pb = p_lo;
+    w.bB = w.bE = brp[p_lo];
+    w.first_full = w.last_full = true;
+    return w;
+  }
+  w.pa = p0;  // the panel containing unit t0
+  // the panel containing unit t1 - 1: p1 unless t1 is exactly p1's first unit (then the one before)
+  const int64_t pl = (p1 >= p_hi || t1 == (uint64_t)brp[p1] + (uint64_t)p1) ? p1 - 1 : p1;
+  w.pb = pl + 1;
+  w.first_full = t0 == (uint64_t)brp[w.pa] + (uint64_t)w.pa;
+  w.last_full = t1 == (uint64_t)brp[pl + 1] + (uint64_t)pl + 1;
+  w.bB = (uint32_t)max((uint64_t)brp[w.pa], t0 - (uint64_t)w.pa);
+  w.bE = (uint32_t)min((uint64_t)brp[pl + 1], t1 - (uint64_t)pl);
+  return w;
+}
+struct SerialFind {
+  __device__ int64_t operator()(const uint32_t* b, int64_t lo, int64_t hi, uint64_t t) const {
+    return panel_of_unit(b, lo, hi, t);
+  }
+};
+struct WarpFind {
+  __device__ int64_t operator()(const uint32_t* b, int64_t lo, int64_t hi, uint64_t t) const {
+    return warp_panel_of_unit(b, lo, hi, t);
+  }
+};
+
 // Warp-cooperative iteration over panels [pa, pb): blockedRowPtr is fetched 32 panels per coalesced
 // load, one chunk ahead. All 32 lanes must call next() convergently; it returns false at the end.
 struct PanelCursor {
@@ -187,11 +304,11 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   uint64_t* empty = bars + 2 * S;
   uint64_t* tfull = bars + 3 * S;
   uint64_t* tempty = tfull + 4;
-  uint32_t* misc = (uint32_t*)(tempty + 4);  // [0] tmem base, [2..3] panel range
-  int64_t* range = (int64_t*)(misc + 2);
-  volatile uint32_t* mma_prog = (volatile uint32_t*)(range + 2);  // [kMmaWarps] next block each MMA warp waits for
+  uint32_t* misc = (uint32_t*)(tempty + 4);  // [0] tmem base
+  int64_t* range = (int64_t*)(misc + 2);     // CtaWork: pa, pb, bB, bE, first_full, last_full
+  volatile uint32_t* mma_prog = (volatile uint32_t*)(range + 6);  // [kMmaWarps] next block each MMA warp waits for
   // per decoder warp: brick-slot table (pattern, value offset) of the block being decoded
-  uint64_t* slot_pat = (uint64_t*)(range + 2 + kMmaWarps);     // [kDecWarps][kNbk]
+  uint64_t* slot_pat = (uint64_t*)(range + 6 + kMmaWarps);     // [kDecWarps][kNbk]
   uint32_t* slot_off = (uint32_t*)(slot_pat + kDecWarps * L::kNbk);  // [kDecWarps][kNbk]
   // per producer warp: ring of kPfRing own blocks {sizePtr[b], sizePtr[b + 1], activeCols[b * TK .. + TK)}
   uint32_t* pring = (uint32_t*)(((uintptr_t)(slot_off + kDecWarps * L::kNbk) + 15) & ~(uintptr_t)15);
@@ -211,21 +328,26 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     }
     for (int i = 0; i < L::kSlots; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     fence_mbar_init();
-    // S1: contiguous panel range with ~equal (blocks + panels) inside [p_lo, p_hi)
-    const uint64_t base = (uint64_t)prm.brp[prm.p_lo] + (uint64_t)prm.p_lo;
-    const uint64_t W = (uint64_t)prm.brp[prm.p_hi] + (uint64_t)prm.p_hi - base;
-    const uint64_t G = gridDim.x, c = blockIdx.x;
-    range[0] = panel_lower_bound(prm.brp, prm.p_lo, prm.p_hi, base + c * W / G);
-    range[1] = c + 1 == G ? prm.p_hi : panel_lower_bound(prm.brp, prm.p_lo, prm.p_hi, base + (c + 1) * W / G);
+
     for (int m = 0; m < kMmaWarps; ++m) mma_prog[m] = 0u;
     prefetch_tmap(&tmB);
   }
   if (warp == kMmaWarp) tmem_alloc(&misc[0], tmem_cols);
+  if (warp == 0) {  // S1: contiguous range of ~equal work (blocks + panels) in [p_lo, p_hi); big panels may split
+    const CtaWork cw = cta_work(prm.brp, prm.p_lo, prm.p_hi, blockIdx.x, gridDim.x, WarpFind());
+    if (lane == 0) {
+      range[0] = cw.pa; range[1] = cw.pb; range[2] = cw.bB; range[3] = cw.bE;
+      range[4] = cw.first_full; range[5] = cw.last_full;
+      if (cw.bB < cw.bE && !(cw.first_full && cw.last_full)) *prm.split_flag = prm.epoch;
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = misc[0];
   const int64_t pa = range[0], pb = range[1];
+  const uint32_t cbB = (uint32_t)range[2], cbE = (uint32_t)range[3];
+  const bool first_full = range[4] != 0, last_full = range[5] != 0;
   const uint32_t* __restrict__ brp = prm.brp;
   const int n0 = prm.n0;
   const int64_t N = prm.N, M = prm.M;
@@ -238,7 +360,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     // ahead and the row index is broadcast by shuffle.
     const uint64_t pol_a = policy_evict_first();
     const int na_eff = (int)min((int64_t)L::kNA, ceil_div(N - n0, 32));  // 32-col atoms with a column < N
-    const int64_t b_begin = brp[pa], b_end = brp[pb];
+    const int64_t b_begin = cbB, b_end = cbE;
     const int pw = warp;
     const uint32_t Kr = (uint32_t)prm.K;
     const int64_t ldb = prm.ldb;
@@ -350,7 +472,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     // Lane l expands bits l and l+32 of each brick. All four patterns are loaded first, then
     // the values, so the per-block latency is ~3 dependent shared loads.
     const int dw = warp - kProdWarps;
-    const int64_t b_begin = brp[pa], b_end = brp[pb];
+    const int64_t b_begin = cbB, b_end = cbE;
     const uint32_t nib_sh = (uint32_t)(lane & 15) * 4u;            // tile row r with r % 16 == lane % 16
     const uint64_t below_row = (1ull << nib_sh) - 1ull;            // pattern bits of the rows above it
     int s = dw % S;
@@ -471,7 +593,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     // would only serialise (c5 at N = 512: panels longer than the S = 4 stages)
     constexpr int kSplit = NT <= 2 ? kMmaWarps : 1;
     const int mw = warp - kMmaWarp;
-    const int64_t b_begin = brp[pa];
+    const int64_t b_begin = cbB;
     uint32_t pc = 0;
     constexpr uint32_t kIdesc = idesc_tf32<TMV>();
     // descriptors of stage 0; stage s adds s * stage bytes / 16 to the start-address field (no carry: < 256 KB)
@@ -482,7 +604,9 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     int64_t p;
     uint32_t bb, be;
     while (cursor.next(p, bb, be)) {
-      if (bb == be) continue;
+      bb = bb > cbB ? bb : cbB;  // this CTA's blocks of the panel (all of them unless the panel is split)
+      be = be < cbE ? be : cbE;
+      if (bb >= be) continue;
       if ((int)(pc % kSplit) != mw) {
         ++pc;
         continue;
@@ -550,11 +674,17 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     while (cursor.next(p, bb, be)) {
       const int64_t row0 = p * TMV;
       const int nrows = (int)min((int64_t)TMV, M - row0);
-      if (bb == be) {  // empty panel: zero rows (R13)
+      if (bb == be) {  // empty panel (always owned whole): zero rows (R13)
         for (int r = 0; r < nrows; ++r)
           for (int64_t c = et; c < ncols; c += 128) prm.C[(row0 + r) * N + n0 + c] = 0.f;
         continue;
       }
+      const bool full = (p != pa || first_full) && (p != pb - 1 || last_full);
+      if ((bb > cbB ? bb : cbB) >= (be < cbE ? be : cbE)) continue;  // split panel without blocks here
+      // a split panel's share goes to this CTA's workspace tile (slot 0: its first panel, 1: its last)
+      float* const obase = full ? prm.C + row0 * N + n0
+                                : prm.ws + ((int64_t)(2 * blockIdx.x + (p == pa ? 0 : 1)) * TMV) * (128 * NT);
+      const int64_t ostride = full ? N : 128 * NT;
       const uint32_t slot = pc % L::kSlots;
       mbar_wait_acc(prm, &tfull[slot], (pc / L::kSlots) & 1, wacc);
       if (et == 0) trace_ev(prm, 5, pc);
@@ -568,14 +698,14 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
         tmem_ld_wait();
         const int64_t c = 128 * t + 32 * qd + lane;
         if (c < ncols && !(dbg(prm, 1))) {
-          float* dst = prm.C + row0 * N + n0 + c;
+          float* dst = obase + c;
           if (nrows == TMV) {
 #pragma unroll
-            for (int r = 0; r < TMV; ++r) __stcs(dst + (int64_t)r * N, __uint_as_float(v[r >> 4][r & 15]));
+            for (int r = 0; r < TMV; ++r) __stcs(dst + (int64_t)r * ostride, __uint_as_float(v[r >> 4][r & 15]));
           } else {
 #pragma unroll
             for (int r = 0; r < TMV; ++r)
-              if (r < nrows) __stcs(dst + (int64_t)r * N, __uint_as_float(v[r >> 4][r & 15]));
+              if (r < nrows) __stcs(dst + (int64_t)r * ostride, __uint_as_float(v[r >> 4][r & 15]));
           }
         }
       }
@@ -597,15 +727,51 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   }
 }
 
+// S1 fix-up: CTA c looks at boundary c; if a big panel q is split there and c is the first boundary inside q, it
+// sums the partial tiles of every CTA holding blocks of q, in CTA order, and writes q's rows of C.
+template <int TMV>
+__global__ void __launch_bounds__(128) k_spmm_fixup(const uint32_t* __restrict__ brp, int64_t p_lo, int64_t p_hi,
+                                                    const float* __restrict__ ws, float* __restrict__ C, int64_t M,
+                                                    int64_t N, int n0, int wcols, const uint64_t* split_flag,
+                                                    uint64_t epoch) {
+  const uint64_t G = gridDim.x, c = blockIdx.x;
+  if (c == 0 || *split_flag != epoch) return;  // no split panel in this launch
+  int64_t pt;
+  const uint64_t t = work_boundary(brp, p_lo, p_hi, c, G, pt, SerialFind());
+  const uint64_t base = (uint64_t)brp[p_lo] + (uint64_t)p_lo;
+  if (t <= base) return;
+  const int64_t q = panel_of_unit(brp, p_lo, p_hi, t - 1);
+  if (q >= p_hi) return;
+  const uint64_t qs = (uint64_t)brp[q] + (uint64_t)q, qe = (uint64_t)brp[q + 1] + (uint64_t)q + 1;
+  if (t >= qe || t <= qs) return;  // boundary c is not inside q
+  if (c >= 2 && work_boundary(brp, p_lo, p_hi, c - 1, G, pt, SerialFind()) > qs) return;  // earlier one inside q
+  const int64_t row0 = q * TMV;
+  const int nrows = (int)min((int64_t)TMV, M - row0);
+  const int64_t ncols = min((int64_t)wcols, N - n0);
+  for (int64_t e = threadIdx.x; e < (int64_t)nrows * ncols; e += blockDim.x) {
+    const int r = (int)(e / ncols);
+    const int64_t col = e % ncols;
+    float acc = 0.f;
+    for (uint64_t cc = c - 1; cc < G; ++cc) {
+      const CtaWork w = cta_work(brp, p_lo, p_hi, cc, G, SerialFind());
+      if (w.pa > q) break;
+      const uint32_t b0 = max(brp[q], w.bB), b1 = min(brp[q + 1], w.bE);
+      if (b0 >= b1) continue;  // no blocks of q in CTA cc
+      acc += ws[((int64_t)(2 * cc + (q == w.pa ? 0 : 1)) * TMV + r) * wcols + col];
+    }
+    C[(row0 + r) * N + n0 + col] = acc;
+  }
+}
+
 template <int NT, int GM, int TMV, int TKV>
 static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, const float* B, int64_t ldb, float* C,
-                               int64_t N, int n0, int64_t p_lo, int64_t p_hi, cudaStream_t s) {
+                               int64_t N, int n0, int64_t p_lo, int64_t p_hi, const Scratch& scr, cudaStream_t s) {
   using L = SmemLayout<NT, TMV, TKV>;
   // producer warp w (and decoder warp w) owns blocks i = w mod 4; with S a multiple of 4 every stage is
   // only ever filled by one warp, so a warp running ahead cannot alias an mbarrier phase.
   static_assert(kDecWarps % kProdWarps == 0, "stage ownership: decoder count must be a multiple of producers");
   auto smem_for = [](int st) {
-    return (size_t)1024 /*alignment*/ + (size_t)st * L::kStage + (3 * st + 8) * 8 + 64 + 8 * kMmaWarps +
+    return (size_t)1024 /*alignment*/ + (size_t)st * L::kStage + (3 * st + 8) * 8 + 128 + 8 * kMmaWarps +
            kDecWarps * L::kNbk * 12 + 16 + kProdWarps * kPfRing * (TKV + 4) * 4;
   };
   int stages = kMaxStages - kMaxStages % kDecWarps;
@@ -633,12 +799,13 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     const char* e = kInstr ? getenv("HRPB_DEBUG") : nullptr;
     return e ? atoi(e) : 0;
   }();
-  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, p_lo, p_hi, B, h->K, ldb, n0, stages,
-                 trace, debug};
   int grid = num_sms();
   if ((int64_t)grid > p_hi - p_lo) grid = (int)(p_hi > p_lo ? p_hi - p_lo : 1);
+  SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, p_lo, p_hi, scr.ws, scr.flag, scr.epoch,
+                 B, h->K, ldb, n0, stages, trace, debug};
   k_spmm<NT, GM, TMV, TKV><<<grid, kSpmmThreads, smem, s>>>(tm, prm);
-  note_launch();
+  k_spmm_fixup<TMV><<<grid, 128, 0, s>>>(h->brp, p_lo, p_hi, scr.ws, C, h->M, N, n0, 128 * NT, scr.flag, scr.epoch);
+  note_launch(2);
   if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)
     static long long host[kTraceSlots * kTraceN];
     cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s);
@@ -656,6 +823,7 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
 // one translation unit per TK instantiates its kernels (parallel compilation): spmm_tk16.cu, spmm_tk32.cu
 template <int TKV>
 hrpb_status_t spmm_dispatch(const hrpb_handle* h, const CUtensorMap& tm, const float* Bt, int64_t ld, float* C,
-                            int64_t N, int n0, int nt, int gm, int64_t p_lo, int64_t p_hi, cudaStream_t s);
+                            int64_t N, int n0, int nt, int gm, int64_t p_lo, int64_t p_hi, const Scratch& scr,
+                            cudaStream_t s);
 
 }  // namespace hrpb

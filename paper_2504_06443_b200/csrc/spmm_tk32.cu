@@ -6,11 +6,12 @@ namespace hrpb {
 
 template <>
 hrpb_status_t spmm_dispatch<32>(const hrpb_handle* h, const CUtensorMap& tm, const float* Bt, int64_t ld, float* C,
-                                 int64_t N, int n0, int nt, int gm, int64_t p_lo, int64_t p_hi, cudaStream_t s) {
+                                 int64_t N, int n0, int nt, int gm, int64_t p_lo, int64_t p_hi, const Scratch& scr,
+                                 cudaStream_t s) {
 #define HRPB_NT(GM_, TMV_)                                                                       \
   switch (nt) {                                                                                  \
-    case 1: return launch_nt<1, GM_, TMV_, 32>(h, tm, Bt, ld, C, N, n0, p_lo, p_hi, s);          \
-    default: return launch_nt<2, GM_, TMV_, 32>(h, tm, Bt, ld, C, N, n0, p_lo, p_hi, s);         \
+    case 1: return launch_nt<1, GM_, TMV_, 32>(h, tm, Bt, ld, C, N, n0, p_lo, p_hi, scr, s);          \
+    default: return launch_nt<2, GM_, TMV_, 32>(h, tm, Bt, ld, C, N, n0, p_lo, p_hi, scr, s);         \
   }
   (void)gm;
   if (h->tm == 16) { HRPB_NT(1, 16) }

@@ -205,7 +205,12 @@ def test_host_entry_point_matches_device_path():
     check_float(C, Cref, S, "host path")
     A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
     Cd = hp.spmm(A, dev(B)).cpu().numpy()
-    assert np.array_equal(C.view(np.uint32), Cd.view(np.uint32))   # same kernels, same bits
+    check_float(Cd, Cref, S, "device path")
+    # the host path runs the SpMM in 16 panel-range launches, whose S1 work split (and hence the order in which a
+    # split panel's partial tiles are added) differs from the single launch: equal within the bound, and each
+    # path is deterministic
+    C2 = hp.build_spmm_host(w.row_ptr, w.col_idx, w.vals, B, w.M, w.K)
+    assert np.array_equal(C.view(np.uint32), C2.view(np.uint32))
 
 
 def test_spmm_deterministic():
@@ -259,3 +264,27 @@ def test_host_entry_empty_and_zero_rows():
     rp = np.zeros(M + 1, np.int64)
     C = hp.build_spmm_host(rp, np.zeros(0, np.int32), np.zeros(0, np.float32), np.ones((K, N), np.float32), M, K)
     assert C.shape == (M, N) and not C.any()
+
+
+# --------------------------------------------------------------------------- S1: split big panels + fix-up
+@pytest.mark.parametrize("tm", [16, 64])
+@pytest.mark.parametrize("N", [32, 300])
+def test_spmm_split_hub_panels(tm, N):
+    """A few hub panels each worth many CTAs' shares among thousands of small ones: the hubs are split between
+    CTAs (partial tiles in the workspace, summed by k_spmm_fixup in CTA order). Exact mode, so C is bit-exact
+    whatever the split; repeated calls are bitwise identical (deterministic fix-up order)."""
+    rng = np.random.default_rng(5)
+    M, K = 64 * 400, 30000
+    lens = rng.integers(0, 6, M)
+    for r in (tm * 7, tm * 7 + 3, tm * 200 + 1, M - 1):  # hub rows (two in one panel)
+        lens[r] = 12000
+    cols = [np.sort(rng.choice(K, n, replace=False)).astype(np.int32) for n in lens]
+    rp = np.zeros(M + 1, np.int64); rp[1:] = np.cumsum(lens)
+    ci = np.concatenate(cols)
+    v = rng.choice(np.array([-2, -1, 1, 2], np.float32), size=ci.shape[0])
+    B = rng.integers(-2, 3, (K, N)).astype(np.float32)
+    A = gpu_build(M, K, rp, ci, v, tm=tm)
+    c1 = hp.spmm(A, dev(B)).cpu().numpy()
+    check_exact(c1, oracle.csr_spmm(M, K, rp, ci, v, B), f"split hubs tm={tm} N={N}")
+    c2 = hp.spmm(A, dev(B)).cpu().numpy()
+    assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
