@@ -821,6 +821,73 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
       s_q[i] = pre[w] + __popc(bm[w] & ((1u << b) - 1u));
     }
   } else {
+    // windowed bitmap (wide but clustered columns, e.g. FEM stencils: a few 1024-column windows): distinct windows
+    // via a shared hash set, ordered by counting, then one bitmap per window and a popcount prefix over all of
+    // them. More than kMaxWin windows (scattered columns): the sort below.
+    constexpr int kWinWords = 32, kMaxWin = 32, kHash = 256;
+    uint32_t* wbm = reinterpret_cast<uint32_t*>(s_keys);         // [kMaxWin * 32] window bitmaps
+    uint32_t* wpre = wbm + kMaxWin * kWinWords;                  // [kMaxWin * 32] word prefixes
+    int32_t* hkey = reinterpret_cast<int32_t*>(wpre + kMaxWin * kWinWords);  // [kHash] window ids (-1 empty)
+    int32_t* hidx = hkey + kHash;                                // [kHash] window order
+    int32_t* wlist = hidx + kHash;                               // [kMaxWin] distinct windows
+    __shared__ int s_nwin;
+    for (int i = threadIdx.x; i < kHash; i += blockDim.x) { hkey[i] = -1; hidx[i] = -1; }
+    for (int i = threadIdx.x; i < kMaxWin * kWinWords; i += blockDim.x) wbm[i] = 0u;
+    if (threadIdx.x == 0) s_nwin = 0;
+    __syncthreads();
+    auto slot_of = [&](int32_t wv, bool insert) -> int {
+      int h = (int)(((uint32_t)wv * 2654435761u) >> 24);
+      for (int k = 0; k < kHash; ++k, h = (h + 1) & (kHash - 1)) {
+        const int32_t cur = insert ? atomicCAS(&hkey[h], -1, wv) : hkey[h];
+        if (cur == wv) return h;
+        if (cur == -1) {
+          if (insert) { atomicAdd(&s_nwin, 1); return h; }
+          return -1;
+        }
+      }
+      return -1;
+    };
+    // (a negative column — invalid CSR, flagged above — is ranked as column 0 to keep every index in bounds)
+    for (int i = threadIdx.x; i < E; i += blockDim.x) slot_of(max((int32_t)s_col[i], 0) >> 10, true);
+    __syncthreads();
+    const int nwin = s_nwin;
+    bool windowed = nwin <= kMaxWin;
+    if (windowed) {
+      if (threadIdx.x == 0) s_nwin = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < kHash; i += blockDim.x)
+        if (hkey[i] >= 0) wlist[atomicAdd(&s_nwin, 1)] = i;
+      __syncthreads();
+      if ((int)threadIdx.x < nwin) {  // order of each window = number of smaller window ids
+        const int32_t me = hkey[wlist[threadIdx.x]];
+        int ord = 0;
+        for (int k = 0; k < nwin; ++k) ord += hkey[wlist[k]] < me;
+        hidx[wlist[threadIdx.x]] = ord;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < E; i += blockDim.x) {
+        const int32_t c = max((int32_t)s_col[i], 0);
+        const int wi = hidx[slot_of(c >> 10, false)], bit = c & 1023;
+        atomicOr(&wbm[wi * kWinWords + (bit >> 5)], 1u << (bit & 31));
+      }
+      __syncthreads();
+      constexpr int kPer = kMaxWin * kWinWords / kSmallThreads;
+      uint32_t cnt[kPer], sum = 0;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) { cnt[i] = __popc(wbm[threadIdx.x * kPer + i]); sum += cnt[i]; }
+      uint32_t run = block_excl_scan<kSmallThreads>(sum, &nact, s_scan);
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) { wpre[threadIdx.x * kPer + i] = run; run += cnt[i]; }
+      __syncthreads();
+      for (int i = threadIdx.x; i < E; i += blockDim.x) {
+        const int32_t c = max((int32_t)s_col[i], 0);
+        const int wi = hidx[slot_of(c >> 10, false)], bit = c & 1023;
+        const int wd = wi * kWinWords + (bit >> 5);
+        s_q[i] = wpre[wd] + __popc(wbm[wd] & ((1u << (bit & 31)) - 1u));
+      }
+      __syncthreads();
+    }
+    if (!windowed) {
     // sort ranking: bitonic sort of (col << 32 | local index), unique flags, scan
     int n = 32;
     while (n < E) n <<= 1;
@@ -849,6 +916,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
       if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++run;
       s_q[(uint32_t)s_keys[i]] = run - 1;
     }
+    }  // !windowed
   }
   // patterns (fill_brick_nnz_pattern): brick i = bc * (TM/16) + br in CSC order
   const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;

@@ -42,9 +42,25 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps until the phase completes (or the hint expires)
+// instead of re-polling, which frees issue slots for the other roles of a warp-specialised kernel
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity), "r"(0x10000u)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+#ifdef HRPB_WAIT_HINT
+  while (!mbar_try_wait_sleep(b, parity)) {
+  }
+#else
   while (!mbar_try_wait(b, parity)) {
   }
+#endif
 }
 
 // ------------------------------------------------------------------ TMA / bulk copies
