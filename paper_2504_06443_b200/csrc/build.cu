@@ -389,30 +389,22 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ scol
   const int E = w.E;
   const int32_t mn = w.mn;
   bool bad_range = false, bad_order = false;
-  int32_t prev_c = 0;
-  int prev_r = -1;
-  for (int c0 = 0; c0 < E; c0 += 32) {  // pass 1: validation + bitmap bits (or sort keys)
-    const int i = c0 + lane;
-    const int r = i < E ? srow[i] : -2;
-    const int32_t c = i < E ? scol[i] : 0;
-    int32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
-    int pr = __shfl_up_sync(0xffffffffu, r, 1);
-    if (lane == 0) { pc = prev_c; pr = prev_r; }
-    prev_c = __shfl_sync(0xffffffffu, c, 31);
-    prev_r = __shfl_sync(0xffffffffu, r, 31);
-    if (i < E) {
-      const uint32_t off = (uint32_t)(c - mn);
-      if (c < 0 || c >= K) bad_range = true;
-      if (pr == r && pc >= c) bad_order = true;
-      if (sorted) {
-        keys[i] = ((uint64_t)(uint32_t)c << 32) | (uint32_t)i;
-      } else if (off >= 32u * kWBmWords) {
-        bad_order = true;  // only an unsorted row can leave [mn, mx]
-        sq[i] = 0xFFFFu;
-      } else {
-        atomicOr(&bm[off >> 5], 1u << (off & 31));
-        sq[i] = (uint16_t)off;  // column offset, turned into the rank below (no second global load)
-      }
+#pragma unroll 4
+  for (int i = lane; i < E; i += 32) {  // pass 1: validation + bitmap bits (or sort keys)
+    const int r = srow[i];
+    const int32_t c = scol[i];
+    // in-row order against the previous entry, read from shared memory (no shuffle chain)
+    if (i > 0 && srow[i - 1] == r && scol[i - 1] >= c) bad_order = true;
+    const uint32_t off = (uint32_t)(c - mn);
+    if (c < 0 || c >= K) bad_range = true;
+    if (sorted) {
+      keys[i] = ((uint64_t)(uint32_t)c << 32) | (uint32_t)i;
+    } else if (off >= 32u * kWBmWords) {
+      bad_order = true;  // only an unsorted row can leave [mn, mx]
+      sq[i] = 0xFFFFu;
+    } else {
+      atomicOr(&bm[off >> 5], 1u << (off & 31));
+      sq[i] = (uint16_t)off;  // column offset, turned into the rank below (no second global load)
     }
   }
   const bool any_range = __any_sync(0xffffffffu, bad_range), any_order = __any_sync(0xffffffffu, bad_order);
@@ -567,6 +559,13 @@ __device__ __forceinline__ uint64_t warp_lookback(uint64_t* st, int64_t p, uint6
   return excl;
 }
 
+#ifdef HRPB_BTRACE
+__device__ unsigned long long g_btrace[8];  // per-phase cycles summed over warps (diagnostic builds only)
+#define BT_MARK(k) do { const long long t_ = clock64(); bt[k] += t_ - bt_last; bt_last = t_; } while (0)
+#else
+#define BT_MARK(k) do { } while (0)
+#endif
+
 // Fused pass for all panels: warp-path panels are ranked, their (blocks, bytes) published, the exclusive
 // prefixes (blockedRowPtr, B2; panel byte offset, B4) found by look-back, and the panel emitted:
 // sizePtr, HRPB-v1 headers + patterns + zero padding (R7), values in brick-CSC order at popcount
@@ -596,10 +595,14 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
   uint64_t* vbase = reinterpret_cast<uint64_t*>(my + L.off_vbase);
   // 16-B cp.async staging needs 16-B aligned col_idx / values arrays
   const bool al16 = ((reinterpret_cast<uintptr_t>(ci) | reinterpret_cast<uintptr_t>(vals)) & 15) == 0;
+#ifdef HRPB_BTRACE
+  long long bt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bt_last = clock64();
+#endif
   while (true) {
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(ticket, 1u);
     const int64_t p = (int64_t)__shfl_sync(0xffffffffu, t, 0);
+    BT_MARK(0);
     if (p >= P) break;
     WarpPanel w;
     w.E = 0;
@@ -613,12 +616,15 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
       bytes = pbytes_listed[p];
     } else {
       warp_panel_rows<tm, tk>(rp, M, nnz, p, w, status);  // (true: the classification pass agreed)
+      BT_MARK(1);
       if (w.E > 0) {
         const int sh = warp_stage(ci, nnz, w.e0, w.E, my + L.off_stage, al16);
         warp_stage_wait();
+        BT_MARK(2);
         const int32_t* scol = reinterpret_cast<const int32_t*>(my + L.off_stage) + sh;
         warp_panel_span<tm>(w, [&](uint32_t i) { return scol[i]; });
         warp_panel_rank<tm, tk>(scol, K, w, my, L, status);
+        BT_MARK(3);
         __syncwarp();  // the staged columns are dead: the values go into the same window, landing meanwhile
         vsh = warp_stage(vals, nnz, w.e0, w.E, my + L.off_stage, al16);
         for (uint32_t jb0 = 0; jb0 < w.nblk; jb0 += kChunkBlk) {
@@ -635,7 +641,9 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
         for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
       }
     }
+    BT_MARK(4);
     const uint64_t ex = warp_lookback(lb, p, ((uint64_t)w.nblk << 34) | bytes);
+    BT_MARK(5);
     const uint32_t b0 = (uint32_t)(ex >> 34);
     const uint64_t pbase = ex & ((1ull << 34) - 1);
     if (lane == 0) {
@@ -653,16 +661,19 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
     // activeCols (R6, R23): the panel's distinct columns in ascending order, from the ranking structures
     uint32_t* acp = ac + (int64_t)b0 * tk;
     if (!w.sorted) {
+      // a non-zero bitmap word at a time, its 32 bits across the lanes: lane l writes bit l's column at its rank
       const uint32_t* bm = reinterpret_cast<const uint32_t*>(my);
       const uint32_t* pre = reinterpret_cast<const uint32_t*>(my + L.off_pre);
 #pragma unroll
       for (int k = 0; k < kWBmWords / 32; ++k) {
-        const int wd = lane + 32 * k;
-        uint32_t bits = bm[wd], rank = pre[wd];
-        while (bits) {
-          const int bit = __ffs(bits) - 1;
-          acp[rank++] = (uint32_t)(w.mn + 32 * wd + bit);
-          bits &= bits - 1;
+        const uint32_t mine = bm[32 * k + lane];
+        uint32_t nzw = __ballot_sync(0xffffffffu, mine != 0u);
+        while (nzw) {
+          const int kk = __ffs(nzw) - 1;
+          nzw &= nzw - 1;
+          const int wd = 32 * k + kk;
+          const uint32_t bits = __shfl_sync(0xffffffffu, mine, kk);
+          if ((bits >> lane) & 1u) acp[pre[wd] + __popc(bits & ((1u << lane) - 1u))] = (uint32_t)(w.mn + 32 * wd + lane);
         }
       }
     } else {
@@ -740,7 +751,12 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
       }
       __syncwarp();
     }
+    BT_MARK(6);
   }
+#ifdef HRPB_BTRACE
+  if (lane == 0)
+    for (int k = 0; k < 7; ++k) atomicAdd(&g_btrace[k], (unsigned long long)bt[k]);
+#endif
 }
 
 // ------------------------------------------------------------------ pass A (CTA), listed panels with <= kSmallCap entries
@@ -1283,6 +1299,15 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     if (e == cudaSuccess) e = cudaMemcpyAsync(hinfo, info, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) st = cuda_status(e);
+#ifdef HRPB_BTRACE
+    unsigned long long bt[8];
+    cudaMemcpyFromSymbol(bt, g_btrace, sizeof(bt));
+    fprintf(stderr, "btrace cycles (sum over warps): ticket %.3g rows %.3g stage %.3g rank %.3g patterns %.3g "
+            "lookback %.3g emit %.3g\n", (double)bt[0], (double)bt[1], (double)bt[2], (double)bt[3], (double)bt[4],
+            (double)bt[5], (double)bt[6]);
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_btrace, z, sizeof(z));
+#endif
   }
   dfree(q, s); dfree(cnt, s); dfree(poff, s); dfree(gpat, s); dfree(biglist, s); dfree(info, s);
   dfree(bigscr, s);
