@@ -134,7 +134,11 @@ hrpb_status_t hrpb_build_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz,
     cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking);
   });
-  constexpr int kBChunks = 32, kCChunks = 16;
+#ifndef HRPB_E2E_BCH
+#define HRPB_E2E_BCH 32
+#define HRPB_E2E_CCH 16
+#endif
+  constexpr int kBChunks = HRPB_E2E_BCH, kCChunks = HRPB_E2E_CCH;
   cudaEvent_t ev[2 + kBChunks + kCChunks];
   for (auto& x : ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
   cudaEvent_t ev_in = ev[0], ev_done = ev[1], *ev_b = ev + 2, *ev_c = ev + 2 + kBChunks;
