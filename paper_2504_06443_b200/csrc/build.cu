@@ -542,10 +542,14 @@ __device__ __forceinline__ uint64_t warp_lookback(uint64_t* st, int64_t p, uint6
   while (true) {
     const int64_t idx = j - lane;
     uint64_t v = idx >= 0 ? ld_relaxed_gpu(st + idx) : kLbP;
-    while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
+    uint32_t pm;
+    while (true) {  // only the states up to the nearest inclusive prefix are needed: wait for those alone
+      pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+      const uint32_t zm = __ballot_sync(0xffffffffu, (v >> 62) == 0);
+      const uint32_t need = pm ? ((pm & (0u - pm)) - 1u) : 0xFFFFFFFFu;  // lanes before the first P
+      if (!(zm & need)) break;
       if ((v >> 62) == 0) v = ld_relaxed_gpu(st + idx);
     }
-    const uint32_t pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
     const int last = pm ? __ffs(pm) - 1 : 31;  // lanes 0..last contribute (lane `last` has the prefix)
     uint64_t x = lane <= last ? (v & kLbMask) : 0;
 #pragma unroll
