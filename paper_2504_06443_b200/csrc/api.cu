@@ -52,11 +52,16 @@ void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
 }
 
-int num_sms() {
-  int dev = 0, n = 148;
+int num_sms() {  // cached per device (called on every launch)
+  static int cached[64] = {0};
+  int dev = 0;
   cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && cached[dev] > 0) return cached[dev];
+  int n = 148;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 148;
+  n = n > 0 ? n : 148;
+  if (dev >= 0 && dev < 64) cached[dev] = n;
+  return n;
 }
 
 static hrpb_status_t check_device() {
