@@ -241,11 +241,9 @@ def run_ours(args, rank, world, local_rank):
             for it in range(3):
                 s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s0.record(stream)
-                A = hp.build(rp_d, ci_d, v_d, M0, K0, tm=cand)
-                hp.spmm(A, B_d, out=C_d)
+                hp.build_spmm(rp_d, ci_d, v_d, B_d, M0, K0, out=C_d, tm=cand, stream=stream)
                 s1.record(stream)
                 torch.cuda.synchronize()
-                A.free()
             tm_plan[cand] = round(s0.elapsed_time(s1), 4)
         best = min(tm_plan, key=tm_plan.get)
         if world > 1:  # every rank uses rank 0's choice
@@ -254,23 +252,19 @@ def run_ours(args, rank, world, local_rank):
             best = int(t.item())
         args.tm = best
 
-    def step(evs=None):
-        if evs is not None:
-            evs[0].record(stream)
-        A = hp.build(rp_d, ci_d, v_d, M0, K0, tm=args.tm)
-        if evs is not None:
-            evs[1].record(stream)
-        hp.spmm(A, B_d, out=C_d)
-        if evs is not None:
-            evs[2].record(stream)
-        return A
+    phase = []  # (build_ms, spmm_ms) per timed step, CUDA events recorded by the library on `stream`
+
+    def step(timed=False):
+        # hrpb_build_spmm: build + SpMM enqueued back to back, one synchronisation per step
+        _, _, ms = hp.build_spmm(rp_d, ci_d, v_d, B_d, M0, K0, out=C_d, tm=args.tm, stream=stream)
+        if timed:
+            phase.append(ms)
 
     for _ in range(max(args.warmup, 3)):
-        A = step()
-        A.free()
+        step()
     torch.cuda.synchronize()
-    # structural statistics for the roofline (from the built handle, outside the timed region)
-    A = step()
+    # structural statistics for the roofline (from a built handle, outside the timed region)
+    A = hp.build(rp_d, ci_d, v_d, M0, K0, tm=args.tm)
     torch.cuda.synchronize()
     brp, ac, sp, packed_h = A.to_host()
     NB, P, packed = A.num_blocks, A.num_panels, A.packed_bytes
@@ -281,7 +275,6 @@ def run_ours(args, rank, world, local_rank):
     uniq = int(np.count_nonzero(np.bincount(ci, minlength=K0)))
 
     # ---------------------------------------------------------------- timed region
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local_rank)
     if world > 1:
@@ -290,8 +283,7 @@ def run_ours(args, rank, world, local_rank):
     launches0 = hp.launch_count()
     t0.record(stream)
     for k in range(args.steps):
-        A = step(evs[k])
-        A.free()
+        step(timed=True)
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -299,8 +291,8 @@ def run_ours(args, rank, world, local_rank):
     launches = hp.launch_count() - launches0
     clk = clocks.stop()
     ms = t0.elapsed_time(t1) / max(args.steps, 1)
-    build_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
-    spmm_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    build_ms = float(np.mean([p[0] for p in phase]))
+    spmm_ms = float(np.mean([p[1] for p in phase]))
     stats = torch.tensor([ms, build_ms, spmm_ms, float(nnz)], dtype=torch.float64, device=dev)
     if world > 1:
         mx = stats.clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -392,7 +384,8 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": WORKLOAD, "nnz_per_rank": nnz, "N": NCOL, "num_blocks": NB, "panels": P,
                        "bricks": bricks, "alpha": round(alpha, 4), "sum_nact": sum_nact, "distinct_cols": uniq,
                        "parallelism": f"row-panel shards x{world}, B broadcast once (NCCL)",
-                       "step": "hrpb_build (CSR->HRPB) + hrpb_spmm", "TM": args.tm, "TK": 16,
+                       "step": "hrpb_build_spmm: hrpb_build (CSR->HRPB) + hrpb_spmm, one sync", "TM": args.tm,
+                       "TK": 16,
                        "tm_plan_ms": tm_plan,
                        "l2": "inputs larger than L2 (CSR 134 MB + B 512 MB per rank)",
                        "build_ms": round(build_ms, 4), "spmm_ms": round(spmm_ms, 4),

@@ -97,6 +97,18 @@ hrpb_status_t hrpb_spmm(const hrpb_t A, const float* B, float* C, int64_t M, int
                         hrpb_stream_t stream);
 
 /*
+ * hrpb_build_spmm — the whole hot path on device buffers in one call: hrpb_build then hrpb_spmm, enqueued
+ * back to back on `stream` (the SpMM does not wait for the build's size read-back), one synchronization at the
+ * end. Arguments as for hrpb_build / hrpb_spmm (all DEVICE pointers).
+ *   out      : NULL (the handle is released) or receives the handle (NULL on error).
+ *   phase_ms : NULL or float[2] receiving the build and SpMM phase times measured with CUDA events on `stream`.
+ * Errors as hrpb_build / hrpb_spmm; an INVALID_CSR input is reported after the SpMM ran, C is then undefined.
+ */
+hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
+                              const int32_t* col_idx, const float* values, const float* B, float* C,
+                              const hrpb_config_t* cfg, hrpb_stream_t stream, hrpb_t* out, float* phase_ms);
+
+/*
  * hrpb_build_spmm_host — the whole hot path from HOST buffers (end-to-end entry point):
  * H2D copies of the CSR and B, hrpb_build, hrpb_spmm, D2H copy of C, returning after C is in host memory.
  * Pipelined: the CSR and then B (in 32 row chunks) are copied on a library-owned copy stream, the build runs on

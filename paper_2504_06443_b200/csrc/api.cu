@@ -111,6 +111,51 @@ hrpb_status_t hrpb_build(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   return HRPB_SUCCESS;
 }
 
+hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
+                              const int32_t* col_idx, const float* values, const float* B, float* C,
+                              const hrpb_config_t* cfg, hrpb_stream_t stream, hrpb_t* out, float* phase_ms) {
+  if (out) *out = nullptr;
+  if (M < 0 || K < 0 || N < 0 || nnz < 0 || M >= (1ll << 31) || K >= (1ll << 31) || N >= (1ll << 31) || !row_ptr)
+    return HRPB_ERROR_INVALID_VALUE;
+  if ((nnz > 0 && (!col_idx || !values)) || (M > 0 && N > 0 && !C) || (K > 0 && N > 0 && !B))
+    return HRPB_ERROR_INVALID_VALUE;
+  const int32_t tm = cfg ? cfg->tm : 16, tk = cfg ? cfg->tk : 16;
+  if (!(tm == 16 || tm == 32 || tm == 64 || tm == 128) || !(tk == 16 || tk == 32)) return HRPB_ERROR_INVALID_VALUE;
+  hrpb_status_t st = check_device();
+  if (st != HRPB_SUCCESS) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  // pinned read-back buffer and phase events, one set per host thread
+  static thread_local uint64_t* info = nullptr;
+  static thread_local cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  if (!info) {
+    if (cudaMallocHost(&info, 4 * sizeof(uint64_t)) != cudaSuccess) return HRPB_ERROR_OUT_OF_MEMORY;
+    for (auto& e : ev) cudaEventCreate(&e);
+  }
+  hrpb_handle* h = new (std::nothrow) hrpb_handle;
+  if (!h) return HRPB_ERROR_OUT_OF_MEMORY;
+  std::memset(h, 0, sizeof(*h));
+  cudaEventRecord(ev[0], s);
+  st = build_impl(M, K, nnz, row_ptr, col_idx, values, tm, tk, s, h, info);
+  cudaEventRecord(ev[1], s);
+  // the SpMM goes in right behind the build (no host round trip between them); it reads the HRPB arrays on
+  // the device, so it does not need the sizes the build reports
+  if (st == HRPB_SUCCESS && M > 0 && N > 0) st = spmm_impl(h, B, N, C, N, s);
+  cudaEventRecord(ev[2], s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (st == HRPB_SUCCESS && e != cudaSuccess) st = cuda_status(e);
+  if (st == HRPB_SUCCESS) st = build_finish(h, info, st);  // INVALID_CSR is reported here (C is then undefined)
+  if (phase_ms && st == HRPB_SUCCESS) {
+    cudaEventElapsedTime(&phase_ms[0], ev[0], ev[1]);
+    cudaEventElapsedTime(&phase_ms[1], ev[1], ev[2]);
+  }
+  if (st != HRPB_SUCCESS || !out) {
+    release(h);
+    return st;
+  }
+  *out = h;
+  return HRPB_SUCCESS;
+}
+
 hrpb_status_t hrpb_spmm(const hrpb_t A, const float* B, float* C, int64_t M, int64_t K, int64_t N,
                         hrpb_stream_t stream) {
   if (!A || N < 0) return HRPB_ERROR_INVALID_VALUE;

@@ -1224,7 +1224,8 @@ static void launch_wbuild(int tm, int tk, cudaStream_t s, const int64_t* rp, con
 }
 
 hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
-                         const float* values, int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h) {
+                         const float* values, int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h,
+                         uint64_t* deferred_info) {
   const int64_t P = ceil_div(M, tm);
   const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
   // upper bounds (no host round trip): sum_p ceil(nact_p/tk) <= nnz/tk + min(P, nnz)
@@ -1300,8 +1301,12 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     k_finalize<<<1, 1, 0, s>>>(row_ptr, M, nnz, P, h->brp, poff, h->sp, status, info);
     note_launch();
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hinfo, info, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (deferred_info) {  // (NUM_BLKS, bytes, status) land in the caller's pinned buffer; it syncs and finishes
+      if (e == cudaSuccess) e = cudaMemcpyAsync(deferred_info, info, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    } else {
+      if (e == cudaSuccess) e = cudaMemcpyAsync(hinfo, info, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    }
     if (e != cudaSuccess) st = cuda_status(e);
 #ifdef HRPB_BTRACE
     unsigned long long bt[8];
@@ -1316,9 +1321,17 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   dfree(q, s); dfree(cnt, s); dfree(poff, s); dfree(gpat, s); dfree(biglist, s); dfree(info, s);
   dfree(bigscr, s);
   dfree(ctr, s); dfree(lb, s); dfree(listed, s);
-  if (st == HRPB_SUCCESS && hinfo[2] != 0) st = HRPB_ERROR_INVALID_CSR;
-  h->NB = (int64_t)hinfo[0];
-  h->bytes = (int64_t)hinfo[1];
+  if (deferred_info) {
+    h->NB = -1;  // unknown until build_finish
+    return st;
+  }
+  return build_finish(h, hinfo, st);
+}
+
+hrpb_status_t build_finish(hrpb_handle* h, const uint64_t* info, hrpb_status_t st) {
+  if (st == HRPB_SUCCESS && info[2] != 0) st = HRPB_ERROR_INVALID_CSR;
+  h->NB = (int64_t)info[0];
+  h->bytes = (int64_t)info[1];
   return st;
 }
 

@@ -23,8 +23,12 @@ void dfree(void* p, cudaStream_t s);
 void note_launch(int n = 1);
 hrpb_status_t cuda_status(cudaError_t e);
 
+// deferred_info == NULL: synchronous (one stream sync, sizes and status read back). Otherwise the read-back is
+// enqueued into that pinned 3-word buffer and the caller synchronizes the stream and calls build_finish.
 hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
-                         const float* values, int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h);
+                         const float* values, int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h,
+                         uint64_t* deferred_info = nullptr);
+hrpb_status_t build_finish(hrpb_handle* h, const uint64_t* info, hrpb_status_t st);
 
 hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, cudaStream_t s);
 // C rows of panels [p_lo, p_hi) only (the pipelined host entry point)

@@ -59,6 +59,8 @@ def lib():
         L.hrpb_build.argtypes = [i64, i64, i64, vp, vp, vp, C.POINTER(_Config), vp, C.POINTER(vp)]
         L.hrpb_spmm.argtypes = [vp, vp, vp, i64, i64, i64, vp]
         L.hrpb_build_spmm_host.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Config), vp]
+        L.hrpb_build_spmm.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Config), vp,
+                                      C.POINTER(vp), C.POINTER(C.c_float)]
         L.hrpb_free.argtypes = [vp]
         L.hrpb_get_view.argtypes = [vp, C.POINTER(_View)]
         L.hrpb_copy_view_to_host.argtypes = [vp, vp, vp, vp, vp]
@@ -66,7 +68,7 @@ def lib():
         L.hrpb_get_error_string.restype = C.c_char_p
         L.hrpb_last_cuda_error.restype = C.c_int
         L.hrpb_launch_count.restype = C.c_int64
-        for f in ("hrpb_build", "hrpb_spmm", "hrpb_build_spmm_host", "hrpb_free", "hrpb_get_view",
+        for f in ("hrpb_build", "hrpb_spmm", "hrpb_build_spmm", "hrpb_build_spmm_host", "hrpb_free", "hrpb_get_view",
                   "hrpb_copy_view_to_host"):
             getattr(L, f).restype = C.c_int
         _lib = L
@@ -164,6 +166,28 @@ def spmm(A: Hrpb, B, out=None, stream=None):
                          _stream(stream))
     _check(st, "hrpb_spmm")
     return out
+
+
+def build_spmm(row_ptr, col_idx, values, B, M: int, K: int, out=None, tm: int = 16, tk: int = 16, stream=None,
+               keep: bool = False):
+    """hrpb_build_spmm: build + SpMM on CUDA tensors in one call (one synchronization). Returns (C, handle or
+    None, (build_ms, spmm_ms)) — the phase times are CUDA-event measured on the stream."""
+    import torch
+    if B.dim() != 2 or B.shape[0] != K:
+        raise ValueError(f"B must be ({K}, N)")
+    N = int(B.shape[1])
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=B.device)
+    nnz = int(col_idx.numel())
+    cfg = _Config(tm, tk)
+    h = C.c_void_p()
+    ms = (C.c_float * 2)()
+    st = lib().hrpb_build_spmm(M, K, N, nnz, _dev(row_ptr, torch.int64, "row_ptr"), _dev(col_idx, torch.int32, "col_idx"),
+                               _dev(values, torch.float32, "values"), _dev(B, torch.float32, "B"),
+                               _dev(out, torch.float32, "out"), C.byref(cfg), _stream(stream),
+                               C.byref(h) if keep else None, ms)
+    _check(st, "hrpb_build_spmm")
+    return out, (Hrpb(h) if keep else None), (float(ms[0]), float(ms[1]))
 
 
 def build_spmm_host(row_ptr, col_idx, values, B, M: int, K: int, out=None, tm: int = 16, tk: int = 16, stream=None):

@@ -288,3 +288,25 @@ def test_spmm_split_hub_panels(tm, N):
     check_exact(c1, oracle.csr_spmm(M, K, rp, ci, v, B), f"split hubs tm={tm} N={N}")
     c2 = hp.spmm(A, dev(B)).cpu().numpy()
     assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
+
+
+# --------------------------------------------------------------------------- fused device entry point
+@pytest.mark.parametrize("tm", [16, 64])
+def test_build_spmm_fused_matches_separate_calls(tm):
+    w = synth.make("c2a", scale=6, N=128)
+    B = dev(w.B())
+    C1, A, (bms, sms) = hp.build_spmm(dev(w.row_ptr), dev(w.col_idx), dev(w.vals), B, w.M, w.K, tm=tm, keep=True)
+    assert bms > 0 and sms > 0
+    assert_same_hrpb(A, oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm), "fused build")
+    C2 = hp.spmm(gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm), B)
+    assert torch.equal(C1.view(torch.int32), C2.view(torch.int32))   # same kernels, same launch configuration
+    Cref, S = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, w.B(), with_bound=True)
+    check_float(C1.cpu().numpy(), Cref, S, "fused")
+
+
+def test_build_spmm_fused_reports_invalid_csr():
+    rp = np.array([0, 2, 3], np.int64)
+    ci = np.array([5, 1, 0], np.int32)  # row 0 unsorted
+    v = np.ones(3, np.float32)
+    with pytest.raises(hp.HrpbError, match="INVALID_CSR"):
+        hp.build_spmm(dev(rp), dev(ci), dev(v), torch.ones((8, 4), device="cuda"), 2, 8)
