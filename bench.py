@@ -233,7 +233,10 @@ def run_ours(args, rank, world, local_rank):
         bcast_ms = s.elapsed_time(e)
     C_d = torch.empty((M0, NCOL), dtype=torch.float32, device=dev)
 
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library captures the repeated build + SpMM call into a CUDA graph,
+    # which the legacy default stream does not allow
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     tm_plan = None
     if args.tm == 0:  # plan: time one build + spmm per candidate TM (untimed, like a library autotuner)
         tm_plan = {}

@@ -103,6 +103,11 @@ hrpb_status_t hrpb_spmm(const hrpb_t A, const float* B, float* C, int64_t M, int
  *   out      : NULL (the handle is released) or receives the handle (NULL on error).
  *   phase_ms : NULL or float[2] receiving the build and SpMM phase times measured with CUDA events on `stream`.
  * Errors as hrpb_build / hrpb_spmm; an INVALID_CSR input is reported after the SpMM ran, C is then undefined.
+ * Replay: when the same arguments (pointers, sizes, config, stream, device) come twice in a row with out == NULL,
+ * the second call captures the whole enqueue sequence (allocations, kernels, read-back, frees) into a CUDA graph
+ * and later identical calls launch that graph (one host call, no launch gaps between the dependent kernels).
+ * Requires a non-default stream (capture is not possible on the legacy default stream: those calls stay eager).
+ * HRPB_NO_GRAPH=1 disables it.
  */
 hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
                               const int32_t* col_idx, const float* values, const float* B, float* C,

@@ -111,6 +111,49 @@ hrpb_status_t hrpb_build(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   return HRPB_SUCCESS;
 }
 
+// Replay plan of hrpb_build_spmm: the second consecutive call with the same arguments (and no handle requested)
+// captures the whole enqueue sequence — allocations, builder kernels, size read-back, SpMM kernels, frees —
+// into a CUDA graph; later identical calls launch the graph (one host call instead of ~40 API calls, and no
+// per-kernel launch latency between the dependent kernels). Any change of arguments falls back to eager calls.
+namespace {
+struct BuildSpmmPlan {
+  int64_t M = -1, K = -1, N = -1, nnz = -1;
+  const void *rp = nullptr, *ci = nullptr, *va = nullptr, *B = nullptr, *C = nullptr;
+  int32_t tm = 0, tk = 0;
+  cudaStream_t s = nullptr;
+  int dev = -1;
+  int hits = 0;
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;  // launches recorded while capturing (hrpb_launch_count accounting of replays)
+  bool same(int64_t M_, int64_t K_, int64_t N_, int64_t nnz_, const void* rp_, const void* ci_, const void* va_,
+            const void* B_, const void* C_, int32_t tm_, int32_t tk_, cudaStream_t s_, int dev_) const {
+    return M == M_ && K == K_ && N == N_ && nnz == nnz_ && rp == rp_ && ci == ci_ && va == va_ && B == B_ &&
+           C == C_ && tm == tm_ && tk == tk_ && s == s_ && dev == dev_;
+  }
+};
+}  // namespace
+
+// enqueue: (ev0) build (deferred read-back into `info`) (ev1) SpMM (ev2); `release_arrays` frees the handle's
+// arrays on the stream too (graph capture: the graph owns every allocation it makes)
+static hrpb_status_t enqueue_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
+                                        const int32_t* col_idx, const float* values, const float* B, float* C,
+                                        int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h, uint64_t* info,
+                                        cudaEvent_t* ev, bool capturing, bool release_arrays) {
+  const unsigned fl = capturing ? cudaEventRecordExternal : 0u;
+  cudaEventRecordWithFlags(ev[0], s, fl);
+  hrpb_status_t st = build_impl(M, K, nnz, row_ptr, col_idx, values, tm, tk, s, h, info);
+  cudaEventRecordWithFlags(ev[1], s, fl);
+  // the SpMM goes in right behind the build (no host round trip between them); it reads the HRPB arrays on
+  // the device, so it does not need the sizes the build reports
+  if (st == HRPB_SUCCESS && M > 0 && N > 0) st = spmm_impl(h, B, N, C, N, s);
+  cudaEventRecordWithFlags(ev[2], s, fl);
+  if (release_arrays) {
+    dfree(h->brp, s); dfree(h->ac, s); dfree(h->sp, s); dfree(h->packed, s);
+    h->brp = nullptr; h->ac = nullptr; h->sp = nullptr; h->packed = nullptr;
+  }
+  return st;
+}
+
 hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
                               const int32_t* col_idx, const float* values, const float* B, float* C,
                               const hrpb_config_t* cfg, hrpb_stream_t stream, hrpb_t* out, float* phase_ms) {
@@ -124,23 +167,70 @@ hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, cons
   hrpb_status_t st = check_device();
   if (st != HRPB_SUCCESS) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  // pinned read-back buffer and phase events, one set per host thread
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // pinned read-back buffer, phase events and the replay plan: one set per host thread
   static thread_local uint64_t* info = nullptr;
   static thread_local cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  static thread_local BuildSpmmPlan plan;
+  static thread_local hrpb_handle plan_h;
   if (!info) {
     if (cudaMallocHost(&info, 4 * sizeof(uint64_t)) != cudaSuccess) return HRPB_ERROR_OUT_OF_MEMORY;
     for (auto& e : ev) cudaEventCreate(&e);
   }
+  static const bool use_graph = [] {
+    const char* e = getenv("HRPB_NO_GRAPH");  // debugging aid: always run eagerly
+    return !(e && atoi(e));
+  }();
+  const bool same = plan.same(M, K, N, nnz, row_ptr, col_idx, values, B, C, tm, tk, s, dev);
+  if (!out && use_graph && same && plan.hits >= 1) {
+    if (!plan.exec) {  // capture the enqueue sequence once
+      std::memset(&plan_h, 0, sizeof(plan_h));
+      const int64_t l0 = g_launches.load();
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+      hrpb_status_t cst = HRPB_ERROR_CUDA;
+      if (e == cudaSuccess) {
+        cst = enqueue_build_spmm(M, K, N, nnz, row_ptr, col_idx, values, B, C, tm, tk, s, &plan_h, info, ev, true,
+                                 true);
+        e = cudaStreamEndCapture(s, &g);
+      }
+      if (e == cudaSuccess && cst == HRPB_SUCCESS && g) e = cudaGraphInstantiate(&plan.exec, g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (e != cudaSuccess || cst != HRPB_SUCCESS) {
+        cudaGetLastError();
+        plan.exec = nullptr;
+        plan.hits = -1000000;  // do not retry this key: eager calls from now on
+      }
+      plan.kernels = g_launches.load() - l0;
+      g_launches.fetch_sub(plan.kernels);  // counted per replay below
+    }
+    if (plan.exec) {
+      cudaError_t e = cudaGraphLaunch(plan.exec, s);
+      g_launches.fetch_add(plan.kernels);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return cuda_status(e);
+      hrpb_handle tmp;
+      std::memset(&tmp, 0, sizeof(tmp));
+      st = build_finish(&tmp, info, HRPB_SUCCESS);
+      if (phase_ms && st == HRPB_SUCCESS) {
+        cudaEventElapsedTime(&phase_ms[0], ev[0], ev[1]);
+        cudaEventElapsedTime(&phase_ms[1], ev[1], ev[2]);
+      }
+      return st;
+    }
+  }
+  if (!same) {
+    if (plan.exec) cudaGraphExecDestroy(plan.exec);
+    plan = BuildSpmmPlan();
+    plan.M = M; plan.K = K; plan.N = N; plan.nnz = nnz; plan.rp = row_ptr; plan.ci = col_idx; plan.va = values;
+    plan.B = B; plan.C = C; plan.tm = tm; plan.tk = tk; plan.s = s; plan.dev = dev;
+  }
+  ++plan.hits;
   hrpb_handle* h = new (std::nothrow) hrpb_handle;
   if (!h) return HRPB_ERROR_OUT_OF_MEMORY;
   std::memset(h, 0, sizeof(*h));
-  cudaEventRecord(ev[0], s);
-  st = build_impl(M, K, nnz, row_ptr, col_idx, values, tm, tk, s, h, info);
-  cudaEventRecord(ev[1], s);
-  // the SpMM goes in right behind the build (no host round trip between them); it reads the HRPB arrays on
-  // the device, so it does not need the sizes the build reports
-  if (st == HRPB_SUCCESS && M > 0 && N > 0) st = spmm_impl(h, B, N, C, N, s);
-  cudaEventRecord(ev[2], s);
+  st = enqueue_build_spmm(M, K, N, nnz, row_ptr, col_idx, values, B, C, tm, tk, s, h, info, ev, false, false);
   const cudaError_t e = cudaStreamSynchronize(s);
   if (st == HRPB_SUCCESS && e != cudaSuccess) st = cuda_status(e);
   if (st == HRPB_SUCCESS) st = build_finish(h, info, st);  // INVALID_CSR is reported here (C is then undefined)

@@ -310,3 +310,23 @@ def test_build_spmm_fused_reports_invalid_csr():
     v = np.ones(3, np.float32)
     with pytest.raises(hp.HrpbError, match="INVALID_CSR"):
         hp.build_spmm(dev(rp), dev(ci), dev(v), torch.ones((8, 4), device="cuda"), 2, 8)
+
+
+def test_build_spmm_graph_replay_exact():
+    """Repeated identical hrpb_build_spmm calls on a side stream: call 1 eager, call 2 captured into a CUDA graph,
+    calls 3+ replay it. Every result bit-exact (exact mode); a changed argument falls back to an eager call."""
+    w = synth.make("c1", scale=1, N=64, mode=synth.EXACT)
+    Cref = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, w.B())
+    rp, ci, v, B = dev(w.row_ptr), dev(w.col_idx), dev(w.vals), dev(w.B())
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        C = torch.empty((w.M, w.N), device="cuda")
+        for k in range(5):
+            C.fill_(float("nan"))
+            hp.build_spmm(rp, ci, v, B, w.M, w.K, out=C, stream=side)
+            side.synchronize()
+            check_exact(C.cpu().numpy(), Cref, f"call {k}")
+        C2 = torch.empty_like(C)  # new output pointer: the plan is rebuilt
+        hp.build_spmm(rp, ci, v, B, w.M, w.K, out=C2, stream=side)
+        side.synchronize()
+        check_exact(C2.cpu().numpy(), Cref, "changed out")
