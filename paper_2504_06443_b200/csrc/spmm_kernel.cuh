@@ -137,7 +137,7 @@ __device__ __forceinline__ int64_t panel_lower_bound(const uint32_t* brp, int64_
 
 // S1 work assignment. Work units: panel p owns units [brp[p] + p, brp[p+1] + p + 1) — one per block plus one for
 // its epilogue (so empty panels cost one unit). CTA c of G takes units [t_c, t_c+1) with t_c = c W / G snapped up
-// to the next panel start unless the panel containing it is "big" (more than half a CTA's share): such a panel
+// to the next panel start unless the panel containing it is "big" (more than a whole CTA share): such a panel
 // is split between CTAs, each accumulating its blocks into a workspace tile, and k_spmm_fixup adds the partial
 // tiles in CTA order (deterministic) into C.
 __device__ __forceinline__ int64_t panel_of_unit(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t t) {
@@ -194,7 +194,7 @@ __device__ __forceinline__ uint64_t work_boundary(const uint32_t* brp, int64_t p
   if (p >= p_hi) return base + W;
   const uint64_t start = (uint64_t)brp[p] + (uint64_t)p, end = (uint64_t)brp[p + 1] + (uint64_t)p + 1;
   if (t == start) return t;
-  if ((end - start) * 2 * G > W) return t;  // big panel: split here
+  if ((end - start) * G > W) return t;  // big panel (more than a whole CTA share): split here
   pt = p + 1;                               // small panel: round up to the next panel start
   return end;
 }
