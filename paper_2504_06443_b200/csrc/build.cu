@@ -182,11 +182,17 @@ __device__ __forceinline__ void warp_panel_rows(const int64_t* __restrict__ rp, 
 // Panels that do not fit go to the CTA / hub paths (k_count, k_count_big, k_emit), listed by k_wclassify.
 constexpr int kWCap = 1024;       // entries per panel on the warp path (TM = 128: 512, see wcap)
 constexpr int kWBmWords = 256;    // bitmap words: column span <= 8192
-constexpr int kWSlotCap = 256;    // brick slots held at once: patterns are built per chunk of blocks
+// brick slots held at once (patterns are built per chunk of blocks): 16 blocks' worth, at most 128 slots — the
+// per-warp shared memory bounds the resident warps of this latency-bound kernel (measured on c2a: 256 slots
+// 0.333 / 0.427 ms at TM = 64 / 16, 128 slots 0.322 / 0.401, 64 slots 0.407 (two chunks) / 0.377)
+__host__ __device__ constexpr int wslots(int tm, int tk) {
+  return 16 * (tk / HRPB_BRICK_K) * (tm / HRPB_BRICK_M) < 128 ? 16 * (tk / HRPB_BRICK_K) * (tm / HRPB_BRICK_M)
+                                                                : 128;
+}
 constexpr int kWWarps = 4;        // warps per CTA
 
 struct WarpLayout {  // per-warp shared memory (bytes), depends on tm/tk only
-  int slots;         // brick slots per block chunk = kWSlotCap (a chunk is kWSlotCap / nbk blocks)
+  int slots;         // brick slots per block chunk = wslots (a chunk is wslots / nbk blocks)
   int off_pre, off_row, off_q, off_pat, off_soff, off_vbase, off_stage, bytes;
 };
 constexpr int kWSortCap = 256;  // wide-span panels with <= 256 entries: warp bitonic sort ranking
@@ -196,14 +202,14 @@ __host__ __device__ inline WarpLayout warp_layout(int tm, int tk) {  // (also us
   const int nbk = (tk / HRPB_BRICK_K) * (tm / HRPB_BRICK_M);
   WarpLayout L;
   const int cap = wcap(tm, tk);
-  L.slots = kWSlotCap;
+  L.slots = wslots(tm, tk);
   L.off_pre = kWBmWords * 4;
   L.off_row = L.off_pre + kWBmWords * 4;                    // u8 row of each entry
   L.off_q = L.off_row + cap;                                // u16 rank of each entry
   L.off_pat = (L.off_q + 2 * cap + 7) & ~7;
   L.off_soff = L.off_pat + L.slots * 8;
   L.off_vbase = (L.off_soff + L.slots * 2 + 7) & ~7;
-  L.off_stage = (L.off_vbase + (kWSlotCap / nbk) * 8 + 15) & ~15;  // staged col_idx, later the values
+  L.off_stage = (L.off_vbase + (L.slots / nbk) * 8 + 15) & ~15;  // staged col_idx, later the values
   L.bytes = L.off_stage + 4 * (cap + 8);
   return L;
 }
@@ -613,7 +619,7 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
     w.nblk = 0;
     uint32_t bytes = 0;
     int vsh = 0;
-    constexpr uint32_t kChunkBlk = kWSlotCap / nbk;  // blocks whose patterns fit the slot array
+    constexpr uint32_t kChunkBlk = wslots(tm, tk) / nbk;  // blocks whose patterns fit the slot array
     const bool is_listed = listed[p] != 0;
     if (is_listed) {
       w.nblk = nblk_listed[p];
