@@ -125,15 +125,6 @@ struct SmemLayout {
   static_assert(2 * NT * TMV <= 512, "two TMEM accumulator slots must fit in 512 columns");
 };
 
-__device__ __forceinline__ int64_t panel_lower_bound(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t target) {
-  // first p in [lo, hi] with brp[p] + p >= target (brp[p] + p strictly increasing)
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if ((uint64_t)brp[mid] + (uint64_t)mid >= target) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo;
-}
 
 // S1 work assignment. Work units: panel p owns units [brp[p] + p, brp[p+1] + p + 1) — one per block plus one for
 // its epilogue (so empty panels cost one unit). CTA c of G takes units [t_c, t_c+1) with t_c = c W / G snapped up
