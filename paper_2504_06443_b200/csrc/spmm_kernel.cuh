@@ -119,7 +119,7 @@ struct SmemLayout {
   static constexpr int kStage = kBTile + kARawBytes + kATileBytes;
   // TMEM accumulator slots (panels in flight between the MMA warp and the epilogue): up to 4
   static constexpr int kSlots = 4 * NT * TMV <= 512 ? 4 : 2;
-  static_assert(kSlots % kMmaWarps == 0, "a TMEM slot must always be used by the same MMA warp");
+  static_assert(kSlots % (NT <= 2 ? kMmaWarps : 1) == 0, "a TMEM slot must always be used by the same MMA warp");
   static constexpr int kSlotCols = kSlots * NT * TMV;
   static constexpr uint32_t kTmemCols = kSlotCols <= 32 ? 32 : (kSlotCols <= 64 ? 64 : (kSlotCols <= 128 ? 128 : (kSlotCols <= 256 ? 256 : 512)));
   static_assert(2 * NT * TMV <= 512, "two TMEM accumulator slots must fit in 512 columns");
