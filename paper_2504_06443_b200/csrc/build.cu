@@ -35,6 +35,8 @@ constexpr int kSmallThreads = 128;
 constexpr int kSmallCap = 2048;      // entries per panel handled in shared memory
 constexpr int kSpanWords = 512;      // bitmap ranking when the panel's column span <= 16384
 constexpr int kBigThreads = 512;
+constexpr int64_t kHubEmit = 16384;
+constexpr int64_t kHubChunk = 4096;  // listed panels with more entries get their values scattered by all CTAs
 constexpr int kEmitThreads = 128;
 
 // ------------------------------------------------------------------ block-wide helpers
@@ -975,7 +977,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
 }
 
 // ------------------------------------------------------------------ pass A, panels with > kSmallCap entries
-// Persistent CTAs over the hub-panel list; each CTA owns a global bitmap over the panel's column span.
+// Persistent CTAs over the hub-panel list. Ranks by a two-level bitmap over the column space: bm (one bit per
+// column, W = K/32 words) and occ (one bit per bm word). Only the words a panel touches are visited: occupied
+// words get dense ordinals (popcount prefix over occ), their popcounts are scanned densely, and
+// rank(c) = dense prefix of c's word + popcount of the lower bits. The bitmaps are zero between panels (cleared
+// word by word after use, zeroed once per CTA at its first panel), so the work is O(entries + K/1024) per panel
+// instead of O(column span) (R-MAT panels span all 4M columns with a few thousand entries).
 __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __restrict__ rp,
                                                           const int32_t* __restrict__ ci, int64_t M, int64_t K,
                                                           int64_t nnz, int tm, int tk, uint32_t* __restrict__ q,
@@ -988,61 +995,87 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
                                                           int64_t words_per_cta, uint32_t* status) {
   __shared__ int64_t s_rp[129];
   __shared__ uint32_t s_scan[kBigThreads / 32 + 1];
-  __shared__ int32_t s_mm[2 * kBigThreads / 32];
-  uint32_t* bm = scratch + (int64_t)blockIdx.x * 2 * words_per_cta;
-  uint32_t* pre = bm + words_per_cta;
+  const int64_t W = words_per_cta;          // >= K/32 + 2
+  const int64_t W1 = (W + 31) / 32;         // occupancy words
+  uint32_t* bm = scratch + (int64_t)blockIdx.x * (2 * W + 2 * W1);
+  uint32_t* dense = bm + W;                 // popcount prefix of the occupied words, in ordinal order
+  uint32_t* occ = dense + W;
+  uint32_t* occ_pre = occ + W1;
   const uint32_t count = *nbig;
   const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  if (blockIdx.x < count) {  // establish the all-zero invariant once
+    for (int64_t i = threadIdx.x; i < W; i += blockDim.x) bm[i] = 0u;
+    for (int64_t i = threadIdx.x; i < W1; i += blockDim.x) occ[i] = 0u;
+    __threadfence_block();
+  }
   for (uint32_t t = blockIdx.x; t < count; t += gridDim.x) {
     const int64_t p = biglist[t];
-    load_panel_rows(rp, M, nnz, tm, p, s_rp, status);
+    load_panel_rows(rp, M, nnz, tm, p, s_rp, status);  // (barriers: also orders the zeroing above)
     const int nrows = (int)min((int64_t)tm, M - p * tm);
     const int64_t e0 = s_rp[0], e1 = s_rp[nrows];
-    int32_t mn = INT32_MAX, mx = INT32_MIN;
+    // (1) bits + occupancy + validation
     for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
       const int32_t c = ci[e];
-      const bool ok = c >= 0 && c < K;
-      if (!ok) atomicOr(status, ST_COL_RANGE);
+      if (c < 0 || c >= K) { atomicOr(status, ST_COL_RANGE); continue; }
       const int r = row_of(s_rp, nrows, e);
       if (e > s_rp[r] && ci[e - 1] >= c) atomicOr(status, ST_COL_ORDER);
-      if (ok) { mn = min(mn, c); mx = max(mx, c); }
-    }
-    block_minmax<kBigThreads>(mn, mx, s_mm);
-    if (mn > mx) { mn = 0; mx = 0; }
-    const int64_t base = mn >> 5;
-    const int64_t W = (mx >> 5) - base + 1;
-    for (int64_t i = threadIdx.x; i < W; i += blockDim.x) bm[i] = 0;
-    __syncthreads();
-    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      const int32_t c = ci[e];
-      if (c >= 0 && c < K) atomicOr(&bm[(c >> 5) - base], 1u << (c & 31));
+      const uint32_t w = (uint32_t)c >> 5;
+      const uint32_t old = atomicOr(&bm[w], 1u << (c & 31));
+      if (old == 0u) atomicOr(&occ[w >> 5], 1u << (w & 31));
     }
     __threadfence_block();
     __syncthreads();
-    const int64_t per = (W + blockDim.x - 1) / blockDim.x;
-    const int64_t beg = threadIdx.x * per, end = min(W, beg + per);
+    // (2) ordinals of the occupied words: exclusive popcount prefix over occ (W1 words, per-thread runs)
+    const int64_t per = (W1 + blockDim.x - 1) / blockDim.x;
+    const int64_t beg = threadIdx.x * per, end = min(W1, beg + per);
     uint32_t sum = 0;
-    for (int64_t i = beg; i < end; ++i) sum += __popc(__ldcg(&bm[i]));
-    uint32_t nact;
-    uint32_t run = block_excl_scan<kBigThreads>(sum, &nact, s_scan);
-    for (int64_t i = beg; i < end; ++i) { pre[i] = run; run += __popc(__ldcg(&bm[i])); }
+    for (int64_t i = beg; i < end; ++i) sum += __popc(__ldcg(&occ[i]));
+    uint32_t nocc;
+    uint32_t run = block_excl_scan<kBigThreads>(sum, &nocc, s_scan);
+    for (int64_t i = beg; i < end; ++i) {
+      occ_pre[i] = run;
+      // (3) popcount of every occupied word at its ordinal
+      uint32_t o = __ldcg(&occ[i]), k = run;
+      while (o) {
+        const int b = __ffs(o) - 1;
+        o &= o - 1;
+        dense[k++] = __popc(__ldcg(&bm[i * 32 + b]));
+      }
+      run = k;
+    }
+    __threadfence_block();
+    __syncthreads();
+    // (4) dense exclusive scan of the occupied words' popcounts (in place, chunks of blockDim)
+    uint32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < nocc; c0 += blockDim.x) {
+      const uint32_t i = c0 + threadIdx.x;
+      const uint32_t v = i < nocc ? __ldcg(&dense[i]) : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<kBigThreads>(v, &tot, s_scan);
+      if (i < nocc) dense[i] = carry + ex;
+      carry += tot;
+    }
+    const uint32_t nact = carry;
     const uint32_t nblk = (nact + tk - 1) / tk;
     unsigned long long* gp = reinterpret_cast<unsigned long long*>(gpat + pat_base(e0, p, nbk, tk));
     for (int64_t i = threadIdx.x; i < (int64_t)nblk * nbk; i += blockDim.x) gp[i] = 0ull;
     __threadfence_block();
     __syncthreads();
+    // (5) ranks and patterns (fill_brick_nnz_pattern)
     for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
       const int32_t c = ci[e];
       if (c < 0 || c >= K) { q[e] = 0xFFFFFFFFu; continue; }
       const int r = row_of(s_rp, nrows, e);
-      const int64_t w = (c >> 5) - base;
-      const uint32_t qq = __ldcg(&pre[w]) + __popc(__ldcg(&bm[w]) & ((1u << (c & 31)) - 1u));
+      const uint32_t w = (uint32_t)c >> 5, w1 = w >> 5;
+      const uint32_t ord = __ldcg(&occ_pre[w1]) + __popc(__ldcg(&occ[w1]) & ((1u << (w & 31)) - 1u));
+      const uint32_t qq = __ldcg(&dense[ord]) + __popc(__ldcg(&bm[w]) & ((1u << (c & 31)) - 1u));
       q[e] = qq;
       const uint32_t j = qq / tk, lc = qq % tk;
       atomicOr(&gp[(int64_t)j * nbk + (lc >> 2) * nbrow + (r >> 4)], 1ull << (((r & 15) << 2) | (lc & 3)));
     }
     __threadfence_block();
     __syncthreads();
+    // (6) block sizes; clear the touched bitmap words and the occupancy words (invariant for the next panel)
     uint32_t bytes = 0;
     for (int64_t j = threadIdx.x; j < nblk; j += blockDim.x) {
       uint32_t nbr = 0, nz = 0;
@@ -1053,9 +1086,15 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
       }
       bytes += block_bytes(nbc, nbr, nz);
     }
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const int32_t c = ci[e];
+      if (c >= 0 && c < K) bm[(uint32_t)c >> 5] = 0u;
+    }
+    for (int64_t i = beg; i < end; ++i) occ[i] = 0u;
     uint32_t total;
-    block_excl_scan<kBigThreads>(bytes, &total, s_scan);
+    block_excl_scan<kBigThreads>(bytes, &total, s_scan);  // (barriers: the clears are done before the next panel)
     if (threadIdx.x == 0) { nact_out[p] = nact; nblk_out[p] = nblk; pbytes_out[p] = total; }
+    __threadfence_block();
   }
 }
 
@@ -1073,7 +1112,9 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int64_t* __restrict
                                                       const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac,
                                                       uint64_t* __restrict__ sp, uint8_t* __restrict__ packed,
                                                       const uint32_t* __restrict__ midlist,
-                                                      const uint32_t* __restrict__ nmid) {
+                                                      const uint32_t* __restrict__ nmid,
+                                                      uint32_t* __restrict__ hublist, uint32_t* __restrict__ hubch,
+                                                      unsigned long long* __restrict__ nhub) {
   __shared__ int64_t s_rp[129];
   __shared__ uint32_t s_scan[kEmitThreads / 32 + 1];
   __shared__ uint64_t s_vbase[kEmitThreads];     // byte offset of each block's values (single-chunk panels)
@@ -1136,6 +1177,15 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int64_t* __restrict
   __syncthreads();  // sizePtr entries / staged metadata of this panel are visible to the whole CTA
   const bool staged = nblk <= kEmitThreads && nbk <= 4;
   const int64_t e1 = s_rp[nrows];
+  if (e1 - e0 > kHubEmit) {  // a hub's values are spread over every CTA by k_emit_hubvals (critical path)
+    if (threadIdx.x == 0) {  // one 64-bit atomic: (hub count << 32 | chunk count), so chunk bases rise with t
+      const unsigned long long nch = (unsigned long long)((e1 - e0 + kHubChunk - 1) / kHubChunk);
+      const unsigned long long old = atomicAdd(nhub, (1ull << 32) + nch);
+      hublist[old >> 32] = (uint32_t)p;
+      hubch[old >> 32] = (uint32_t)old;
+    }
+    continue;
+  }
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     const uint32_t qq = q[e];
     const int32_t c = ci[e];
@@ -1164,6 +1214,64 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int64_t* __restrict
     reinterpret_cast<float*>(packed + vb)[off] = v;
   }
   }  // panel loop
+}
+
+// Values + activeCols of hub panels (more than kHubEmit entries; R-MAT has panels of 600K entries, which one CTA
+// took ~10 ms to scatter): every CTA takes a strided share of each hub's 4096-entry chunks. Block byte offsets,
+// headers and patterns were written by k_emit; ranks q and patterns come from the count kernels' scratch.
+__global__ void __launch_bounds__(kEmitThreads) k_emit_hubvals(const int64_t* __restrict__ rp,
+                                                              const int32_t* __restrict__ ci,
+                                                              const float* __restrict__ vals, int64_t M,
+                                                              int64_t nnz, int tm, int tk,
+                                                              const uint32_t* __restrict__ q,
+                                                              const uint32_t* __restrict__ nact_in,
+                                                              const uint32_t* __restrict__ brp,
+                                                              const uint64_t* __restrict__ gpat,
+                                                              uint32_t* __restrict__ ac, const uint64_t* __restrict__ sp,
+                                                              uint8_t* __restrict__ packed,
+                                                              const uint32_t* __restrict__ hublist,
+                                                              const uint32_t* __restrict__ hubch,
+                                                              const unsigned long long* __restrict__ nhub) {
+  __shared__ int64_t s_rp[129];
+  const unsigned long long hc = *nhub;
+  const uint32_t count = (uint32_t)(hc >> 32), total = (uint32_t)hc;
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {  // one flat list of every hub's chunks
+    uint32_t lo = 0, hi = count - 1;  // last t with hubch[t] <= g
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (hubch[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const int64_t p = hublist[lo];
+    const int64_t ch = g - hubch[lo];
+    load_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);  // (contains the barriers)
+    const int nrows = (int)min((int64_t)tm, M - p * tm);
+    const int64_t e0 = s_rp[0], e1 = s_rp[nrows];
+    const uint32_t b0 = brp[p], nact = nact_in[p];
+    const uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
+    {
+      const int64_t ce1 = min(e1, e0 + (ch + 1) * kHubChunk);
+      for (int64_t e = e0 + ch * kHubChunk + threadIdx.x; e < ce1; e += blockDim.x) {
+        const uint32_t qq = q[e];
+        if (qq >= nact) continue;  // only for invalid CSR input
+        const int r = row_of(s_rp, nrows, e);
+        const uint32_t j = qq / tk, lc = qq % tk;
+        ac[((int64_t)b0 + j) * tk + lc] = (uint32_t)ci[e];
+        const int bit = ((r & 15) << 2) | (lc & 3);
+        const int mine = (lc >> 2) * nbrow + (r >> 4);
+        const uint64_t* pt = gp + (int64_t)j * nbk;
+        uint32_t nbr = 0, off = 0;
+        for (int i = 0; i < nbk; ++i) {
+          const uint64_t w = pt[i];
+          nbr += w != 0ull;
+          if (i < mine) off += __popcll(w);
+        }
+        off += __popcll(pt[mine] & ((1ull << bit) - 1ull));
+        const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+        reinterpret_cast<float*>(packed + sp[b0 + j] + hdr + 8 * nbr)[off] = vals[e];
+      }
+    }
+  }
 }
 
 __global__ void k_finalize(const int64_t* __restrict__ rp, int64_t M, int64_t nnz, int64_t P,
@@ -1254,7 +1362,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   uint64_t* poff = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t), s);
   uint64_t* gpat = (uint64_t*)dalloc(pat_cap * sizeof(uint64_t), s);
   // panel lists: big (> kSmallCap entries, hub bitmap) | L1 (not on the warp path: CTA count + CTA emit)
-  uint32_t* biglist = (uint32_t*)dalloc(2 * (P + 1) * sizeof(uint32_t), s);
+  uint32_t* biglist = (uint32_t*)dalloc(3 * (P + 1) * sizeof(uint32_t), s);
   uint32_t* l1 = biglist + (P + 1);
   uint32_t* ctr = (uint32_t*)dalloc(8 * sizeof(uint32_t), s);  // nbig, nl1, ticket, -, status
   uint64_t* lb = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t), s);  // look-back states (blocks << 34 | bytes)
@@ -1262,7 +1370,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   uint64_t* info = (uint64_t*)dalloc(4 * sizeof(uint64_t), s);  // [3] = status word | hub count
   const int big_ctas = num_sms();
   const int64_t words = ceil_div(K, 32) + 2;
-  uint32_t* bigscr = (uint32_t*)dalloc((size_t)big_ctas * 2 * words * sizeof(uint32_t), s);
+  uint32_t* bigscr = (uint32_t*)dalloc((size_t)big_ctas * (2 * words + 2 * ((words + 31) / 32)) * sizeof(uint32_t), s);
   hrpb_status_t st = HRPB_SUCCESS;
   // the fused look-back packs (blocks, bytes) into 62 bits
   if (nb_cap >= (1ll << 28) || bytes_cap >= (1ll << 34)) {
@@ -1276,6 +1384,9 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     uint32_t* nbig = ctr;
     uint32_t* nl1 = ctr + 1;
     uint32_t* ticket = ctr + 2;
+    unsigned long long* nhub = reinterpret_cast<unsigned long long*>(ctr + 6);  // (hubs << 32 | chunks)
+    uint32_t* hublist = biglist;  // (the big list is consumed by k_count_big before k_emit reuses it)
+    uint32_t* hubch = biglist + 2 * (P + 1);
     uint32_t* status = ctr + 4;
     cudaMemsetAsync(ctr, 0, 8 * sizeof(uint32_t), s);
     const size_t count_smem =
@@ -1301,8 +1412,10 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
       launch_wbuild(tm, tk, s, row_ptr, col_idx, values, M, K, nnz, P, listed, nblk, pbytes, ticket, lb, h->brp,
                     poff, h->ac, h->sp, h->packed, status);
       k_emit<<<mid_ctas, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp, poff,
-                                               gpat, h->ac, h->sp, h->packed, l1, nl1);
-      note_launch(5);
+                                               gpat, h->ac, h->sp, h->packed, l1, nl1, hublist, hubch, nhub);
+      k_emit_hubvals<<<mid_ctas, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, nnz, tm, tk, q, nact, h->brp,
+                                                       gpat, h->ac, h->sp, h->packed, hublist, hubch, nhub);
+      note_launch(6);
     }
     k_finalize<<<1, 1, 0, s>>>(row_ptr, M, nnz, P, h->brp, poff, h->sp, status, info);
     note_launch();
