@@ -184,6 +184,9 @@ __device__ __forceinline__ void warp_panel_rows(const int64_t* __restrict__ rp, 
 // Panels that do not fit go to the CTA / hub paths (k_count, k_count_big, k_emit), listed by k_wclassify.
 constexpr int kWCap = 1024;       // entries per panel on the warp path (TM = 128: 512, see wcap)
 constexpr int kWBmWords = 256;    // bitmap words: column span <= 8192
+constexpr int kWNarrow = 768;     // spans below this mark columns in a byte map (plain stores, no atomics)
+constexpr int kWByteMap = 256;    // byte offset of the byte map (after the <= 24 bitmap words it turns into)
+static_assert(kWByteMap >= kWNarrow / 8 && kWByteMap + kWNarrow <= 4 * kWBmWords, "byte map inside the bitmap area");
 // brick slots held at once (patterns are built per chunk of blocks): 16 blocks' worth, at most 128 slots — the
 // per-warp shared memory bounds the resident warps of this latency-bound kernel (measured on c2a: 256 slots
 // 0.333 / 0.427 ms at TM = 64 / 16, 128 slots 0.322 / 0.401, 64 slots 0.407 (two chunks) / 0.377)
@@ -192,6 +195,7 @@ __host__ __device__ constexpr int wslots(int tm, int tk) {
                                                                 : 128;
 }
 constexpr int kWWarps = 4;        // warps per CTA
+constexpr int kB = 4;             // entries per lane per round in the warp-path entry loops
 
 struct WarpLayout {  // per-warp shared memory (bytes), depends on tm/tk only
   int slots;         // brick slots per block chunk = wslots (a chunk is wslots / nbk blocks)
@@ -209,8 +213,9 @@ __host__ __device__ inline WarpLayout warp_layout(int tm, int tk) {  // (also us
   L.off_row = L.off_pre + kWBmWords * 4;                    // u8 row of each entry
   L.off_q = L.off_row + cap;                                // u16 rank of each entry
   L.off_pat = (L.off_q + 2 * cap + 7) & ~7;
-  L.off_soff = L.off_pat + L.slots * 8;
-  L.off_vbase = (L.off_soff + L.slots * 2 + 7) & ~7;
+  const int sl = (L.slots / nbk) * (nbk + 1);                // slots with one pad slot per block (bank skew)
+  L.off_soff = L.off_pat + sl * 8;
+  L.off_vbase = (L.off_soff + sl * 2 + 7) & ~7;
   L.off_stage = (L.off_vbase + (L.slots / nbk) * 8 + 15) & ~15;  // staged col_idx, later the values
   L.bytes = L.off_stage + 4 * (cap + 8);
   return L;
@@ -222,6 +227,7 @@ struct WarpPanel {
   int32_t mn;
   uint32_t nact, nblk;
   bool sorted;      // rank by warp sort (column span wider than the bitmap, E <= kWSortCap)
+  int nbw;          // bitmap words in use: ceil(span / 32) <= kWNarrow / 32 (byte-map path) or kWBmWords
   uint32_t st[4];   // row starts of rows lane + 32k (entry index relative to e0), valid for 1 <= r < nrows
 };
 
@@ -310,7 +316,9 @@ __device__ __forceinline__ bool warp_panel_span(WarpPanel& w, GetCol col) {
   }
   w.mn = mn;
   w.sorted = false;
+  w.nbw = kWBmWords;
   if (w.E == 0) return true;
+  if ((int64_t)mx - (int64_t)mn < kWNarrow) w.nbw = (int)(((int64_t)mx - (int64_t)mn) / 32) + 1;
   if ((int64_t)mx - (int64_t)mn < 32 * kWBmWords) return true;
   w.sorted = true;
   return w.E <= kWSortCap;
@@ -389,7 +397,12 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ scol
   uint8_t* srow = my + L.off_row;
   uint16_t* sq = reinterpret_cast<uint16_t*>(my + L.off_q);
   const bool sorted = w.sorted;
-  if (!sorted) {
+  const int nbw = w.nbw;
+  const bool narrow = !sorted && nbw < kWBmWords;
+  uint8_t* bmap = my + kWByteMap;  // narrow spans: one byte per column of [mn, mn + 32 nbw)
+  if (narrow) {
+    for (int i = lane; i < 8 * nbw; i += 32) reinterpret_cast<uint32_t*>(bmap)[i] = 0u;
+  } else if (!sorted) {
 #pragma unroll
     for (int i = 0; i < kWBmWords / 32; ++i) bm[lane + 32 * i] = 0u;
   }
@@ -397,22 +410,42 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ scol
   const int E = w.E;
   const int32_t mn = w.mn;
   bool bad_range = false, bad_order = false;
-#pragma unroll 4
-  for (int i = lane; i < E; i += 32) {  // pass 1: validation + bitmap bits (or sort keys)
-    const int r = srow[i];
-    const int32_t c = scol[i];
-    // in-row order against the previous entry, read from shared memory (no shuffle chain)
-    if (i > 0 && srow[i - 1] == r && scol[i - 1] >= c) bad_order = true;
-    const uint32_t off = (uint32_t)(c - mn);
-    if (c < 0 || c >= K) bad_range = true;
-    if (sorted) {
-      keys[i] = ((uint64_t)(uint32_t)c << 32) | (uint32_t)i;
-    } else if (off >= 32u * kWBmWords) {
-      bad_order = true;  // only an unsorted row can leave [mn, mx]
-      sq[i] = 0xFFFFu;
-    } else {
-      atomicOr(&bm[off >> 5], 1u << (off & 31));
-      sq[i] = (uint16_t)off;  // column offset, turned into the rank below (no second global load)
+  // Loops over the entries run kB entries per lane per round with every shared load of the round issued before
+  // its stores (generic pointers: the compiler cannot move the next entry's loads above a store itself).
+  for (int c0 = 0; c0 < E; c0 += 32 * kB) {  // pass 1: validation + bitmap bits (or sort keys)
+    int rr[kB], rp1[kB];
+    int32_t cc[kB], cp1[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int i = c0 + 32 * u + lane;
+      const bool in = i < E;
+      rr[u] = in ? srow[i] : 0;
+      cc[u] = in ? scol[i] : 0;
+      rp1[u] = in && i > 0 ? srow[i - 1] : -1;
+      cp1[u] = in && i > 0 ? scol[i - 1] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int i = c0 + 32 * u + lane;
+      if (i >= E) continue;
+      const int r = rr[u];
+      const int32_t c = cc[u];
+      // in-row order against the previous entry, read from shared memory (no shuffle chain)
+      if (rp1[u] == r && cp1[u] >= c) bad_order = true;
+      const uint32_t off = (uint32_t)(c - mn);
+      if (c < 0 || c >= K) bad_range = true;
+      if (sorted) {
+        keys[i] = ((uint64_t)(uint32_t)c << 32) | (uint32_t)i;
+      } else if (off >= 32u * nbw) {
+        bad_order = true;  // only an unsorted row can leave [mn, mx]
+        sq[i] = 0xFFFFu;
+      } else {
+        // byte map: same-word stores from many lanes cost one wavefront; bitmap atomics on the few words of a
+        // banded panel serialised ~16-way (ncu: 8.7M of k_wbuild's 50M shared wavefronts)
+        if (narrow) bmap[off] = 1;
+        else atomicOr(&bm[off >> 5], 1u << (off & 31));
+        sq[i] = (uint16_t)off;  // column offset, turned into the rank below (no second global load)
+      }
     }
   }
   const bool any_range = __any_sync(0xffffffffu, bad_range), any_order = __any_sync(0xffffffffu, bad_order);
@@ -422,23 +455,45 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ scol
   }
   __syncwarp();
   uint32_t nact;
-  if (!sorted) {
-    constexpr int kW = kWBmWords / 32;
-    uint32_t cnt[kW], sum = 0;
+  if (narrow) {  // byte map -> bitmap words (lane l: columns [32 l, 32 l + 32)) + popcount prefix
+    uint32_t word = 0;
+    if (lane < nbw) {
+      const uint4* src = reinterpret_cast<const uint4*>(bmap + 32 * lane);
 #pragma unroll
-    for (int i = 0; i < kW; ++i) { cnt[i] = __popc(bm[lane * kW + i]); sum += cnt[i]; }
-    uint32_t run = warp_excl_scan(sum, &nact);
+      for (int h = 0; h < 2; ++h) {
+        const uint4 v = src[h];
+        const uint32_t x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int i = 0; i < kW; ++i) { pre[lane * kW + i] = run; run += cnt[i]; }
-    __syncwarp();
-    for (int c0 = 0; c0 < E; c0 += 32) {  // ranks: popcount prefix of the lower bits (R23: ascending columns)
-      const int i = c0 + lane;
-      if (i < E) {
-        const uint32_t off = sq[i];
-        uint32_t qq = 0xFFFFu;
-        if (off < 32u * kWBmWords) qq = pre[off >> 5] + __popc(bm[off >> 5] & ((1u << (off & 31)) - 1u));
-        sq[i] = (uint16_t)qq;
+        for (int k = 0; k < 4; ++k)  // bytes are 0 / 1: gather bits 0, 8, 16, 24 into a nibble
+          word |= ((x[k] | (x[k] >> 7) | (x[k] >> 14) | (x[k] >> 21)) & 0xFu) << (16 * h + 4 * k);
       }
+    }
+    const uint32_t run = warp_excl_scan((uint32_t)__popc(word), &nact);
+    if (lane < nbw) { bm[lane] = word; pre[lane] = run; }
+    __syncwarp();
+  }
+  if (!sorted) {
+    if (!narrow) {
+      constexpr int kW = kWBmWords / 32;
+      uint32_t cnt[kW], sum = 0;
+#pragma unroll
+      for (int i = 0; i < kW; ++i) { cnt[i] = __popc(bm[lane * kW + i]); sum += cnt[i]; }
+      uint32_t run = warp_excl_scan(sum, &nact);
+#pragma unroll
+      for (int i = 0; i < kW; ++i) { pre[lane * kW + i] = run; run += cnt[i]; }
+      __syncwarp();
+    }
+    for (int c0 = 0; c0 < E; c0 += 32 * kB) {  // ranks: popcount prefix of the lower bits (R23: ascending columns)
+      uint32_t off[kB], qq[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) off[u] = c0 + 32 * u + lane < E ? sq[c0 + 32 * u + lane] : 0xFFFFu;
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+        qq[u] = off[u] < 32u * nbw ? pre[off[u] >> 5] + __popc(bm[off[u] >> 5] & ((1u << (off[u] & 31)) - 1u))
+                                   : 0xFFFFu;
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+        if (c0 + 32 * u + lane < E) sq[c0 + 32 * u + lane] = (uint16_t)qq[u];
     }
   } else {
     // bitonic sort of (column, entry) keys, n = next power of two >= E (<= 256), then first-occurrence scan
@@ -474,7 +529,8 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ scol
 }
 
 // Brick patterns (P:L132 fill_brick_nnz_pattern; bit = (r % 16) * 4 + q % 4, R3) of blocks [jb0, jb0 + nb) of a
-// ranked warp-path panel into the warp's slot array (slot = (j - jb0) * nbk + brick column * nbrow + brick row).
+// ranked warp-path panel into the warp's slot array (slot = (j - jb0) * (nbk + 1) + brick column * nbrow + brick
+// row; one pad slot per block).
 template <int tm, int tk>
 __device__ __forceinline__ void warp_panel_patterns(const WarpPanel& w, uint8_t* my, const WarpLayout& L,
                                                     uint32_t jb0, uint32_t nb) {
@@ -484,18 +540,26 @@ __device__ __forceinline__ void warp_panel_patterns(const WarpPanel& w, uint8_t*
   uint32_t* pat32 = reinterpret_cast<uint32_t*>(my + L.off_pat);
   constexpr int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
   constexpr int tk_sh = tk == 16 ? 4 : 5;
-  for (int i = lane; i < 2 * (int)nb * nbk; i += 32) pat32[i] = 0u;
+  for (int i = lane; i < 2 * (int)nb * (nbk + 1); i += 32) pat32[i] = 0u;
   __syncwarp();
   const uint32_t q0 = jb0 * tk, q1 = min((jb0 + nb) * tk, w.nact);
-  for (int c0 = 0; c0 < w.E; c0 += 32) {
-    const int i = c0 + lane;
-    if (i < w.E) {
-      const uint32_t qq = sq[i];
+  for (int c0 = 0; c0 < w.E; c0 += 32 * kB) {
+    uint32_t qa[kB];
+    int ra[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int i = c0 + 32 * u + lane;
+      qa[u] = i < w.E ? sq[i] : 0xFFFFFFFFu;
+      ra[u] = i < w.E ? srow[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const uint32_t qq = qa[u];
       if (qq >= q0 && qq < q1) {
-        const int r = srow[i];
+        const int r = ra[u];
         const uint32_t j = (qq >> tk_sh) - jb0, lc = qq & (tk - 1);
         const int bit = ((r & 15) << 2) | (int)(lc & 3);
-        atomicOr(&pat32[2 * (j * nbk + (lc >> 2) * nbrow + (r >> 4)) + (bit >> 5)], 1u << (bit & 31));
+        atomicOr(&pat32[2 * (j * (nbk + 1) + (lc >> 2) * nbrow + (r >> 4)) + (bit >> 5)], 1u << (bit & 31));
       }
     }
   }
@@ -599,6 +663,8 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
   const WarpLayout L = warp_layout(tm, tk);
   uint8_t* my = dsm + (size_t)wid * L.bytes;
   constexpr int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  constexpr int kbs = nbk + 1;  // slot stride of a block: the +1 skews blocks across banks (the per-lane block
+                                // loops and the pattern atomics hit one bank 16-way with a stride of nbk)
   const uint8_t* srow = my + L.off_row;
   const uint16_t* sq = reinterpret_cast<const uint16_t*>(my + L.off_q);
   const unsigned long long* pat = reinterpret_cast<const unsigned long long*>(my + L.off_pat);
@@ -645,7 +711,7 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
           for (uint32_t j = lane; j < nb; j += 32) {
             uint32_t nbr = 0, nz = 0;
 #pragma unroll
-            for (int i = 0; i < nbk; ++i) { const uint64_t v = pat[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
+            for (int i = 0; i < nbk; ++i) { const uint64_t v = pat[j * kbs + i]; nbr += v != 0ull; nz += __popcll(v); }
             bytes += block_bytes(nbc, nbr, nz);
           }
         }
@@ -676,9 +742,8 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
       // a non-zero bitmap word at a time, its 32 bits across the lanes: lane l writes bit l's column at its rank
       const uint32_t* bm = reinterpret_cast<const uint32_t*>(my);
       const uint32_t* pre = reinterpret_cast<const uint32_t*>(my + L.off_pre);
-#pragma unroll
-      for (int k = 0; k < kWBmWords / 32; ++k) {
-        const uint32_t mine = bm[32 * k + lane];
+      for (int k = 0; k < (w.nbw + 31) / 32; ++k) {
+        const uint32_t mine = 32 * k + lane < w.nbw ? bm[32 * k + lane] : 0u;
         uint32_t nzw = __ballot_sync(0xffffffffu, mine != 0u);
         while (nzw) {
           const int kk = __ffs(nzw) - 1;
@@ -702,8 +767,8 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
         if (j < nbch) {
 #pragma unroll
           for (int i = 0; i < nbk; ++i) {
-            const uint64_t v = pat[j * nbk + i];
-            soff[j * nbk + i] = (uint16_t)nz;  // values of the earlier bricks of the block (CSC slot order)
+            const uint64_t v = pat[j * kbs + i];
+            soff[j * kbs + i] = (uint16_t)nz;  // values of the earlier bricks of the block (CSC slot order)
             nbr += v != 0ull;
             nz += __popcll(v);
           }
@@ -722,20 +787,20 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
 #pragma unroll
           for (int bc = 0; bc < nbc; ++bc) {
 #pragma unroll
-            for (int br = 0; br < nbrow; ++br) k += pat[j * nbk + bc * nbrow + br] != 0ull;
+            for (int br = 0; br < nbrow; ++br) k += pat[j * kbs + bc * nbrow + br] != 0ull;
             acc |= (uint64_t)k << (8 * (nb & 7));
             if ((++nb & 7) == 0) { blk[wi++] = acc; acc = 0; }
           }
           for (int bc = 0; bc < nbc; ++bc)
             for (int br = 0; br < nbrow; ++br) {
-              const uint64_t v = pat[j * nbk + bc * nbrow + br];
+              const uint64_t v = pat[j * kbs + bc * nbrow + br];
               if (!v) continue;
               acc |= (uint64_t)br << (8 * (nb & 7));
               if ((++nb & 7) == 0) { blk[wi++] = acc; acc = 0; }
             }
           if (nb & 7) blk[wi++] = acc;
           for (int i = 0; i < nbk; ++i) {
-            const uint64_t v = pat[j * nbk + i];
+            const uint64_t v = pat[j * kbs + i];
             if (v) blk[wi++] = v;
           }
           uint32_t* tail = reinterpret_cast<uint32_t*>(packed + off + hdr + 8 * nbr + 4 * nz);
@@ -746,20 +811,33 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
       }
       __syncwarp();
       const uint32_t q0 = jb0 * tk, q1 = min((jb0 + nbch) * tk, w.nact);
-      for (int c0 = 0; c0 < E; c0 += 32) {  // values and activeCols of this chunk's blocks
-        const int i = c0 + lane;
-        if (i < E) {
-          const uint32_t qq = sq[i];
+      for (int c0 = 0; c0 < E; c0 += 32 * kB) {  // values of this chunk's blocks (loads of the round first)
+        uint32_t qa[kB], oa[kB];
+        int ra[kB];
+        float va[kB];
+        uint64_t ba[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int i = c0 + 32 * u + lane;
+          qa[u] = i < E ? sq[i] : 0xFFFFFFFFu;
+          ra[u] = i < E ? srow[i] : 0;
+          va[u] = i < E ? sval[i] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const uint32_t qq = qa[u];
           if (qq >= q0 && qq < q1) {
-            const int r = srow[i];
-            const float v = sval[i];
+            const int r = ra[u];
             const uint32_t j = (qq >> tk_sh) - jb0, lc = qq & (tk - 1);
             const int bit = ((r & 15) << 2) | (int)(lc & 3);
-            const uint32_t slot = j * nbk + (lc >> 2) * nbrow + (r >> 4);
-            const uint32_t o = soff[slot] + __popcll(pat[slot] & ((1ull << bit) - 1ull));
-            reinterpret_cast<float*>(packed + vbase[j])[o] = v;
+            const uint32_t slot = j * kbs + (lc >> 2) * nbrow + (r >> 4);
+            oa[u] = soff[slot] + __popcll(pat[slot] & ((1ull << bit) - 1ull));
+            ba[u] = vbase[j];
           }
         }
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (qa[u] >= q0 && qa[u] < q1) reinterpret_cast<float*>(packed + ba[u])[oa[u]] = va[u];
       }
       __syncwarp();
     }
