@@ -196,6 +196,9 @@ __host__ __device__ constexpr int wslots(int tm, int tk) {
 }
 constexpr int kWWarps = 4;        // warps per CTA
 constexpr int kB = 4;             // entries per lane per round in the warp-path entry loops
+#ifndef HRPB_WB_MINB
+#define HRPB_WB_MINB 5            // k_wbuild CTAs per SM the register allocation must allow (shared memory: 5)
+#endif
 
 struct WarpLayout {  // per-warp shared memory (bytes), depends on tm/tk only
   int slots;         // brick slots per block chunk = wslots (a chunk is wslots / nbk blocks)
@@ -588,6 +591,9 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wclassify(const int64_t* __res
 // Decoupled look-back over panels (single-pass exclusive scan, warp granularity): st[p] holds the panel's
 // aggregate (flag A) as soon as it is known, later its inclusive prefix (flag P). Panels are claimed in order
 // through a ticket, so every predecessor belongs to a warp that is running or done.
+#ifndef HRPB_LB_SLEEP
+#define HRPB_LB_SLEEP 64
+#endif
 #define kLbA (1ull << 62)
 #define kLbP (2ull << 62)
 #define kLbMask ((1ull << 62) - 1)
@@ -601,14 +607,17 @@ __device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
 }
 // One look-back over a state word carrying (blocks << 34 | bytes) (host checks both fit: blocks < 2^28,
 // bytes < 2^34). Returns the exclusive prefix of the packed pair (the fields never carry into each other).
-__device__ __forceinline__ uint64_t warp_lookback(uint64_t* st, int64_t p, uint64_t agg) {
+// Publishes the panel's aggregate (flag A; panel 0: its inclusive prefix, flag P). Work placed between this and
+// warp_lb_wait gives the successors slack: they stall only until the aggregate is out, not until our wait ends.
+__device__ __forceinline__ void warp_lb_publish(uint64_t* st, int64_t p, uint64_t agg) {
+  if ((threadIdx.x & 31) == 0) st_relaxed_gpu(st + p, (p == 0 ? kLbP : kLbA) | agg);
+}
+__device__ __forceinline__ uint64_t warp_lb_wait(uint64_t* st, int64_t p, uint64_t agg) {
   const int lane = threadIdx.x & 31;
   if (p == 0) {
-    if (lane == 0) st_relaxed_gpu(st, kLbP | agg);
     __syncwarp();
     return 0;
   }
-  if (lane == 0) st_relaxed_gpu(st + p, kLbA | agg);
   uint64_t excl = 0;
   int64_t j = p - 1;
   while (true) {
@@ -620,6 +629,7 @@ __device__ __forceinline__ uint64_t warp_lookback(uint64_t* st, int64_t p, uint6
       const uint32_t zm = __ballot_sync(0xffffffffu, (v >> 62) == 0);
       const uint32_t need = pm ? ((pm & (0u - pm)) - 1u) : 0xFFFFFFFFu;  // lanes before the first P
       if (!(zm & need)) break;
+      __nanosleep(HRPB_LB_SLEEP);  // back off: a spinning warp takes issue slots from the warps it waits for
       if ((v >> 62) == 0) v = ld_relaxed_gpu(st + idx);
     }
     const int last = pm ? __ffs(pm) - 1 : 31;  // lanes 0..last contribute (lane `last` has the prefix)
@@ -635,6 +645,40 @@ __device__ __forceinline__ uint64_t warp_lookback(uint64_t* st, int64_t p, uint6
   return excl;
 }
 
+// One block's HRPB-v1 metadata at blk (16-B aligned): header bytes colPtr[0..nbc] (stored bricks before each
+// brick column), rows[nbr] (brick row of each stored brick), zero pad to 8 B -- assembled 8 bytes at a time --
+// then the non-zero brick patterns in CSC slot order, and the zero tail padding after the nz values (R7).
+template <int nbc, int nbrow>
+__device__ __forceinline__ void emit_block_meta(uint8_t* blkp, const unsigned long long* pj, uint32_t nbr,
+                                                uint32_t nz, uint32_t size) {
+  constexpr int nbk = nbc * nbrow;
+  uint64_t* blk = reinterpret_cast<uint64_t*>(blkp);
+  const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+  uint64_t acc = 0;
+  uint32_t nb = 1, k = 0, wi = 0;  // byte 0 = colPtr[0] = 0
+#pragma unroll
+  for (int bc = 0; bc < nbc; ++bc) {
+#pragma unroll
+    for (int br = 0; br < nbrow; ++br) k += pj[bc * nbrow + br] != 0ull;
+    acc |= (uint64_t)k << (8 * (nb & 7));
+    if ((++nb & 7) == 0) { blk[wi++] = acc; acc = 0; }
+  }
+  for (int bc = 0; bc < nbc; ++bc)
+    for (int br = 0; br < nbrow; ++br) {
+      const uint64_t v = pj[bc * nbrow + br];
+      if (!v) continue;
+      acc |= (uint64_t)br << (8 * (nb & 7));
+      if ((++nb & 7) == 0) { blk[wi++] = acc; acc = 0; }
+    }
+  if (nb & 7) blk[wi++] = acc;
+  for (int i = 0; i < nbk; ++i) {
+    const uint64_t v = pj[i];
+    if (v) blk[wi++] = v;
+  }
+  uint32_t* tail = reinterpret_cast<uint32_t*>(blkp + hdr + 8 * nbr + 4 * nz);
+  for (uint32_t t = hdr + 8 * nbr + 4 * nz; t < size; t += 4) *tail++ = 0u;
+}
+
 #ifdef HRPB_BTRACE
 __device__ unsigned long long g_btrace[8];  // per-phase cycles summed over warps (diagnostic builds only)
 #define BT_MARK(k) do { const long long t_ = clock64(); bt[k] += t_ - bt_last; bt_last = t_; } while (0)
@@ -648,7 +692,7 @@ __device__ unsigned long long g_btrace[8];  // per-phase cycles summed over warp
 // ranks, activeCols with sentinel K (R2, R6). Listed panels only take part in the scan
 // with the (nblk, bytes) their CTA / hub count produced; k_emit writes them afterwards.
 template <int tm, int tk>
-__global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+__global__ void __launch_bounds__(32 * kWWarps, HRPB_WB_MINB) k_wbuild(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                                         const float* __restrict__ vals, int64_t M, int64_t K,
                                                         int64_t nnz, int64_t P, const uint8_t* __restrict__ listed,
                                                         const uint32_t* __restrict__ nblk_listed,
@@ -688,6 +732,12 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
     uint32_t bytes = 0;
     int vsh = 0;
     constexpr uint32_t kChunkBlk = wslots(tm, tk) / nbk;  // blocks whose patterns fit the slot array
+    static_assert(kChunkBlk <= 16, "prepared emission: lane j holds block j, codes carry j in 4 bits");
+    // Prepared emission (bitmap-ranked panels whose blocks fit one pattern chunk, the common case): block sizes,
+    // in-panel offsets, brick value offsets and every entry's destination are computed between publishing the
+    // aggregate and waiting for the predecessors; after the look-back only the stores remain.
+    bool prep = false;
+    uint32_t pnbr = 0, pnz = 0, psize = 0, proff = 0;  // lane j: block j (prepared emission)
     const bool is_listed = listed[p] != 0;
     if (is_listed) {
       w.nblk = nblk_listed[p];
@@ -705,9 +755,11 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
         BT_MARK(3);
         __syncwarp();  // the staged columns are dead: the values go into the same window, landing meanwhile
         vsh = warp_stage(vals, nnz, w.e0, w.E, my + L.off_stage, al16);
+        prep = !w.sorted && w.nblk <= kChunkBlk;
         for (uint32_t jb0 = 0; jb0 < w.nblk; jb0 += kChunkBlk) {
           const uint32_t nb = min(kChunkBlk, w.nblk - jb0);
           warp_panel_patterns<tm, tk>(w, my, L, jb0, nb);
+          if (prep) break;
           for (uint32_t j = lane; j < nb; j += 32) {
             uint32_t nbr = 0, nz = 0;
 #pragma unroll
@@ -715,12 +767,57 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
             bytes += block_bytes(nbc, nbr, nz);
           }
         }
+        if (prep) {
+          if ((uint32_t)lane < w.nblk) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+            for (int i = 0; i < nbk; ++i) {
+              const uint64_t v = pat[lane * kbs + i];
+              soff[lane * kbs + i] = (uint16_t)pnz;  // values of the earlier bricks of the block (CSC slot order)
+              pnbr += v != 0ull;
+              pnz += __popcll(v);
+            }
+            psize = block_bytes(nbc, pnbr, pnz);
+          }
+          proff = warp_excl_scan(psize, &bytes);
+          if ((uint32_t)lane < w.nblk) vbase[lane] = proff + ((nbc + 1 + pnbr + 7) & ~7u) + 8 * pnbr;  // relative
+        } else {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+        }
       }
     }
     BT_MARK(4);
-    const uint64_t ex = warp_lookback(lb, p, ((uint64_t)w.nblk << 34) | bytes);
+    const uint64_t agg = ((uint64_t)w.nblk << 34) | bytes;
+    warp_lb_publish(lb, p, agg);
+    if (prep) {  // entry destinations: sq[i] <- (block << 11) | value index in the block (0xFFFF stays invalid)
+      __syncwarp();
+      uint16_t* sqw = reinterpret_cast<uint16_t*>(my + L.off_q);
+      for (int c0 = 0; c0 < w.E; c0 += 32 * kB) {
+        uint32_t qa[kB], code[kB];
+        int ra[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int i = c0 + 32 * u + lane;
+          qa[u] = i < w.E ? sq[i] : 0xFFFFu;
+          ra[u] = i < w.E ? srow[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          code[u] = 0xFFFFu;
+          if (qa[u] < w.nact) {
+            const int r = ra[u];
+            const uint32_t j = qa[u] >> tk_sh, lc = qa[u] & (tk - 1);
+            const int bit = ((r & 15) << 2) | (int)(lc & 3);
+            const uint32_t slot = j * kbs + (lc >> 2) * nbrow + (r >> 4);
+            code[u] = (j << 11) | (soff[slot] + __popcll(pat[slot] & ((1ull << bit) - 1ull)));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (c0 + 32 * u + lane < w.E) sqw[c0 + 32 * u + lane] = (uint16_t)code[u];
+      }
+    }
+    const uint64_t ex = warp_lb_wait(lb, p, agg);
     BT_MARK(5);
     const uint32_t b0 = (uint32_t)(ex >> 34);
     const uint64_t pbase = ex & ((1ull << 34) - 1);
@@ -757,6 +854,31 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
       const uint64_t* keys = reinterpret_cast<const uint64_t*>(my);
       for (int i = lane; i < w.E; i += 32) acp[sq[(uint32_t)keys[i]]] = (uint32_t)(keys[i] >> 32);
     }
+    if (prep) {
+      if ((uint32_t)lane < nblk) {
+        const uint64_t off = pbase + proff;
+        sp[b0 + lane] = off;
+        emit_block_meta<nbc, nbrow>(packed + off, pat + lane * kbs, pnbr, pnz, psize);
+      }
+      for (int c0 = 0; c0 < E; c0 += 32 * kB) {  // values at the prepared destinations (loads of the round first)
+        uint32_t ca[kB];
+        float va[kB];
+        uint64_t ba[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int i = c0 + 32 * u + lane;
+          ca[u] = i < E ? sq[i] : 0xFFFFu;
+          va[u] = i < E ? sval[i] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) ba[u] = ca[u] != 0xFFFFu ? vbase[ca[u] >> 11] : 0ull;
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (ca[u] != 0xFFFFu) reinterpret_cast<float*>(packed + pbase + ba[u])[ca[u] & 0x7FFu] = va[u];
+      }
+      BT_MARK(6);
+      continue;
+    }
     for (uint32_t jb0 = 0; jb0 < nblk; jb0 += kChunkBlk) {
       const uint32_t nbch = min(kChunkBlk, nblk - jb0);
       if (jb0 > 0) warp_panel_patterns<tm, tk>(w, my, L, jb0, nbch);  // (chunk 0 is still in place if alone)
@@ -778,34 +900,8 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wbuild(const int64_t* __restri
         const uint64_t off = carry + warp_excl_scan(size, &tot);
         if (j < nbch) {
           sp[b0 + jb0 + j] = off;
-          uint64_t* blk = reinterpret_cast<uint64_t*>(packed + off);  // 16-B aligned
-          const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
-          // header bytes: colPtr[0..nbc] (stored bricks before each brick column), rows[nbr] (brick row of each
-          // stored brick), zero pad to 8 B; assembled 8 bytes at a time
-          uint64_t acc = 0;
-          uint32_t nb = 1, k = 0, wi = 0;  // byte 0 = colPtr[0] = 0
-#pragma unroll
-          for (int bc = 0; bc < nbc; ++bc) {
-#pragma unroll
-            for (int br = 0; br < nbrow; ++br) k += pat[j * kbs + bc * nbrow + br] != 0ull;
-            acc |= (uint64_t)k << (8 * (nb & 7));
-            if ((++nb & 7) == 0) { blk[wi++] = acc; acc = 0; }
-          }
-          for (int bc = 0; bc < nbc; ++bc)
-            for (int br = 0; br < nbrow; ++br) {
-              const uint64_t v = pat[j * kbs + bc * nbrow + br];
-              if (!v) continue;
-              acc |= (uint64_t)br << (8 * (nb & 7));
-              if ((++nb & 7) == 0) { blk[wi++] = acc; acc = 0; }
-            }
-          if (nb & 7) blk[wi++] = acc;
-          for (int i = 0; i < nbk; ++i) {
-            const uint64_t v = pat[j * kbs + i];
-            if (v) blk[wi++] = v;
-          }
-          uint32_t* tail = reinterpret_cast<uint32_t*>(packed + off + hdr + 8 * nbr + 4 * nz);
-          for (uint32_t t = hdr + 8 * nbr + 4 * nz; t < size; t += 4) *tail++ = 0u;
-          vbase[j] = off + hdr + 8 * nbr;
+          emit_block_meta<nbc, nbrow>(packed + off, pat + j * kbs, nbr, nz, size);
+          vbase[j] = off + ((nbc + 1 + nbr + 7) & ~7u) + 8 * nbr;
         }
         carry += tot;
       }

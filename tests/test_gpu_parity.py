@@ -85,6 +85,32 @@ def test_builder_other_tiles(tm, tk, name):
     assert_same_hrpb(A, oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm, tk=tk), f"{tm}x{tk}")
 
 
+@pytest.mark.parametrize("tm", [16, 64])
+def test_builder_span_boundaries(tm):
+    # warp-path ranking variants by panel column span: byte map (span < 768), bitmap atomics (< 8192), warp sort
+    # (wider, <= 256 entries) and the listed CTA path; spans straddle each boundary, panels start at random offsets
+    rng = np.random.default_rng(tm)
+    spans = [1, 31, 32, 33, 700, 767, 768, 769, 800, 4000, 8191, 8192, 8193, 50000]
+    K = 60000
+    rows, cols = [], []
+    for span in spans:
+        for _ in range(3):
+            base = int(rng.integers(0, K - span + 1))
+            for r in range(tm):
+                k = int(rng.integers(1, min(span, 12) + 1))
+                c = np.sort(rng.choice(span, k, replace=False)) + base
+                if r == 0:
+                    c = np.unique(np.concatenate([c, [base, base + span - 1]]))
+                cols.append(c.astype(np.int32))
+    M = len(cols)
+    rp = np.zeros(M + 1, np.int64)
+    rp[1:] = np.cumsum([len(c) for c in cols])
+    ci = np.concatenate(cols)
+    v = rng.standard_normal(ci.size).astype(np.float32)
+    A = gpu_build(M, K, rp, ci, v, tm=tm)
+    assert_same_hrpb(A, oracle.csr_to_hrpb(M, K, rp, ci, v, tm=tm), f"spans tm={tm}")
+
+
 def test_builder_rejects_invalid_csr():
     M, K = 40, 50
     rp, ci, v = rand_csr(M, K, 0.2, 1)
