@@ -230,6 +230,7 @@ struct WarpPanel {
   int32_t mn;
   uint32_t nact, nblk;
   bool sorted;      // rank by warp sort (column span wider than the bitmap, E <= kWSortCap)
+  bool patterns_done;  // the rank pass also set the brick patterns (all blocks in one slot chunk)
   int nbw;          // bitmap words in use: ceil(span / 32) <= kWNarrow / 32 (byte-map path) or kWBmWords
   uint32_t st[4];   // row starts of rows lane + 32k (entry index relative to e0), valid for 1 <= r < nrows
 };
@@ -402,6 +403,7 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ scol
   const bool sorted = w.sorted;
   const int nbw = w.nbw;
   const bool narrow = !sorted && nbw < kWBmWords;
+  w.patterns_done = false;
   uint8_t* bmap = my + kWByteMap;  // narrow spans: one byte per column of [mn, mn + 32 nbw)
   if (narrow) {
     for (int i = lane; i < 8 * nbw; i += 32) reinterpret_cast<uint32_t*>(bmap)[i] = 0u;
@@ -486,18 +488,38 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ scol
       for (int i = 0; i < kW; ++i) { pre[lane * kW + i] = run; run += cnt[i]; }
       __syncwarp();
     }
+    // all blocks' patterns fit the slot array (one chunk): set the brick pattern bits in the rank loop itself
+    constexpr int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+    constexpr int tk_sh = tk == 16 ? 4 : 5;
+    const bool fuse = (nact + tk - 1) / tk <= (uint32_t)(wslots(tm, tk) / nbk);
+    uint32_t* pat32 = reinterpret_cast<uint32_t*>(my + L.off_pat);
+    if (fuse) {
+      for (int i = lane; i < 2 * (int)((nact + tk - 1) / tk) * (nbk + 1); i += 32) pat32[i] = 0u;
+      __syncwarp();
+    }
     for (int c0 = 0; c0 < E; c0 += 32 * kB) {  // ranks: popcount prefix of the lower bits (R23: ascending columns)
       uint32_t off[kB], qq[kB];
+      int ra[kB];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) off[u] = c0 + 32 * u + lane < E ? sq[c0 + 32 * u + lane] : 0xFFFFu;
+      for (int u = 0; u < kB; ++u) {
+        off[u] = c0 + 32 * u + lane < E ? sq[c0 + 32 * u + lane] : 0xFFFFu;
+        ra[u] = fuse && c0 + 32 * u + lane < E ? srow[c0 + 32 * u + lane] : 0;
+      }
 #pragma unroll
       for (int u = 0; u < kB; ++u)
         qq[u] = off[u] < 32u * nbw ? pre[off[u] >> 5] + __popc(bm[off[u] >> 5] & ((1u << (off[u] & 31)) - 1u))
                                    : 0xFFFFu;
 #pragma unroll
-      for (int u = 0; u < kB; ++u)
+      for (int u = 0; u < kB; ++u) {
         if (c0 + 32 * u + lane < E) sq[c0 + 32 * u + lane] = (uint16_t)qq[u];
+        if (fuse && qq[u] < nact) {  // (same bit formula as warp_panel_patterns)
+          const uint32_t j = qq[u] >> tk_sh, lc = qq[u] & (tk - 1);
+          const int r = ra[u], bit = ((r & 15) << 2) | (int)(lc & 3);
+          atomicOr(&pat32[2 * (j * (nbk + 1) + (lc >> 2) * nbrow + (r >> 4)) + (bit >> 5)], 1u << (bit & 31));
+        }
+      }
     }
+    w.patterns_done = fuse;
   } else {
     // bitonic sort of (column, entry) keys, n = next power of two >= E (<= 256), then first-occurrence scan
     int n = 32;
@@ -758,7 +780,8 @@ __global__ void __launch_bounds__(32 * kWWarps, HRPB_WB_MINB) k_wbuild(const int
         prep = !w.sorted && w.nblk <= kChunkBlk;
         for (uint32_t jb0 = 0; jb0 < w.nblk; jb0 += kChunkBlk) {
           const uint32_t nb = min(kChunkBlk, w.nblk - jb0);
-          warp_panel_patterns<tm, tk>(w, my, L, jb0, nb);
+          if (!w.patterns_done) warp_panel_patterns<tm, tk>(w, my, L, jb0, nb);
+          else __syncwarp();
           if (prep) break;
           for (uint32_t j = lane; j < nb; j += 32) {
             uint32_t nbr = 0, nz = 0;
