@@ -35,6 +35,9 @@ constexpr int kSmallThreads = 128;
 constexpr int kSmallCap = 2048;      // entries per panel handled in shared memory
 constexpr int kSpanWords = 512;      // bitmap ranking when the panel's column span <= 16384
 constexpr int kBigThreads = 512;
+#ifndef HRPB_BIG_CTAS_PER_SM
+#define HRPB_BIG_CTAS_PER_SM 2  // hub CTAs per SM (each with its own column bitmap scratch, ~1 MB at K = 4M)
+#endif
 constexpr int64_t kHubEmit = 16384;
 constexpr int64_t kHubChunk = 4096;  // listed panels with more entries get their values scattered by all CTAs
 constexpr int kEmitThreads = 128;
@@ -1217,8 +1220,8 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
       const int r = row_of(s_rp, nrows, e);
       if (e > s_rp[r] && ci[e - 1] >= c) atomicOr(status, ST_COL_ORDER);
       const uint32_t w = (uint32_t)c >> 5;
-      const uint32_t old = atomicOr(&bm[w], 1u << (c & 31));
-      if (old == 0u) atomicOr(&occ[w >> 5], 1u << (w & 31));
+      atomicOr(&bm[w], 1u << (c & 31));        // (results unused: fire-and-forget reductions, no round trip)
+      atomicOr(&occ[w >> 5], 1u << (w & 31));
     }
     __threadfence_block();
     __syncthreads();
@@ -1231,12 +1234,25 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
     uint32_t run = block_excl_scan<kBigThreads>(sum, &nocc, s_scan);
     for (int64_t i = beg; i < end; ++i) {
       occ_pre[i] = run;
-      // (3) popcount of every occupied word at its ordinal
+      // (3) popcount of every occupied word at its ordinal, 8 loads in flight before their stores
       uint32_t o = __ldcg(&occ[i]), k = run;
       while (o) {
-        const int b = __ffs(o) - 1;
-        o &= o - 1;
-        dense[k++] = __popc(__ldcg(&bm[i * 32 + b]));
+        uint32_t v[8];
+        int n = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          v[u] = 0u;
+          if (o) {
+            const int b = __ffs(o) - 1;
+            o &= o - 1;
+            v[u] = __ldcg(&bm[i * 32 + b]);
+            n = u + 1;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (u < n) dense[k + u] = __popc(v[u]);
+        k += n;
       }
       run = k;
     }
@@ -1259,16 +1275,39 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
     __threadfence_block();
     __syncthreads();
     // (5) ranks and patterns (fill_brick_nnz_pattern)
-    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      const int32_t c = ci[e];
-      if (c < 0 || c >= K) { q[e] = 0xFFFFFFFFu; continue; }
-      const int r = row_of(s_rp, nrows, e);
-      const uint32_t w = (uint32_t)c >> 5, w1 = w >> 5;
-      const uint32_t ord = __ldcg(&occ_pre[w1]) + __popc(__ldcg(&occ[w1]) & ((1u << (w & 31)) - 1u));
-      const uint32_t qq = __ldcg(&dense[ord]) + __popc(__ldcg(&bm[w]) & ((1u << (c & 31)) - 1u));
-      q[e] = qq;
-      const uint32_t j = qq / tk, lc = qq % tk;
-      atomicOr(&gp[(int64_t)j * nbk + (lc >> 2) * nbrow + (r >> 4)], 1ull << (((r & 15) << 2) | (lc & 3)));
+    constexpr int kU = 4;  // entries per thread per round, every load of the round before its stores
+    for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)kU * blockDim.x) {
+      int32_t c[kU];
+      uint32_t ord[kU], qq[kU], wb[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t e = eb + (int64_t)u * blockDim.x;
+        c[u] = e < e1 ? ci[e] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        ord[u] = 0u;
+        wb[u] = 0u;
+        if (c[u] >= 0 && c[u] < K) {
+          const uint32_t w = (uint32_t)c[u] >> 5, w1 = w >> 5;
+          ord[u] = __ldcg(&occ_pre[w1]) + __popc(__ldcg(&occ[w1]) & ((1u << (w & 31)) - 1u));
+          wb[u] = __ldcg(&bm[w]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        qq[u] = (c[u] >= 0 && c[u] < K) ? __ldcg(&dense[ord[u]]) + __popc(wb[u] & ((1u << (c[u] & 31)) - 1u))
+                                         : 0xFFFFFFFFu;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t e = eb + (int64_t)u * blockDim.x;
+        if (e >= e1) continue;
+        q[e] = qq[u];
+        if (qq[u] == 0xFFFFFFFFu) continue;
+        const int r = row_of(s_rp, nrows, e);
+        const uint32_t j = qq[u] / tk, lc = qq[u] % tk;
+        atomicOr(&gp[(int64_t)j * nbk + (lc >> 2) * nbrow + (r >> 4)], 1ull << (((r & 15) << 2) | (lc & 3)));
+      }
     }
     __threadfence_block();
     __syncthreads();
@@ -1565,7 +1604,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   uint64_t* lb = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t), s);  // look-back states (blocks << 34 | bytes)
   uint8_t* listed = (uint8_t*)dalloc(P + 1, s);
   uint64_t* info = (uint64_t*)dalloc(4 * sizeof(uint64_t), s);  // [3] = status word | hub count
-  const int big_ctas = num_sms();
+  const int big_ctas = HRPB_BIG_CTAS_PER_SM * num_sms();
   const int64_t words = ceil_div(K, 32) + 2;
   uint32_t* bigscr = (uint32_t*)dalloc((size_t)big_ctas * (2 * words + 2 * ((words + 31) / 32)) * sizeof(uint32_t), s);
   hrpb_status_t st = HRPB_SUCCESS;
