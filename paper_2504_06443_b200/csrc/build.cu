@@ -1076,7 +1076,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
       return -1;
     };
     // (a negative column — invalid CSR, flagged above — is ranked as column 0 to keep every index in bounds)
-    for (int i = threadIdx.x; i < E; i += blockDim.x) slot_of(max((int32_t)s_col[i], 0) >> 10, true);
+    for (int i = threadIdx.x; i < E; i += blockDim.x) {  // (stops once the windows overflow: scattered columns)
+      if (*reinterpret_cast<volatile int*>(&s_nwin) > kMaxWin) break;
+      slot_of(max((int32_t)s_col[i], 0) >> 10, true);
+    }
     __syncthreads();
     const int nwin = s_nwin;
     bool windowed = nwin <= kMaxWin;
@@ -1116,34 +1119,60 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
       __syncthreads();
     }
     if (!windowed) {
-    // sort ranking: bitonic sort of (col << 32 | local index), unique flags, scan
-    int n = 32;
-    while (n < E) n <<= 1;
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-      s_keys[i] = i < E ? ((uint64_t)s_col[i] << 32) | (uint32_t)i : ~0ull;
-    __syncthreads();
-    for (int k = 2; k <= n; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const uint64_t a = s_keys[i], b = s_keys[ixj];
-            if ((a > b) == ((i & k) == 0)) { s_keys[i] = b; s_keys[ixj] = a; }
+      // merge ranking. The panel's rows are sorted runs of (column, entry) keys (unique: the entry breaks ties);
+      // ceil(log2(rows)) levels of pairwise run merges place each key by one binary search in its partner run,
+      // then first occurrences of each column are counted (R23: ascending distinct columns). An unsorted row
+      // (invalid CSR, flagged above) only has to keep every index in bounds.
+      uint64_t* src = s_keys;
+      uint64_t* dst = reinterpret_cast<uint64_t*>(s_col);  // s_col + s_q: 2 kSmallCap words
+      int levels = 0;
+      while ((1 << levels) < nrows) ++levels;
+      if (levels & 1) { uint64_t* t2 = src; src = dst; dst = t2; }  // the last level lands in s_keys
+      uint32_t cv[kSmallCap / kSmallThreads];
+#pragma unroll
+      for (int k = 0; k < kSmallCap / kSmallThreads; ++k) {
+        const int i = threadIdx.x + k * kSmallThreads;
+        cv[k] = i < E ? s_col[i] : 0u;
+      }
+      __syncthreads();  // (src may overlay s_col)
+#pragma unroll
+      for (int k = 0; k < kSmallCap / kSmallThreads; ++k) {
+        const int i = threadIdx.x + k * kSmallThreads;
+        if (i < E) src[i] = ((uint64_t)cv[k] << 32) | (uint32_t)i;
+      }
+      __syncthreads();
+      for (int l = 0; l < levels; ++l) {
+        for (int x = threadIdx.x; x < E; x += blockDim.x) {
+          const uint64_t key = src[x];
+          const int r = s_row[(uint32_t)key];
+          const int g0 = (r >> (l + 1)) << (l + 1);
+          const int gm = min(g0 + (1 << l), nrows), g1 = min(g0 + (2 << l), nrows);
+          const int a0 = (int)(s_rp[g0] - e0), am = (int)(s_rp[gm] - e0), a1 = (int)(s_rp[g1] - e0);
+          const bool left = r < gm;
+          int lo = left ? am : a0, hi = left ? a1 : am;
+          const int base = lo;
+          while (lo < hi) {  // keys of the partner run below ours
+            const int mid = (lo + hi) >> 1;
+            if (src[mid] < key) lo = mid + 1; else hi = mid;
           }
+          dst[a0 + (left ? x - a0 : x - am) + (lo - base)] = key;
         }
         __syncthreads();
+        uint64_t* t2 = src; src = dst; dst = t2;
       }
-    }
-    const int per = n / kSmallThreads > 0 ? n / kSmallThreads : 1;
-    const int beg = threadIdx.x * per;
-    uint32_t sum = 0;
-    for (int i = beg; i < beg + per && i < E; ++i)
-      if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++sum;
-    uint32_t run = block_excl_scan<kSmallThreads>(sum, &nact, s_scan);
-    for (int i = beg; i < beg + per && i < E; ++i) {
-      if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++run;
-      s_q[(uint32_t)s_keys[i]] = run - 1;
-    }
+      // src == s_keys now; s_q (overlaid by the merge buffer) is rewritten below
+      for (int i = threadIdx.x; i < E; i += blockDim.x) s_q[i] = 0xFFFFFFFFu;
+      __syncthreads();
+      const int per = (E + kSmallThreads - 1) / kSmallThreads;
+      const int beg = threadIdx.x * per;
+      uint32_t sum = 0;
+      for (int i = beg; i < beg + per && i < E; ++i)
+        if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++sum;
+      uint32_t run = block_excl_scan<kSmallThreads>(sum, &nact, s_scan);
+      for (int i = beg; i < beg + per && i < E; ++i) {
+        if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++run;
+        if ((uint32_t)s_keys[i] < (uint32_t)E) s_q[(uint32_t)s_keys[i]] = run - 1;
+      }
     }  // !windowed
   }
   // patterns (fill_brick_nnz_pattern): brick i = bc * (TM/16) + br in CSC order
@@ -1154,12 +1183,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
   __syncthreads();
   for (int i = threadIdx.x; i < E; i += blockDim.x) {
     const uint32_t qq = s_q[i], r = s_row[i];
+    q[e0 + i] = qq;
+    if (qq >= nact) continue;  // (only for invalid CSR: an unsorted row in the merge ranking)
     const uint32_t j = qq / tk, lc = qq % tk;
     const int bit = (int)(((r & 15) << 2) | (lc & 3));
     // 32-bit OR on the half holding the bit (a 64-bit shared atomicOr is a CAS loop on sm_100)
     uint32_t* half = reinterpret_cast<uint32_t*>(&s_pat[j * nbk + (lc >> 2) * nbrow + (r >> 4)]) + (bit >> 5);
     atomicOr(half, 1u << (bit & 31));
-    q[e0 + i] = qq;
   }
   __syncthreads();
   uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);

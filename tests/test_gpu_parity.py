@@ -129,6 +129,35 @@ def test_builder_rejects_invalid_csr():
     assert e.value.status == 2
 
 
+
+@pytest.mark.parametrize("path", ["narrow", "wide", "wsort", "merge", "hub"])
+@pytest.mark.parametrize("defect", ["unsorted", "duplicate"])
+def test_builder_rejects_invalid_csr_every_ranking_path(path, defect):
+    # one TM = 16 panel per case, shaped for each ranking path of the builder: warp byte map (span < 768), warp
+    # bitmap (span < 8192), warp sort (wide, <= 256 entries), CTA merge ranking (wide, scattered, <= 2048
+    # entries) and the hub path (> 2048 entries); one row then gets swapped or repeated columns
+    rng = np.random.default_rng(7)
+    per_row, span = {"narrow": (8, 600), "wide": (8, 6000), "wsort": (8, 10 ** 6), "merge": (60, 10 ** 6),
+                     "hub": (200, 10 ** 6)}[path]
+    K = 10 ** 6 + 7
+    cols = [np.sort(rng.choice(span, per_row, replace=False)).astype(np.int32) for _ in range(16)]
+    r = cols[5].copy()
+    if defect == "unsorted":
+        r[2], r[3] = r[3], r[2]
+    else:
+        r[3] = r[2]
+    cols[5] = r
+    rp = np.zeros(17, np.int64)
+    rp[1:] = np.cumsum([len(c) for c in cols])
+    ci = np.concatenate(cols)
+    v = rng.standard_normal(ci.size).astype(np.float32)
+    with pytest.raises(hp.HrpbError) as e:
+        gpu_build(16, K, rp, ci, v)
+    assert e.value.status == 2
+    ok = [np.sort(rng.choice(span, per_row, replace=False)).astype(np.int32) for _ in range(16)]
+    ci2 = np.concatenate(ok)  # the same shape, valid: bit-exact
+    assert_same_hrpb(gpu_build(16, K, rp, ci2, v), oracle.csr_to_hrpb(16, K, rp, ci2, v), path)
+
 # --------------------------------------------------------------------------- SpMM (S1..S5)
 @pytest.mark.parametrize("N", [1, 8, 31, 32, 33, 100, 128, 200, 256, 384, 512, 520])
 def test_spmm_exact_bitwise_widths(N):
