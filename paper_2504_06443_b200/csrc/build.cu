@@ -524,32 +524,60 @@ __device__ __forceinline__ bool warp_panel_rank(const int32_t* __restrict__ scol
     }
     w.patterns_done = fuse;
   } else {
-    // bitonic sort of (column, entry) keys, n = next power of two >= E (<= 256), then first-occurrence scan
-    int n = 32;
-    while (n < E) n <<= 1;
-    for (int i = E + lane; i < n; i += 32) keys[i] = ~0ull;
-    __syncwarp();
-    for (int kk = 2; kk <= n; kk <<= 1) {
-      for (int j = kk >> 1; j > 0; j >>= 1) {
-        for (int i = lane; i < n; i += 32) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const uint64_t a = keys[i], b = keys[ixj];
-            if ((a > b) == ((i & kk) == 0)) { keys[i] = b; keys[ixj] = a; }
-          }
-        }
-        __syncwarp();
-      }
+    // merge ranking (as k_count): the rows are sorted runs of (column, entry) keys; ceil(log2(rows)) levels of
+    // pairwise run merges, each key placed by one binary search in its partner run, ping-ponging with the
+    // (now dead) staged columns; then first occurrences are counted. Row starts go to sq[256..] (E <= 256).
+    static_assert(kWSortCap == 256 && kWSortCap * 8 <= 4 * (kWCap / 2 + 8), "merge buffer in the stage window");
+    uint64_t* src = keys;
+    uint64_t* dst = reinterpret_cast<uint64_t*>(my + L.off_stage);
+    uint16_t* rs = sq + kWSortCap;
+    const int nrows = w.nrows;
+#pragma unroll
+    for (int k = 0; k < (tm + 31) / 32; ++k) {
+      const int r = lane + 32 * k;
+      if (r < nrows) rs[r] = (uint16_t)(r == 0 ? 0u : w.st[k]);
     }
-    const int per = n / 32, beg = lane * per;
+    if (lane == 0) rs[nrows] = (uint16_t)E;
+    int levels = 0;
+    while ((1 << levels) < nrows) ++levels;
+    if (levels & 1) {  // the last level must land in `keys` (the values are staged into the window next)
+      for (int i = lane; i < E; i += 32) dst[i] = src[i];
+      uint64_t* t2 = src; src = dst; dst = t2;
+    }
+    __syncwarp();
+    for (int l = 0; l < levels; ++l) {
+      for (int x = lane; x < E; x += 32) {
+        const uint64_t key = src[x];
+        if ((uint32_t)key >= (uint32_t)E) continue;  // (stale slot: only after an unsorted row)
+        const int r = srow[(uint32_t)key];
+        const int g0 = (r >> (l + 1)) << (l + 1);
+        const int gm = min(g0 + (1 << l), nrows), g1 = min(g0 + (2 << l), nrows);
+        const int a0 = rs[g0], am = rs[gm], a1 = rs[g1];
+        const bool left = r < gm;
+        int lo = left ? am : a0, hi = left ? a1 : am;
+        const int base = lo;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (src[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        const int pos = a0 + (left ? x - a0 : x - am) + (lo - base);
+        if ((unsigned)pos < (unsigned)E) dst[pos] = key;  // (always, for sorted rows)
+      }
+      __syncwarp();
+      uint64_t* t2 = src; src = dst; dst = t2;
+    }
+    for (int i = lane; i < E; i += 32) sq[i] = 0xFFFFu;  // (an unsorted row may leave entries unranked)
+    __syncwarp();
+    const int per = (E + 31) / 32, beg = lane * per;
     uint32_t sum = 0;
     for (int i = beg; i < beg + per && i < E; ++i)
       if (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ++sum;
     uint32_t run = warp_excl_scan(sum, &nact);
     for (int i = beg; i < beg + per && i < E; ++i) {
       if (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ++run;
-      sq[(uint32_t)keys[i]] = (uint16_t)(run - 1);
+      if ((uint32_t)keys[i] < (uint32_t)E) sq[(uint32_t)keys[i]] = (uint16_t)(run - 1);
     }
+    __syncwarp();
   }
   w.nact = nact;
   w.nblk = (nact + tk - 1) / tk;
@@ -878,7 +906,10 @@ __global__ void __launch_bounds__(32 * kWWarps, HRPB_WB_MINB) k_wbuild(const int
       }
     } else {
       const uint64_t* keys = reinterpret_cast<const uint64_t*>(my);
-      for (int i = lane; i < w.E; i += 32) acp[sq[(uint32_t)keys[i]]] = (uint32_t)(keys[i] >> 32);
+      for (int i = lane; i < w.E; i += 32) {
+        const uint32_t e = (uint32_t)keys[i];
+        if (e < (uint32_t)w.E && sq[e] < w.nact) acp[sq[e]] = (uint32_t)(keys[i] >> 32);  // (guards: invalid CSR)
+      }
     }
     if (prep) {
       if ((uint32_t)lane < nblk) {
@@ -1144,6 +1175,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
       for (int l = 0; l < levels; ++l) {
         for (int x = threadIdx.x; x < E; x += blockDim.x) {
           const uint64_t key = src[x];
+          if ((uint32_t)key >= (uint32_t)E) continue;  // (stale slot: only after an unsorted row)
           const int r = s_row[(uint32_t)key];
           const int g0 = (r >> (l + 1)) << (l + 1);
           const int gm = min(g0 + (1 << l), nrows), g1 = min(g0 + (2 << l), nrows);
@@ -1155,7 +1187,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
             const int mid = (lo + hi) >> 1;
             if (src[mid] < key) lo = mid + 1; else hi = mid;
           }
-          dst[a0 + (left ? x - a0 : x - am) + (lo - base)] = key;
+          const int pos = a0 + (left ? x - a0 : x - am) + (lo - base);
+          if ((unsigned)pos < (unsigned)E) dst[pos] = key;  // (always, for sorted rows)
         }
         __syncthreads();
         uint64_t* t2 = src; src = dst; dst = t2;
