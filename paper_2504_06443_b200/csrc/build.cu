@@ -1255,9 +1255,11 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
                                                           uint64_t* __restrict__ gpat,
                                                           const uint32_t* __restrict__ biglist,
                                                           const uint32_t* __restrict__ nbig, uint32_t* scratch,
-                                                          int64_t words_per_cta, uint32_t* status) {
+                                                          int64_t words_per_cta, uint32_t* work,
+                                                          uint32_t* status) {
   __shared__ int64_t s_rp[129];
   __shared__ uint32_t s_scan[kBigThreads / 32 + 1];
+  __shared__ uint32_t s_t;
   const int64_t W = words_per_cta;          // >= K/32 + 2
   const int64_t W1 = (W + 31) / 32;         // occupancy words
   uint32_t* bm = scratch + (int64_t)blockIdx.x * (2 * W + 2 * W1);
@@ -1266,12 +1268,20 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
   uint32_t* occ_pre = occ + W1;
   const uint32_t count = *nbig;
   const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
-  if (blockIdx.x < count) {  // establish the all-zero invariant once
-    for (int64_t i = threadIdx.x; i < W; i += blockDim.x) bm[i] = 0u;
-    for (int64_t i = threadIdx.x; i < W1; i += blockDim.x) occ[i] = 0u;
-    __threadfence_block();
-  }
-  for (uint32_t t = blockIdx.x; t < count; t += gridDim.x) {
+  // hubs are claimed dynamically (sizes are power-law: a static round robin left CTAs 1.4x their mean share)
+  bool zeroed = false;
+  while (true) {
+    if (threadIdx.x == 0) s_t = atomicAdd(work, 1u);
+    __syncthreads();
+    const uint32_t t = s_t;
+    __syncthreads();
+    if (t >= count) break;
+    if (!zeroed) {  // establish the all-zero invariant at the CTA's first hub
+      for (int64_t i = threadIdx.x; i < W; i += blockDim.x) bm[i] = 0u;
+      for (int64_t i = threadIdx.x; i < W1; i += blockDim.x) occ[i] = 0u;
+      __threadfence_block();
+      zeroed = true;
+    }
     const int64_t p = biglist[t];
     load_panel_rows(rp, M, nnz, tm, p, s_rp, status);  // (barriers: also orders the zeroing above)
     const int nrows = (int)min((int64_t)tm, M - p * tm);
@@ -1413,13 +1423,19 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int64_t* __restrict
                                                       const uint32_t* __restrict__ midlist,
                                                       const uint32_t* __restrict__ nmid,
                                                       uint32_t* __restrict__ hublist, uint32_t* __restrict__ hubch,
-                                                      unsigned long long* __restrict__ nhub) {
+                                                      unsigned long long* __restrict__ nhub, uint32_t* work) {
   __shared__ int64_t s_rp[129];
   __shared__ uint32_t s_scan[kEmitThreads / 32 + 1];
   __shared__ uint64_t s_vbase[kEmitThreads];     // byte offset of each block's values (single-chunk panels)
   __shared__ uint64_t s_pt[kEmitThreads * 4];    // patterns (single-chunk panels with nbk <= 4)
   const uint32_t count = *nmid;
-  for (uint32_t tt = blockIdx.x; tt < count; tt += gridDim.x) {
+  __shared__ uint32_t s_tt;
+  while (true) {  // panels claimed dynamically (listed panels differ in size by orders of magnitude)
+    if (threadIdx.x == 0) s_tt = atomicAdd(work, 1u);
+    __syncthreads();
+    const uint32_t tt = s_tt;
+    __syncthreads();
+    if (tt >= count) break;
   const int64_t p = midlist[tt];
   const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0;
   if (nblk == 0) continue;
@@ -1706,12 +1722,12 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
       k_count<<<mid_ctas, kSmallThreads, count_smem, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
                                                           pbytes, gpat, l1, nl1, biglist, nbig, status);
       k_count_big<<<big_ctas, kBigThreads, 0, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk, pbytes, gpat,
-                                                    biglist, nbig, bigscr, words, status);
+                                                    biglist, nbig, bigscr, words, ctr + 3, status);
       // B1-B5 for warp-path panels + the single-pass scans B2 / B4 for all panels
       launch_wbuild(tm, tk, s, row_ptr, col_idx, values, M, K, nnz, P, listed, nblk, pbytes, ticket, lb, h->brp,
                     poff, h->ac, h->sp, h->packed, status);
       k_emit<<<mid_ctas, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp, poff,
-                                               gpat, h->ac, h->sp, h->packed, l1, nl1, hublist, hubch, nhub);
+                                               gpat, h->ac, h->sp, h->packed, l1, nl1, hublist, hubch, nhub, ctr + 5);
       k_emit_hubvals<<<mid_ctas, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, nnz, tm, tk, q, nact, h->brp,
                                                        gpat, h->ac, h->sp, h->packed, hublist, hubch, nhub);
       note_launch(6);
