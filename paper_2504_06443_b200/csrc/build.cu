@@ -38,8 +38,14 @@ constexpr int kBigThreads = 512;
 #ifndef HRPB_BIG_CTAS_PER_SM
 #define HRPB_BIG_CTAS_PER_SM 2  // hub CTAs per SM (each with its own column bitmap scratch, ~1 MB at K = 4M)
 #endif
-constexpr int64_t kHubEmit = 16384;
-constexpr int64_t kHubChunk = 4096;  // listed panels with more entries get their values scattered by all CTAs
+#ifndef HRPB_HUB_EMIT
+#define HRPB_HUB_EMIT 16384
+#endif
+#ifndef HRPB_HUB_CHUNK
+#define HRPB_HUB_CHUNK 4096
+#endif
+constexpr int64_t kHubEmit = HRPB_HUB_EMIT;    // listed panels above this many entries: values by k_emit_hubvals
+constexpr int64_t kHubChunk = HRPB_HUB_CHUNK;  // entries per k_emit_hubvals work item  // listed panels with more entries get their values scattered by all CTAs
 constexpr int kEmitThreads = 128;
 
 // ------------------------------------------------------------------ block-wide helpers
@@ -647,6 +653,11 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wclassify(const int64_t* __res
 #ifndef HRPB_LB_SLEEP
 #define HRPB_LB_SLEEP 64
 #endif
+#ifndef HRPB_LB_WIN
+#define HRPB_LB_WIN 1
+#endif
+constexpr int kLbWin = HRPB_LB_WIN;  // look-back windows of 32 states loaded per round (2, 4, 8: fewer rounds
+                                     // -- 4.7 -> 2.1 per panel at 4 -- but measured slower builds)
 #define kLbA (1ull << 62)
 #define kLbP (2ull << 62)
 #define kLbMask ((1ull << 62) - 1)
@@ -665,35 +676,62 @@ __device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
 __device__ __forceinline__ void warp_lb_publish(uint64_t* st, int64_t p, uint64_t agg) {
   if ((threadIdx.x & 31) == 0) st_relaxed_gpu(st + p, (p == 0 ? kLbP : kLbA) | agg);
 }
+#ifdef HRPB_BTRACE
+__device__ unsigned long long g_lbstat[4];  // look-back: panels, load rounds, polls of unpublished states
+#endif
 __device__ __forceinline__ uint64_t warp_lb_wait(uint64_t* st, int64_t p, uint64_t agg) {
   const int lane = threadIdx.x & 31;
+#ifdef HRPB_BTRACE
+  unsigned rounds = 0, polls = 0;
+#endif
   if (p == 0) {
     __syncwarp();
     return 0;
   }
+  // The nearest inclusive prefix is typically ~150 panels back on c2a (its owners are still in their own
+  // look-back); each round loads kLbWin windows of 32 states at once and walks them in order.
   uint64_t excl = 0;
   int64_t j = p - 1;
-  while (true) {
-    const int64_t idx = j - lane;
-    uint64_t v = idx >= 0 ? ld_relaxed_gpu(st + idx) : kLbP;
-    uint32_t pm;
-    while (true) {  // only the states up to the nearest inclusive prefix are needed: wait for those alone
-      pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
-      const uint32_t zm = __ballot_sync(0xffffffffu, (v >> 62) == 0);
-      const uint32_t need = pm ? ((pm & (0u - pm)) - 1u) : 0xFFFFFFFFu;  // lanes before the first P
-      if (!(zm & need)) break;
-      __nanosleep(HRPB_LB_SLEEP);  // back off: a spinning warp takes issue slots from the warps it waits for
-      if ((v >> 62) == 0) v = ld_relaxed_gpu(st + idx);
-    }
-    const int last = pm ? __ffs(pm) - 1 : 31;  // lanes 0..last contribute (lane `last` has the prefix)
-    uint64_t x = lane <= last ? (v & kLbMask) : 0;
+  bool done = false;
+  while (!done) {
+    uint64_t vw[kLbWin];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    excl += x;
-    if (pm) break;
-    j -= 32;
+    for (int u = 0; u < kLbWin; ++u) {
+      const int64_t idx = j - 32 * u - lane;
+      vw[u] = idx >= 0 ? ld_relaxed_gpu(st + idx) : kLbP;
+    }
+#ifdef HRPB_BTRACE
+    ++rounds;
+#endif
+#pragma unroll
+    for (int u = 0; u < kLbWin; ++u) {
+      const int64_t idx = j - 32 * u - lane;
+      uint64_t v = vw[u];
+      uint32_t pm;
+      while (true) {  // only the states up to the nearest inclusive prefix are needed: wait for those alone
+        pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const uint32_t zm = __ballot_sync(0xffffffffu, (v >> 62) == 0);
+        const uint32_t need = pm ? ((pm & (0u - pm)) - 1u) : 0xFFFFFFFFu;  // lanes before the first P
+        if (!(zm & need)) break;
+        __nanosleep(HRPB_LB_SLEEP);  // back off: a spinning warp takes issue slots from the warps it waits for
+#ifdef HRPB_BTRACE
+        ++polls;
+#endif
+        if ((v >> 62) == 0) v = ld_relaxed_gpu(st + idx);
+      }
+      const int last = pm ? __ffs(pm) - 1 : 31;  // lanes 0..last contribute (lane `last` has the prefix)
+      uint64_t x = lane <= last ? (v & kLbMask) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      excl += x;
+      if (pm) { done = true; break; }
+    }
+    j -= 32 * kLbWin;
   }
   if (lane == 0) st_relaxed_gpu(st + p, kLbP | (excl + agg));
+#ifdef HRPB_BTRACE
+  if (lane == 0) { atomicAdd(&g_lbstat[0], 1ull); atomicAdd(&g_lbstat[1], rounds); atomicAdd(&g_lbstat[2], polls); }
+#endif
   __syncwarp();
   return excl;
 }
@@ -1750,6 +1788,11 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
             (double)bt[5], (double)bt[6]);
     const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_btrace, z, sizeof(z));
+    unsigned long long ls[4];
+    cudaMemcpyFromSymbol(ls, g_lbstat, sizeof(ls));
+    fprintf(stderr, "look-back: %llu panels, %.2f load rounds and %.2f polls per panel\n", ls[0],
+            (double)ls[1] / (double)(ls[0] ? ls[0] : 1), (double)ls[2] / (double)(ls[0] ? ls[0] : 1));
+    cudaMemcpyToSymbol(g_lbstat, z, sizeof(ls));
 #endif
   }
   dfree(q, s); dfree(cnt, s); dfree(poff, s); dfree(gpat, s); dfree(biglist, s); dfree(info, s);
