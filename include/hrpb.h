@@ -114,6 +114,28 @@ hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, cons
                               const hrpb_config_t* cfg, hrpb_stream_t stream, hrpb_t* out, float* phase_ms);
 
 /*
+ * hrpb_build_spmm_async — hrpb_build_spmm without the per-call synchronization, for streams of repeated calls
+ * (the serving loop, the bench's timed steps). Same arguments as hrpb_build_spmm with out == NULL and no phase
+ * times. Once the call has been replayed as a CUDA graph (from the second identical call on, see above) it only
+ * launches the graph and returns: CSR errors the device detects (INVALID_CSR) are then reported by the next
+ * hrpb_sync_status on that stream, which returns the OR of every such replay since its previous call — as CUDA
+ * reports asynchronous kernel faults at a later synchronizing call. Until then, and whenever the arguments
+ * change, it behaves exactly like hrpb_build_spmm (synchronous, status returned directly). Argument checks
+ * (INVALID_VALUE, NOT_SUPPORTED) are always synchronous. C is valid after the stream is synchronized.
+ */
+hrpb_status_t hrpb_build_spmm_async(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
+                                    const int32_t* col_idx, const float* values, const float* B, float* C,
+                                    const hrpb_config_t* cfg, hrpb_stream_t stream);
+
+/*
+ * hrpb_sync_status — synchronizes `stream`; returns INVALID_CSR if any asynchronous replay since the previous
+ * call found an invalid CSR (then clears that state; the state is per device), else HRPB_SUCCESS.
+ *   phase_ms : NULL or float[2] receiving the build and SpMM phase times of this thread's most recent
+ *              hrpb_build_spmm / hrpb_build_spmm_async call (CUDA events on its stream).
+ */
+hrpb_status_t hrpb_sync_status(hrpb_stream_t stream, float* phase_ms);
+
+/*
  * hrpb_build_spmm_host — the whole hot path from HOST buffers (end-to-end entry point):
  * H2D copies of the CSR and B, hrpb_build, hrpb_spmm, D2H copy of C, returning after C is in host memory.
  * Pipelined: the CSR and then B (in 32 row chunks) are copied on a library-owned copy stream, the build runs on

@@ -141,7 +141,8 @@ static hrpb_status_t enqueue_build_spmm(int64_t M, int64_t K, int64_t N, int64_t
                                         cudaEvent_t* ev, bool capturing, bool release_arrays) {
   const unsigned fl = capturing ? cudaEventRecordExternal : 0u;
   cudaEventRecordWithFlags(ev[0], s, fl);
-  hrpb_status_t st = build_impl(M, K, nnz, row_ptr, col_idx, values, tm, tk, s, h, info);
+  // inside a graph the build also ORs its status into the sticky word (replays may be asynchronous)
+  hrpb_status_t st = build_impl(M, K, nnz, row_ptr, col_idx, values, tm, tk, s, h, info, capturing);
   cudaEventRecordWithFlags(ev[1], s, fl);
   // the SpMM goes in right behind the build (no host round trip between them); it reads the HRPB arrays on
   // the device, so it does not need the sizes the build reports
@@ -154,9 +155,14 @@ static hrpb_status_t enqueue_build_spmm(int64_t M, int64_t K, int64_t N, int64_t
   return st;
 }
 
-hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
-                              const int32_t* col_idx, const float* values, const float* B, float* C,
-                              const hrpb_config_t* cfg, hrpb_stream_t stream, hrpb_t* out, float* phase_ms) {
+// pinned read-back buffer, phase events and the replay plan: one set per host thread
+static thread_local uint64_t* t_info = nullptr;
+static thread_local cudaEvent_t t_ev[3] = {nullptr, nullptr, nullptr};
+
+static hrpb_status_t build_spmm_common(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
+                                       const int32_t* col_idx, const float* values, const float* B, float* C,
+                                       const hrpb_config_t* cfg, hrpb_stream_t stream, hrpb_t* out,
+                                       float* phase_ms, bool async) {
   if (out) *out = nullptr;
   if (M < 0 || K < 0 || N < 0 || nnz < 0 || M >= (1ll << 31) || K >= (1ll << 31) || N >= (1ll << 31) || !row_ptr)
     return HRPB_ERROR_INVALID_VALUE;
@@ -169,15 +175,14 @@ hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, cons
   cudaStream_t s = (cudaStream_t)stream;
   int dev = 0;
   cudaGetDevice(&dev);
-  // pinned read-back buffer, phase events and the replay plan: one set per host thread
-  static thread_local uint64_t* info = nullptr;
-  static thread_local cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   static thread_local BuildSpmmPlan plan;
   static thread_local hrpb_handle plan_h;
-  if (!info) {
-    if (cudaMallocHost(&info, 4 * sizeof(uint64_t)) != cudaSuccess) return HRPB_ERROR_OUT_OF_MEMORY;
-    for (auto& e : ev) cudaEventCreate(&e);
+  if (!t_info) {
+    if (cudaMallocHost(&t_info, 4 * sizeof(uint64_t)) != cudaSuccess) return HRPB_ERROR_OUT_OF_MEMORY;
+    for (auto& e : t_ev) cudaEventCreate(&e);
   }
+  uint64_t* info = t_info;
+  cudaEvent_t* ev = t_ev;
   static const bool use_graph = [] {
     const char* e = getenv("HRPB_NO_GRAPH");  // debugging aid: always run eagerly
     return !(e && atoi(e));
@@ -208,11 +213,13 @@ hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, cons
     if (plan.exec) {
       cudaError_t e = cudaGraphLaunch(plan.exec, s);
       g_launches.fetch_add(plan.kernels);
+      if (async) return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);  // status: hrpb_sync_status
       if (e == cudaSuccess) e = cudaStreamSynchronize(s);
       if (e != cudaSuccess) return cuda_status(e);
       hrpb_handle tmp;
       std::memset(&tmp, 0, sizeof(tmp));
       st = build_finish(&tmp, info, HRPB_SUCCESS);
+      if (st == HRPB_ERROR_INVALID_CSR) sticky_take(s);  // reported here: not again by hrpb_sync_status
       if (phase_ms && st == HRPB_SUCCESS) {
         cudaEventElapsedTime(&phase_ms[0], ev[0], ev[1]);
         cudaEventElapsedTime(&phase_ms[1], ev[1], ev[2]);
@@ -244,6 +251,29 @@ hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, cons
   }
   *out = h;
   return HRPB_SUCCESS;
+}
+
+hrpb_status_t hrpb_build_spmm(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
+                              const int32_t* col_idx, const float* values, const float* B, float* C,
+                              const hrpb_config_t* cfg, hrpb_stream_t stream, hrpb_t* out, float* phase_ms) {
+  return build_spmm_common(M, K, N, nnz, row_ptr, col_idx, values, B, C, cfg, stream, out, phase_ms, false);
+}
+
+hrpb_status_t hrpb_build_spmm_async(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
+                                    const int32_t* col_idx, const float* values, const float* B, float* C,
+                                    const hrpb_config_t* cfg, hrpb_stream_t stream) {
+  return build_spmm_common(M, K, N, nnz, row_ptr, col_idx, values, B, C, cfg, stream, nullptr, nullptr, true);
+}
+
+hrpb_status_t hrpb_sync_status(hrpb_stream_t stream, float* phase_ms) {
+  hrpb_status_t st = check_device();
+  if (st != HRPB_SUCCESS) return st;
+  st = sticky_take((cudaStream_t)stream);
+  if (phase_ms && st == HRPB_SUCCESS && t_ev[0]) {
+    cudaEventElapsedTime(&phase_ms[0], t_ev[0], t_ev[1]);
+    cudaEventElapsedTime(&phase_ms[1], t_ev[1], t_ev[2]);
+  }
+  return st;
 }
 
 hrpb_status_t hrpb_spmm(const hrpb_t A, const float* B, float* C, int64_t M, int64_t K, int64_t N,

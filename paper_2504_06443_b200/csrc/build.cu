@@ -1627,13 +1627,18 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_hubvals(const int64_t* __
   }
 }
 
+// status bits of asynchronous builds (graph replays of hrpb_build_spmm_async), ORed until read by
+// hrpb_sync_status / the next synchronous replay (sticky_take)
+__device__ unsigned int g_sticky_status;
+
 __global__ void k_finalize(const int64_t* __restrict__ rp, int64_t M, int64_t nnz, int64_t P,
                            const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff,
                            uint64_t* __restrict__ sp, const uint32_t* __restrict__ status,
-                           uint64_t* __restrict__ info) {
+                           uint64_t* __restrict__ info, unsigned int* sticky) {
   uint32_t st = *status;
   if (rp[0] != 0) st |= ST_RP0;
   if (rp[M] != nnz) st |= ST_NNZ;
+  if (sticky && st) atomicOr(sticky, st);
   const uint64_t nb = brp[P];
   sp[nb] = poff[P];
   info[0] = nb;
@@ -1692,7 +1697,7 @@ static void launch_wbuild(int tm, int tk, cudaStream_t s, const int64_t* rp, con
 
 hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
                          const float* values, int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h,
-                         uint64_t* deferred_info) {
+                         uint64_t* deferred_info, bool sticky) {
   const int64_t P = ceil_div(M, tm);
   const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
   // upper bounds (no host round trip): sum_p ceil(nact_p/tk) <= nnz/tk + min(P, nnz)
@@ -1770,7 +1775,9 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
                                                        gpat, h->ac, h->sp, h->packed, hublist, hubch, nhub);
       note_launch(6);
     }
-    k_finalize<<<1, 1, 0, s>>>(row_ptr, M, nnz, P, h->brp, poff, h->sp, status, info);
+    unsigned int* sticky_p = nullptr;
+    if (sticky) cudaGetSymbolAddress(reinterpret_cast<void**>(&sticky_p), g_sticky_status);
+    k_finalize<<<1, 1, 0, s>>>(row_ptr, M, nnz, P, h->brp, poff, h->sp, status, info, sticky_p);
     note_launch();
     cudaError_t e = cudaGetLastError();
     if (deferred_info) {  // (NUM_BLKS, bytes, status) land in the caller's pinned buffer; it syncs and finishes
@@ -1803,6 +1810,17 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     return st;
   }
   return build_finish(h, hinfo, st);
+}
+
+hrpb_status_t sticky_take(cudaStream_t s) {
+  unsigned int* addr = nullptr;
+  cudaError_t e = cudaGetSymbolAddress(reinterpret_cast<void**>(&addr), g_sticky_status);
+  unsigned int v = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&v, addr, sizeof(v), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && v) e = cudaMemsetAsync(addr, 0, sizeof(v), s);
+  if (e != cudaSuccess) return cuda_status(e);
+  return v ? HRPB_ERROR_INVALID_CSR : HRPB_SUCCESS;
 }
 
 hrpb_status_t build_finish(hrpb_handle* h, const uint64_t* info, hrpb_status_t st) {

@@ -27,8 +27,11 @@ hrpb_status_t cuda_status(cudaError_t e);
 // enqueued into that pinned 3-word buffer and the caller synchronizes the stream and calls build_finish.
 hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
                          const float* values, int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h,
-                         uint64_t* deferred_info = nullptr);
+                         uint64_t* deferred_info = nullptr, bool sticky = false);
 hrpb_status_t build_finish(hrpb_handle* h, const uint64_t* info, hrpb_status_t st);
+// synchronizes s, returns INVALID_CSR if any sticky build (sticky = true above) flagged its input since the
+// last call, and clears the flag
+hrpb_status_t sticky_take(cudaStream_t s);
 
 hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, cudaStream_t s);
 // C rows of panels [p_lo, p_hi) only (the pipelined host entry point)

@@ -61,6 +61,8 @@ def lib():
         L.hrpb_build_spmm_host.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Config), vp]
         L.hrpb_build_spmm.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Config), vp,
                                       C.POINTER(vp), C.POINTER(C.c_float)]
+        L.hrpb_build_spmm_async.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Config), vp]
+        L.hrpb_sync_status.argtypes = [vp, C.POINTER(C.c_float)]
         L.hrpb_free.argtypes = [vp]
         L.hrpb_get_view.argtypes = [vp, C.POINTER(_View)]
         L.hrpb_copy_view_to_host.argtypes = [vp, vp, vp, vp, vp]
@@ -68,8 +70,8 @@ def lib():
         L.hrpb_get_error_string.restype = C.c_char_p
         L.hrpb_last_cuda_error.restype = C.c_int
         L.hrpb_launch_count.restype = C.c_int64
-        for f in ("hrpb_build", "hrpb_spmm", "hrpb_build_spmm", "hrpb_build_spmm_host", "hrpb_free", "hrpb_get_view",
-                  "hrpb_copy_view_to_host"):
+        for f in ("hrpb_build", "hrpb_spmm", "hrpb_build_spmm", "hrpb_build_spmm_async", "hrpb_sync_status",
+                  "hrpb_build_spmm_host", "hrpb_free", "hrpb_get_view", "hrpb_copy_view_to_host"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -188,6 +190,32 @@ def build_spmm(row_ptr, col_idx, values, B, M: int, K: int, out=None, tm: int = 
                                C.byref(h) if keep else None, ms)
     _check(st, "hrpb_build_spmm")
     return out, (Hrpb(h) if keep else None), (float(ms[0]), float(ms[1]))
+
+
+def build_spmm_async(row_ptr, col_idx, values, B, M: int, K: int, out, tm: int = 16, tk: int = 16, stream=None):
+    """hrpb_build_spmm_async: build + SpMM into `out` without a per-call synchronization once the call is
+    graph-replayed; device-detected CSR errors surface at the next sync_status()."""
+    import torch
+    if B.dim() != 2 or B.shape[0] != K:
+        raise ValueError(f"B must be ({K}, N)")
+    N = int(B.shape[1])
+    nnz = int(col_idx.numel())
+    cfg = _Config(tm, tk)
+    st = lib().hrpb_build_spmm_async(M, K, N, nnz, _dev(row_ptr, torch.int64, "row_ptr"),
+                                     _dev(col_idx, torch.int32, "col_idx"), _dev(values, torch.float32, "values"),
+                                     _dev(B, torch.float32, "B"), _dev(out, torch.float32, "out"), C.byref(cfg),
+                                     _stream(stream))
+    _check(st, "hrpb_build_spmm_async")
+    return out
+
+
+def sync_status(stream=None):
+    """hrpb_sync_status: synchronize the stream, raise on an asynchronous INVALID_CSR; returns the (build_ms,
+    spmm_ms) phase times of this thread's most recent build_spmm / build_spmm_async call."""
+    ms = (C.c_float * 2)()
+    st = lib().hrpb_sync_status(_stream(stream), ms)
+    _check(st, "hrpb_sync_status")
+    return float(ms[0]), float(ms[1])
 
 
 def build_spmm_host(row_ptr, col_idx, values, B, M: int, K: int, out=None, tm: int = 16, tk: int = 16, stream=None):

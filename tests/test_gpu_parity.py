@@ -385,3 +385,43 @@ def test_build_spmm_graph_replay_exact():
         hp.build_spmm(rp, ci, v, B, w.M, w.K, out=C2, stream=side)
         side.synchronize()
         check_exact(C2.cpu().numpy(), Cref, "changed out")
+
+
+def test_build_spmm_async_replays_exact_and_deferred_errors():
+    """hrpb_build_spmm_async: once graph-replayed, calls return without synchronizing. Results bit-exact (exact
+    mode) after the stream syncs; an invalid CSR written into the same buffers is reported by the next
+    hrpb_sync_status (and only once); valid input afterwards reports success again."""
+    w = synth.make("c1", scale=1, N=64, mode=synth.EXACT)
+    Cref = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, w.B())
+    rp, ci, v, B = dev(w.row_ptr), dev(w.col_idx), dev(w.vals), dev(w.B())
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        C = torch.empty((w.M, w.N), device="cuda")
+        for k in range(6):
+            C.fill_(float("nan"))
+            hp.build_spmm_async(rp, ci, v, B, w.M, w.K, C, stream=side)
+            build_ms, spmm_ms = hp.sync_status(side)
+            assert build_ms > 0 and spmm_ms > 0
+            check_exact(C.cpu().numpy(), Cref, f"async call {k}")
+        for _ in range(4):  # back to back, one sync at the end
+            hp.build_spmm_async(rp, ci, v, B, w.M, w.K, C, stream=side)
+        hp.sync_status(side)
+        check_exact(C.cpu().numpy(), Cref, "back-to-back async calls")
+        r = int(w.row_ptr[3])
+        bad = w.col_idx.copy()
+        bad[r], bad[r + 1] = bad[r + 1], bad[r]  # unsorted row, same buffers (the graph is replayed)
+        ci.copy_(torch.from_numpy(bad).cuda())
+        hp.build_spmm_async(rp, ci, v, B, w.M, w.K, C, stream=side)  # returns before the device has checked
+        with pytest.raises(hp.HrpbError) as e:
+            hp.sync_status(side)
+        assert e.value.status == 2
+        hp.sync_status(side)  # reported once
+        ci.copy_(torch.from_numpy(w.col_idx).cuda())
+        hp.build_spmm_async(rp, ci, v, B, w.M, w.K, C, stream=side)
+        hp.sync_status(side)
+        check_exact(C.cpu().numpy(), Cref, "after the error")
+        with pytest.raises(hp.HrpbError) as e:  # the synchronous replay reports its own error directly
+            ci.copy_(torch.from_numpy(bad).cuda())
+            hp.build_spmm(rp, ci, v, B, w.M, w.K, out=C, stream=side)
+        assert e.value.status == 2
+        hp.sync_status(side)  # ... and not again here
