@@ -71,7 +71,8 @@ struct SpmmParams {
                      // 8 = skip A bulk copy, 16 = B gather zero-fill only (no global reads), 32 = no B cp.async at all
 };
 constexpr int kTraceN = 1024;
-constexpr int kTraceSlots = 9;  // slot 8: per warp of CTA 0 {cycles waiting on mbarriers, cycles total}
+constexpr int kTraceSlots = 10;  // slot 8: per warp of CTA 0 {cycles waiting on mbarriers, cycles total};
+                                 // slot 9: per CTA {cycles, blocks, panels, first panel}
 // trace slots: 0 producer issue (after empty), 1 A arrived (decoder), 2 decode done, 3 B arrived (MMA),
 //              4 MMA issued, 5 epilogue got tfull (per panel), 6 decoder slot table done, 7 decoder rows done
 // Instrumentation (HRPB_TRACE timestamps, HRPB_DEBUG work-skipping bits) exists only in builds with
@@ -126,16 +127,24 @@ struct SmemLayout {
 };
 
 
-// S1 work assignment. Work units: panel p owns units [brp[p] + p, brp[p+1] + p + 1) — one per block plus one for
+// S1 work assignment. Work units: panel p owns units [brp[p] + w p, brp[p+1] + w (p + 1)), w = kPanelW — one per block plus w for
 // its epilogue (so empty panels cost one unit). CTA c of G takes units [t_c, t_c+1) with t_c = c W / G snapped up
 // to the next panel start unless the panel containing it is "big" (more than a whole CTA share): such a panel
 // is split between CTAs, each accumulating its blocks into a workspace tile, and k_spmm_fixup adds the partial
 // tiles in CTA order (deterministic) into C.
+// kPanelW: units per panel epilogue (the C store of TM rows), 1 = one block's worth
+#ifndef HRPB_PANEL_W
+#define HRPB_PANEL_W 3
+#endif
+constexpr uint64_t kPanelW = HRPB_PANEL_W;
+__device__ __forceinline__ uint64_t unit_of(const uint32_t* brp, int64_t p) {  // units before panel p
+  return (uint64_t)brp[p] + kPanelW * (uint64_t)p;
+}
 __device__ __forceinline__ int64_t panel_of_unit(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t t) {
   // first p in [lo, hi) with brp[p + 1] + p + 1 > t (hi if none); binary search (one thread)
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
-    if ((uint64_t)brp[mid + 1] + (uint64_t)mid + 1 > t) hi = mid;
+    if (unit_of(brp, mid + 1) > t) hi = mid;
     else lo = mid + 1;
   }
   return lo;
@@ -147,7 +156,7 @@ __device__ __forceinline__ int64_t warp_panel_of_unit(const uint32_t* brp, int64
   while (hi - lo > 32) {
     const int64_t step = (hi - lo + 31) / 32;
     const int64_t idx = lo + lane * step;
-    const bool pred = idx < hi && (uint64_t)brp[idx + 1] + (uint64_t)idx + 1 > t;
+    const bool pred = idx < hi && unit_of(brp, idx + 1) > t;
     const uint32_t m = __ballot_sync(0xffffffffu, pred);
     if (!m) {  // every probe <= t: the answer is past the last probe inside [lo, hi)
       const int64_t kmax = min((int64_t)31, (hi - 1 - lo) / step);
@@ -161,7 +170,7 @@ __device__ __forceinline__ int64_t warp_panel_of_unit(const uint32_t* brp, int64
     hi = l0 + (int64_t)k * step;  // (itself a candidate: "none in [lo, hi)" means hi)
   }
   const int64_t idx = lo + lane;
-  const bool pred = idx < hi && (uint64_t)brp[idx + 1] + (uint64_t)idx + 1 > t;
+  const bool pred = idx < hi && unit_of(brp, idx + 1) > t;
   const uint32_t m = __ballot_sync(0xffffffffu, pred);
   return m ? lo + __ffs(m) - 1 : hi;
 }
@@ -169,8 +178,8 @@ __device__ __forceinline__ int64_t warp_panel_of_unit(const uint32_t* brp, int64
 template <typename FIND>
 __device__ __forceinline__ uint64_t work_boundary(const uint32_t* brp, int64_t p_lo, int64_t p_hi, uint64_t c,
                                                   uint64_t G, int64_t& pt, FIND find) {
-  const uint64_t base = (uint64_t)brp[p_lo] + (uint64_t)p_lo;
-  const uint64_t W = (uint64_t)brp[p_hi] + (uint64_t)p_hi - base;
+  const uint64_t base = unit_of(brp, p_lo);
+  const uint64_t W = unit_of(brp, p_hi) - base;
   if (c == 0) {
     pt = p_lo;
     return base;
@@ -183,7 +192,7 @@ __device__ __forceinline__ uint64_t work_boundary(const uint32_t* brp, int64_t p
   const int64_t p = find(brp, p_lo, p_hi, t);
   pt = p;
   if (p >= p_hi) return base + W;
-  const uint64_t start = (uint64_t)brp[p] + (uint64_t)p, end = (uint64_t)brp[p + 1] + (uint64_t)p + 1;
+  const uint64_t start = unit_of(brp, p), end = unit_of(brp, p + 1);
   if (t == start) return t;
   if ((end - start) * G > W) return t;  // big panel (more than a whole CTA share): split here
   pt = p + 1;                               // small panel: round up to the next panel start
@@ -209,12 +218,25 @@ __device__ __forceinline__ CtaWork cta_work(const uint32_t* brp, int64_t p_lo, i
   }
   w.pa = p0;  // the panel containing unit t0
   // the panel containing unit t1 - 1: p1 unless t1 is exactly p1's first unit (then the one before)
-  const int64_t pl = (p1 >= p_hi || t1 == (uint64_t)brp[p1] + (uint64_t)p1) ? p1 - 1 : p1;
+  const int64_t pl = (p1 >= p_hi || t1 == unit_of(brp, p1)) ? p1 - 1 : p1;
   w.pb = pl + 1;
-  w.first_full = t0 == (uint64_t)brp[w.pa] + (uint64_t)w.pa;
-  w.last_full = t1 == (uint64_t)brp[pl + 1] + (uint64_t)pl + 1;
-  w.bB = (uint32_t)max((uint64_t)brp[w.pa], t0 - (uint64_t)w.pa);
-  w.bE = (uint32_t)min((uint64_t)brp[pl + 1], t1 - (uint64_t)pl);
+  w.first_full = t0 == unit_of(brp, w.pa);
+  w.last_full = t1 == unit_of(brp, pl + 1);
+  // (a boundary inside a panel's epilogue units maps past its last block: clamp to the panel's blocks)
+  w.bB = (uint32_t)max((uint64_t)brp[w.pa], min((uint64_t)brp[w.pa + 1], t0 - kPanelW * (uint64_t)w.pa));
+  w.bE = (uint32_t)min((uint64_t)brp[pl + 1], t1 - kPanelW * (uint64_t)pl);
+  if (!w.first_full && w.bB >= brp[w.pa + 1]) {
+    // the range starts inside a split panel's epilogue units: it owns none of that panel's blocks (the fix-up
+    // stores the panel), so its first panel is the next one, from its start (else this CTA would treat the
+    // panel as one with no blocks and zero-fill its C rows)
+    ++w.pa;
+    w.first_full = true;
+    w.bB = brp[w.pa];
+    if (w.pa >= w.pb) {
+      w.pb = w.pa;
+      w.bE = w.bB;
+    }
+  }
   return w;
 }
 struct SerialFind {
@@ -712,6 +734,13 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   }
   tc_fence_before();
   __syncthreads();
+  if (tracing(prm) && threadIdx.x == 0 && 4 * blockIdx.x + 3 < kTraceN) {  // per-CTA balance (S1 cost model)
+    long long* t = prm.trace + 9 * kTraceN + 4 * blockIdx.x;
+    t[0] = clock64() - t_start;
+    t[1] = (long long)range[3] - (long long)range[2];
+    t[2] = (long long)range[1] - (long long)range[0];
+    t[3] = (long long)range[0];
+  }
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tbase, tmem_cols);
@@ -729,11 +758,11 @@ __global__ void __launch_bounds__(128) k_spmm_fixup(const uint32_t* __restrict__
   if (c == 0 || *split_flag != epoch) return;  // no split panel in this launch
   int64_t pt;
   const uint64_t t = work_boundary(brp, p_lo, p_hi, c, G, pt, SerialFind());
-  const uint64_t base = (uint64_t)brp[p_lo] + (uint64_t)p_lo;
+  const uint64_t base = unit_of(brp, p_lo);
   if (t <= base) return;
   const int64_t q = panel_of_unit(brp, p_lo, p_hi, t - 1);
   if (q >= p_hi) return;
-  const uint64_t qs = (uint64_t)brp[q] + (uint64_t)q, qe = (uint64_t)brp[q + 1] + (uint64_t)q + 1;
+  const uint64_t qs = unit_of(brp, q), qe = unit_of(brp, q + 1);
   if (t >= qe || t <= qs) return;  // boundary c is not inside q
   if (c >= 2 && work_boundary(brp, p_lo, p_hi, c - 1, G, pt, SerialFind()) > qs) return;  // earlier one inside q
   const int64_t row0 = q * TMV;

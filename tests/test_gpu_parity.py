@@ -425,3 +425,30 @@ def test_build_spmm_async_replays_exact_and_deferred_errors():
             hp.build_spmm(rp, ci, v, B, w.M, w.K, out=C, stream=side)
         assert e.value.status == 2
         hp.sync_status(side)  # ... and not again here
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_spmm_split_boundaries_everywhere(seed):
+    """S1 with epilogue-weighted units: panels of 1..250 blocks so that CTA boundaries fall in every kind of place
+    (block units, a big panel's epilogue units, panel starts); exact mode, bit-exact against the oracle."""
+    rng = np.random.default_rng(100 + seed)
+    P, K, N = 96, 8192, 64
+    rows, cols = [], []
+    for p in range(P):
+        nact = int(rng.choice([1, 5, 16, 40, 300, 1200, 4000])) if rng.random() < 0.7 else int(rng.integers(1, 4000))
+        act = np.sort(rng.choice(K, nact, replace=False))
+        for r in range(16):
+            k = int(rng.integers(0, min(nact, 40) + 1))
+            c = np.sort(rng.choice(act, k, replace=False)) if k else np.zeros(0, np.int64)
+            if r == 0:
+                c = act  # every active column appears in the panel
+            cols.append(c.astype(np.int32))
+    M = len(cols)
+    rp = np.zeros(M + 1, np.int64)
+    rp[1:] = np.cumsum([len(c) for c in cols])
+    ci = np.concatenate(cols)
+    v = rng.choice(np.array([-2, -1, 1, 2], np.float32), ci.size)
+    Bh = rng.integers(-2, 3, (K, N)).astype(np.float32)
+    A = gpu_build(M, K, rp, ci, v)
+    C = hp.spmm(A, dev(Bh))
+    check_exact(C.cpu().numpy(), oracle.csr_spmm(M, K, rp, ci, v, Bh), f"seed {seed}")
