@@ -636,6 +636,7 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wclassify(const int64_t* __res
                                                            int64_t P, uint8_t* __restrict__ listed,
                                                            uint32_t* __restrict__ list,
                                                            uint32_t* __restrict__ nlist) {
+  pdl_wait();
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t p = (int64_t)blockIdx.x * kWWarps + wid; p < P; p += (int64_t)gridDim.x * kWWarps) {
     WarpPanel w;
@@ -793,6 +794,7 @@ __global__ void __launch_bounds__(32 * kWWarps, HRPB_WB_MINB) k_wbuild(const int
                                                         uint64_t* __restrict__ poff, uint32_t* __restrict__ ac,
                                                         uint64_t* __restrict__ sp, uint8_t* __restrict__ packed,
                                                         uint32_t* status) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t dsm[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const WarpLayout L = warp_layout(tm, tk);
@@ -1055,6 +1057,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restri
                                                         const uint32_t* __restrict__ nmid,
                                                         uint32_t* __restrict__ biglist,
                                                         uint32_t* __restrict__ nbig, uint32_t* status) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ int64_t s_rp[129];
   __shared__ uint32_t s_scan[kSmallThreads / 32 + 1];
@@ -1295,6 +1298,7 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
                                                           const uint32_t* __restrict__ nbig, uint32_t* scratch,
                                                           int64_t words_per_cta, uint32_t* work,
                                                           uint32_t* status) {
+  pdl_wait();
   __shared__ int64_t s_rp[129];
   __shared__ uint32_t s_scan[kBigThreads / 32 + 1];
   __shared__ uint32_t s_t;
@@ -1462,6 +1466,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int64_t* __restrict
                                                       const uint32_t* __restrict__ nmid,
                                                       uint32_t* __restrict__ hublist, uint32_t* __restrict__ hubch,
                                                       unsigned long long* __restrict__ nhub, uint32_t* work) {
+  pdl_wait();
   __shared__ int64_t s_rp[129];
   __shared__ uint32_t s_scan[kEmitThreads / 32 + 1];
   __shared__ uint64_t s_vbase[kEmitThreads];     // byte offset of each block's values (single-chunk panels)
@@ -1585,6 +1590,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_hubvals(const int64_t* __
                                                               const uint32_t* __restrict__ hublist,
                                                               const uint32_t* __restrict__ hubch,
                                                               const unsigned long long* __restrict__ nhub) {
+  pdl_wait();
   __shared__ int64_t s_rp[129];
   const unsigned long long hc = *nhub;
   const uint32_t count = (uint32_t)(hc >> 32), total = (uint32_t)hc;
@@ -1635,6 +1641,7 @@ __global__ void k_finalize(const int64_t* __restrict__ rp, int64_t M, int64_t nn
                            const uint32_t* __restrict__ brp, const uint64_t* __restrict__ poff,
                            uint64_t* __restrict__ sp, const uint32_t* __restrict__ status,
                            uint64_t* __restrict__ info, unsigned int* sticky) {
+  pdl_wait();
   uint32_t st = *status;
   if (rp[0] != 0) st |= ST_RP0;
   if (rp[M] != nnz) st |= ST_NNZ;
@@ -1687,7 +1694,7 @@ static void launch_wbuild(int tm, int tk, cudaStream_t s, const int64_t* rp, con
 #define HRPB_WB(A, B)                                                                                          \
   {                                                                                                            \
     const int64_t want = ceil_div(P, kWWarps), have = (int64_t)wbuild_ctas<A, B>() * num_sms();                \
-    k_wbuild<A, B><<<(unsigned)(want < have ? want : have), 32 * kWWarps, smem, s>>>(                          \
+    launch_pdl(k_wbuild<A, B>, (unsigned)(want < have ? want : have), 32 * kWWarps, smem, s,                   \
         rp, ci, vals, M, K, nnz, P, listed, nblk_listed, pbytes_listed, ticket, lb, brp, poff,                \
         ac, sp, packed, status);                                                                               \
   }
@@ -1762,22 +1769,22 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     if (P > 0) {
       // classification; listed panels counted by a CTA (<= kSmallCap entries) or the hub bitmap kernel
       launch_wclassify(tm, tk, wgrid, s, row_ptr, col_idx, M, nnz, P, listed, l1, nl1);
-      k_count<<<mid_ctas, kSmallThreads, count_smem, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
+      launch_pdl(k_count, mid_ctas, kSmallThreads, count_smem, s, row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
                                                           pbytes, gpat, l1, nl1, biglist, nbig, status);
-      k_count_big<<<big_ctas, kBigThreads, 0, s>>>(row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk, pbytes, gpat,
+      launch_pdl(k_count_big, big_ctas, kBigThreads, 0, s, row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk, pbytes, gpat,
                                                     biglist, nbig, bigscr, words, ctr + 3, status);
       // B1-B5 for warp-path panels + the single-pass scans B2 / B4 for all panels
       launch_wbuild(tm, tk, s, row_ptr, col_idx, values, M, K, nnz, P, listed, nblk, pbytes, ticket, lb, h->brp,
                     poff, h->ac, h->sp, h->packed, status);
-      k_emit<<<mid_ctas, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp, poff,
+      launch_pdl(k_emit, mid_ctas, kEmitThreads, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp, poff,
                                                gpat, h->ac, h->sp, h->packed, l1, nl1, hublist, hubch, nhub, ctr + 5);
-      k_emit_hubvals<<<mid_ctas, kEmitThreads, 0, s>>>(row_ptr, col_idx, values, M, nnz, tm, tk, q, nact, h->brp,
+      launch_pdl(k_emit_hubvals, mid_ctas, kEmitThreads, 0, s, row_ptr, col_idx, values, M, nnz, tm, tk, q, nact, h->brp,
                                                        gpat, h->ac, h->sp, h->packed, hublist, hubch, nhub);
       note_launch(6);
     }
     unsigned int* sticky_p = nullptr;
     if (sticky) cudaGetSymbolAddress(reinterpret_cast<void**>(&sticky_p), g_sticky_status);
-    k_finalize<<<1, 1, 0, s>>>(row_ptr, M, nnz, P, h->brp, poff, h->sp, status, info, sticky_p);
+    launch_pdl(k_finalize, 1, 1, 0, s, row_ptr, M, nnz, P, h->brp, poff, h->sp, status, info, sticky_p);
     note_launch();
     cudaError_t e = cudaGetLastError();
     if (deferred_info) {  // (NUM_BLKS, bytes, status) land in the caller's pinned buffer; it syncs and finishes

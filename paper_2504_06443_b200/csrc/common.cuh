@@ -141,4 +141,32 @@ __device__ __forceinline__ float to_tf32_rna(float x) {
 }
 
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may start while its predecessor on the stream
+// drains (its launch latency overlaps the predecessor's last CTAs); pdl_wait() at its top blocks until the
+// predecessor grid has completed and its memory is visible (a no-op for a normal launch). Predecessors never
+// trigger early, so a waiting grid cannot hold SM resources the predecessor still needs.
+#ifndef HRPB_PDL
+#define HRPB_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if HRPB_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = HRPB_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 }  // namespace hrpb

@@ -300,6 +300,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 //                   1 = cp.async 16-B copies by all 128 producer threads into the same swizzled layout.
 template <int NT, int GM, int TMV, int TKV>
 __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant__ CUtensorMap tmB, SpmmParams prm) {
+  pdl_wait();
   using L = SmemLayout<NT, TMV, TKV>;
   static_assert(GM == 1 || TKV == 16, "TMA gather4 staging is written for TK = 16");
   constexpr int kARawBytes = L::kARawBytes, kATileBytes = L::kATileBytes;
@@ -754,6 +755,7 @@ __global__ void __launch_bounds__(128) k_spmm_fixup(const uint32_t* __restrict__
                                                     const float* __restrict__ ws, float* __restrict__ C, int64_t M,
                                                     int64_t N, int n0, int wcols, const uint64_t* split_flag,
                                                     uint64_t epoch) {
+  pdl_wait();
   const uint64_t G = gridDim.x, c = blockIdx.x;
   if (c == 0 || *split_flag != epoch) return;  // no split panel in this launch
   int64_t pt;
@@ -823,8 +825,9 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   if ((int64_t)grid > p_hi - p_lo) grid = (int)(p_hi > p_lo ? p_hi - p_lo : 1);
   SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, p_lo, p_hi, scr.ws, scr.flag, scr.epoch,
                  B, h->K, ldb, n0, stages, trace, debug};
-  k_spmm<NT, GM, TMV, TKV><<<grid, kSpmmThreads, smem, s>>>(tm, prm);
-  k_spmm_fixup<TMV><<<grid, 128, 0, s>>>(h->brp, p_lo, p_hi, scr.ws, C, h->M, N, n0, 128 * NT, scr.flag, scr.epoch);
+  launch_pdl(k_spmm<NT, GM, TMV, TKV>, grid, kSpmmThreads, smem, s, tm, prm);
+  launch_pdl(k_spmm_fixup<TMV>, grid, 128, 0, s, h->brp, p_lo, p_hi, scr.ws, C, h->M, N, n0, 128 * NT, scr.flag,
+             scr.epoch);
   note_launch(2);
   if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)
     static long long host[kTraceSlots * kTraceN];
