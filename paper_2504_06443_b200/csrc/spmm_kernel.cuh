@@ -132,23 +132,39 @@ struct SmemLayout {
 // to the next panel start unless the panel containing it is "big" (more than a whole CTA share): such a panel
 // is split between CTAs, each accumulating its blocks into a workspace tile, and k_spmm_fixup adds the partial
 // tiles in CTA order (deterministic) into C.
-// kPanelW: units per panel epilogue (the C store of TM rows), 1 = one block's worth
+// kPanelW: units per panel epilogue per 16 panel rows (the C store of TM rows), 1 = one block's worth
 #ifndef HRPB_PANEL_W
 #define HRPB_PANEL_W 3
 #endif
 constexpr uint64_t kPanelW = HRPB_PANEL_W;
-__device__ __forceinline__ uint64_t unit_of(const uint32_t* brp, int64_t p) {  // units before panel p
-  return (uint64_t)brp[p] + kPanelW * (uint64_t)p;
+#ifndef HRPB_PANEL_W32
+#define HRPB_PANEL_W32 3
+#endif
+#ifndef HRPB_PANEL_W64
+#define HRPB_PANEL_W64 12
+#endif
+// measured on c3 (R-MAT, N = 256): TM = 16 → 3 units (22.1 → 18.1 ms), TM = 32 → 3 (6: 21.0 ms),
+// TM = 64 → 12 (3: 27.0 ms, 12: 18.8 ms); TM = 128 scales TM = 64's
+template <int TMV>
+__host__ __device__ constexpr uint64_t panel_weight() {
+  return TMV == 16 ? kPanelW : TMV == 32 ? (uint64_t)HRPB_PANEL_W32 : TMV == 64 ? (uint64_t)HRPB_PANEL_W64
+                                                                                : 2 * (uint64_t)HRPB_PANEL_W64;
 }
+template <uint64_t PW>
+__device__ __forceinline__ uint64_t unit_of(const uint32_t* brp, int64_t p) {  // units before panel p
+  return (uint64_t)brp[p] + PW * (uint64_t)p;
+}
+template <uint64_t PW>
 __device__ __forceinline__ int64_t panel_of_unit(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t t) {
   // first p in [lo, hi) with brp[p + 1] + p + 1 > t (hi if none); binary search (one thread)
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
-    if (unit_of(brp, mid + 1) > t) hi = mid;
+    if (unit_of<PW>(brp, mid + 1) > t) hi = mid;
     else lo = mid + 1;
   }
   return lo;
 }
+template <uint64_t PW>
 __device__ __forceinline__ int64_t warp_panel_of_unit(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t t) {
   // the same by a whole warp: 32-way search, ~log32(P) dependent loads instead of log2(P). Invariant: the answer
   // is in [lo, hi] (hi = none in [lo, hi)).
@@ -156,7 +172,7 @@ __device__ __forceinline__ int64_t warp_panel_of_unit(const uint32_t* brp, int64
   while (hi - lo > 32) {
     const int64_t step = (hi - lo + 31) / 32;
     const int64_t idx = lo + lane * step;
-    const bool pred = idx < hi && unit_of(brp, idx + 1) > t;
+    const bool pred = idx < hi && unit_of<PW>(brp, idx + 1) > t;
     const uint32_t m = __ballot_sync(0xffffffffu, pred);
     if (!m) {  // every probe <= t: the answer is past the last probe inside [lo, hi)
       const int64_t kmax = min((int64_t)31, (hi - 1 - lo) / step);
@@ -170,16 +186,16 @@ __device__ __forceinline__ int64_t warp_panel_of_unit(const uint32_t* brp, int64
     hi = l0 + (int64_t)k * step;  // (itself a candidate: "none in [lo, hi)" means hi)
   }
   const int64_t idx = lo + lane;
-  const bool pred = idx < hi && unit_of(brp, idx + 1) > t;
+  const bool pred = idx < hi && unit_of<PW>(brp, idx + 1) > t;
   const uint32_t m = __ballot_sync(0xffffffffu, pred);
   return m ? lo + __ffs(m) - 1 : hi;
 }
 // boundary t_c and the panel containing unit t_c (p_hi if t_c is the end); FIND = (brp, lo, hi, t) -> panel
-template <typename FIND>
+template <uint64_t PW, typename FIND>
 __device__ __forceinline__ uint64_t work_boundary(const uint32_t* brp, int64_t p_lo, int64_t p_hi, uint64_t c,
                                                   uint64_t G, int64_t& pt, FIND find) {
-  const uint64_t base = unit_of(brp, p_lo);
-  const uint64_t W = unit_of(brp, p_hi) - base;
+  const uint64_t base = unit_of<PW>(brp, p_lo);
+  const uint64_t W = unit_of<PW>(brp, p_hi) - base;
   if (c == 0) {
     pt = p_lo;
     return base;
@@ -192,7 +208,7 @@ __device__ __forceinline__ uint64_t work_boundary(const uint32_t* brp, int64_t p
   const int64_t p = find(brp, p_lo, p_hi, t);
   pt = p;
   if (p >= p_hi) return base + W;
-  const uint64_t start = unit_of(brp, p), end = unit_of(brp, p + 1);
+  const uint64_t start = unit_of<PW>(brp, p), end = unit_of<PW>(brp, p + 1);
   if (t == start) return t;
   if ((end - start) * G > W) return t;  // big panel (more than a whole CTA share): split here
   pt = p + 1;                               // small panel: round up to the next panel start
@@ -203,13 +219,13 @@ struct CtaWork {
   uint32_t bB, bE;     // its flat block range
   bool first_full, last_full;  // owns all units of pa / of pb - 1
 };
-template <typename FIND>
+template <uint64_t PW, typename FIND>
 __device__ __forceinline__ CtaWork cta_work(const uint32_t* brp, int64_t p_lo, int64_t p_hi, uint64_t c, uint64_t G,
                                             FIND find) {
   CtaWork w;
   int64_t p0, p1;
-  const uint64_t t0 = work_boundary(brp, p_lo, p_hi, c, G, p0, find);
-  const uint64_t t1 = work_boundary(brp, p_lo, p_hi, c + 1, G, p1, find);
+  const uint64_t t0 = work_boundary<PW>(brp, p_lo, p_hi, c, G, p0, find);
+  const uint64_t t1 = work_boundary<PW>(brp, p_lo, p_hi, c + 1, G, p1, find);
   if (t1 <= t0) {
     w.pa = w.pb = p_lo;
     w.bB = w.bE = brp[p_lo];
@@ -218,13 +234,13 @@ __device__ __forceinline__ CtaWork cta_work(const uint32_t* brp, int64_t p_lo, i
   }
   w.pa = p0;  // the panel containing unit t0
   // the panel containing unit t1 - 1: p1 unless t1 is exactly p1's first unit (then the one before)
-  const int64_t pl = (p1 >= p_hi || t1 == unit_of(brp, p1)) ? p1 - 1 : p1;
+  const int64_t pl = (p1 >= p_hi || t1 == unit_of<PW>(brp, p1)) ? p1 - 1 : p1;
   w.pb = pl + 1;
-  w.first_full = t0 == unit_of(brp, w.pa);
-  w.last_full = t1 == unit_of(brp, pl + 1);
+  w.first_full = t0 == unit_of<PW>(brp, w.pa);
+  w.last_full = t1 == unit_of<PW>(brp, pl + 1);
   // (a boundary inside a panel's epilogue units maps past its last block: clamp to the panel's blocks)
-  w.bB = (uint32_t)max((uint64_t)brp[w.pa], min((uint64_t)brp[w.pa + 1], t0 - kPanelW * (uint64_t)w.pa));
-  w.bE = (uint32_t)min((uint64_t)brp[pl + 1], t1 - kPanelW * (uint64_t)pl);
+  w.bB = (uint32_t)max((uint64_t)brp[w.pa], min((uint64_t)brp[w.pa + 1], t0 - PW * (uint64_t)w.pa));
+  w.bE = (uint32_t)min((uint64_t)brp[pl + 1], t1 - PW * (uint64_t)pl);
   if (!w.first_full && w.bB >= brp[w.pa + 1]) {
     // the range starts inside a split panel's epilogue units: it owns none of that panel's blocks (the fix-up
     // stores the panel), so its first panel is the next one, from its start (else this CTA would treat the
@@ -239,14 +255,16 @@ __device__ __forceinline__ CtaWork cta_work(const uint32_t* brp, int64_t p_lo, i
   }
   return w;
 }
+template <uint64_t PW>
 struct SerialFind {
   __device__ int64_t operator()(const uint32_t* b, int64_t lo, int64_t hi, uint64_t t) const {
-    return panel_of_unit(b, lo, hi, t);
+    return panel_of_unit<PW>(b, lo, hi, t);
   }
 };
+template <uint64_t PW>
 struct WarpFind {
   __device__ int64_t operator()(const uint32_t* b, int64_t lo, int64_t hi, uint64_t t) const {
-    return warp_panel_of_unit(b, lo, hi, t);
+    return warp_panel_of_unit<PW>(b, lo, hi, t);
   }
 };
 
@@ -301,6 +319,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 template <int NT, int GM, int TMV, int TKV>
 __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant__ CUtensorMap tmB, SpmmParams prm) {
   pdl_wait();
+  constexpr uint64_t kPW = panel_weight<TMV>();  // S1 units per panel epilogue
   using L = SmemLayout<NT, TMV, TKV>;
   static_assert(GM == 1 || TKV == 16, "TMA gather4 staging is written for TK = 16");
   constexpr int kARawBytes = L::kARawBytes, kATileBytes = L::kATileBytes;
@@ -348,7 +367,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   }
   if (warp == kMmaWarp) tmem_alloc(&misc[0], tmem_cols);
   if (warp == 0) {  // S1: contiguous range of ~equal work (blocks + panels) in [p_lo, p_hi); big panels may split
-    const CtaWork cw = cta_work(prm.brp, prm.p_lo, prm.p_hi, blockIdx.x, gridDim.x, WarpFind());
+    const CtaWork cw = cta_work<kPW>(prm.brp, prm.p_lo, prm.p_hi, blockIdx.x, gridDim.x, WarpFind<kPW>());
     if (lane == 0) {
       range[0] = cw.pa; range[1] = cw.pb; range[2] = cw.bB; range[3] = cw.bE;
       range[4] = cw.first_full; range[5] = cw.last_full;
@@ -756,17 +775,18 @@ __global__ void __launch_bounds__(128) k_spmm_fixup(const uint32_t* __restrict__
                                                     int64_t N, int n0, int wcols, const uint64_t* split_flag,
                                                     uint64_t epoch) {
   pdl_wait();
+  constexpr uint64_t kPW = panel_weight<TMV>();
   const uint64_t G = gridDim.x, c = blockIdx.x;
   if (c == 0 || *split_flag != epoch) return;  // no split panel in this launch
   int64_t pt;
-  const uint64_t t = work_boundary(brp, p_lo, p_hi, c, G, pt, SerialFind());
-  const uint64_t base = unit_of(brp, p_lo);
+  const uint64_t t = work_boundary<kPW>(brp, p_lo, p_hi, c, G, pt, SerialFind<kPW>());
+  const uint64_t base = unit_of<kPW>(brp, p_lo);
   if (t <= base) return;
-  const int64_t q = panel_of_unit(brp, p_lo, p_hi, t - 1);
+  const int64_t q = panel_of_unit<kPW>(brp, p_lo, p_hi, t - 1);
   if (q >= p_hi) return;
-  const uint64_t qs = unit_of(brp, q), qe = unit_of(brp, q + 1);
+  const uint64_t qs = unit_of<kPW>(brp, q), qe = unit_of<kPW>(brp, q + 1);
   if (t >= qe || t <= qs) return;  // boundary c is not inside q
-  if (c >= 2 && work_boundary(brp, p_lo, p_hi, c - 1, G, pt, SerialFind()) > qs) return;  // earlier one inside q
+  if (c >= 2 && work_boundary<kPW>(brp, p_lo, p_hi, c - 1, G, pt, SerialFind<kPW>()) > qs) return;  // earlier one inside q
   const int64_t row0 = q * TMV;
   const int nrows = (int)min((int64_t)TMV, M - row0);
   const int64_t ncols = min((int64_t)wcols, N - n0);
@@ -775,7 +795,7 @@ __global__ void __launch_bounds__(128) k_spmm_fixup(const uint32_t* __restrict__
     const int64_t col = e % ncols;
     float acc = 0.f;
     for (uint64_t cc = c - 1; cc < G; ++cc) {
-      const CtaWork w = cta_work(brp, p_lo, p_hi, cc, G, SerialFind());
+      const CtaWork w = cta_work<kPW>(brp, p_lo, p_hi, cc, G, SerialFind<kPW>());
       if (w.pa > q) break;
       const uint32_t b0 = max(brp[q], w.bB), b1 = min(brp[q + 1], w.bE);
       if (b0 >= b1) continue;  // no blocks of q in CTA cc
