@@ -203,7 +203,10 @@ __host__ __device__ constexpr int wslots(int tm, int tk) {
   return 16 * (tk / HRPB_BRICK_K) * (tm / HRPB_BRICK_M) < 128 ? 16 * (tk / HRPB_BRICK_K) * (tm / HRPB_BRICK_M)
                                                                 : 128;
 }
-constexpr int kWWarps = 4;        // warps per CTA
+#ifndef HRPB_WWARPS
+#define HRPB_WWARPS 4
+#endif
+constexpr int kWWarps = HRPB_WWARPS;  // warps per CTA (k_wclassify, k_wbuild)
 constexpr int kB = 4;             // entries per lane per round in the warp-path entry loops
 #ifndef HRPB_WB_MINB
 #define HRPB_WB_MINB 5            // k_wbuild CTAs per SM the register allocation must allow (shared memory: 5)
