@@ -340,15 +340,6 @@ __device__ __forceinline__ bool warp_panel_span(WarpPanel& w, GetCol col) {
   return w.E <= kWSortCap;
 }
 
-template <int tm, int tk>
-__device__ __forceinline__ bool warp_panel_open(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                                int64_t M, int64_t nnz, int64_t p, WarpPanel& w,
-                                                uint32_t* status) {
-  if (!warp_panel_rows<tm, tk>(rp, M, nnz, p, w, status)) return false;
-  const int64_t e0 = w.e0;
-  return warp_panel_span<tm>(w, [&](uint32_t i) { return ci[e0 + i]; });
-}
-
 // Stages 4-byte elements [e0, e0 + E) of a CSR array into shared memory with cp.async (one latency for the
 // whole panel): 16-B copies from the 16-B aligned window around e0 (src-size clamps at nnz) when the array base
 // is 16-B aligned, else 4-B copies. Commits one cp.async group; returns the offset of e0 in the window.
@@ -643,7 +634,10 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wclassify(const int64_t* __res
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t p = (int64_t)blockIdx.x * kWWarps + wid; p < P; p += (int64_t)gridDim.x * kWWarps) {
     WarpPanel w;
-    const bool ok = warp_panel_open<tm, tk>(rp, ci, M, nnz, p, w, nullptr);
+    // panels with <= kWSortCap entries take the warp path whatever their span (bitmap or merge ranking, decided
+    // again in k_wbuild): no column reads for them
+    bool ok = warp_panel_rows<tm, tk>(rp, M, nnz, p, w, nullptr);
+    if (ok && w.E > kWSortCap) ok = warp_panel_span<tm>(w, [&](uint32_t i) { return ci[w.e0 + i]; });
     if (lane == 0) {
       listed[p] = ok ? 0 : 1;
       if (!ok) list[atomicAdd(nlist, 1u)] = (uint32_t)p;
