@@ -106,7 +106,7 @@ def ncu_traffic(kernel: str, workload_tag: str):
     try:
         d = json.load(open(path))
         e = d.get(kernel, {})
-        if e.get("workload") == workload_tag:
+        if str(e.get("workload", "")).split("_")[0] == workload_tag:  # (summaries may tag "c2a_tm64")
             return e.get("dram_bytes_per_launch")
     except Exception:
         pass
