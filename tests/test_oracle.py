@@ -273,6 +273,101 @@ def test_checker_catches_corruption():
     assert oracle.hrpb_check(h, 7)[0] != 0          # conservation: sum popcount = nnz
 
 
+# One corruption per O6 return code, each asserting THAT code (oracle.c O6, codes 1-23). The fixture is
+# hand-made so every corruption trips exactly the rule it targets (earlier rules stay satisfied).
+def _o6_fixture():
+    ents = [(0, 0, 1.0), (1, 1, 2.0), (2, 2, 3.0), (3, 3, 4.0)]          # panel 0, brick col 0: 4 bits
+    ents += [(c % 16, c, float(c)) for c in range(4, 20)]                 # panel 0: 20 active cols, 2 blocks
+    ents += [(16, 3, 1.0), (17, 5, 2.0), (20, 9, 3.0), (25, 21, 4.0), (31, 39, 5.0)]  # panel 1: 5 cols
+    ents += [(32, 0, 1.0), (35, 7, 2.0), (39, 12, 3.0)]                   # panel 2 (ragged, rows 32..39)
+    rp, ci, v = to_csr(40, ents)
+    return oracle.csr_to_hrpb(40, 40, rp, ci, v), int(ci.shape[0])
+
+
+def _blk(h, b):
+    """byte offsets of block b's fields (HRPB-v1, TK = 16): colPtr, rows, patterns, values, end."""
+    s = int(h.sizePtr[b])
+    nbr = int(h.packedBlocks[s + 4])
+    hdr = -(-(5 + nbr) // 8) * 8
+    return {"colPtr": s, "rows": s + 5, "pat": s + hdr, "vals": s + hdr + 8 * nbr, "end": int(h.sizePtr[b + 1]),
+            "nbr": nbr}
+
+
+def _set_bit(h, off, bit, on=True):
+    p = int(np.frombuffer(h.packedBlocks[off:off + 8].tobytes(), "<u8")[0])
+    p = p | (1 << bit) if on else p & ~(1 << bit)
+    h.packedBlocks[off:off + 8] = np.frombuffer(np.array([p], "<u8").tobytes(), np.uint8)
+
+
+def _o6_cases():
+    import copy
+    h0, nnz = _o6_fixture()
+    K = h0.K
+    assert h0.blockedRowPtr.tolist() == [0, 2, 3, 4] and oracle.hrpb_check(h0, nnz) == (0, "")
+    b0, b2, b3 = _blk(h0, 0), _blk(h0, 2), _blk(h0, 3)
+
+    def mod(fn):
+        g = copy.deepcopy(h0)
+        fn(g)
+        return g
+    pk = lambda g: g.packedBlocks
+    yield 1, mod(lambda g: setattr(g, "tm", 8)), nnz
+    yield 2, mod(lambda g: g.blockedRowPtr.__setitem__(0, 1)), nnz
+    yield 3, mod(lambda g: g.blockedRowPtr.__setitem__(1, 4)), nnz
+    yield 4, mod(lambda g: g.sizePtr.__setitem__(0, 16)), nnz
+    yield 5, mod(lambda g: g.sizePtr.__setitem__(1, 0)), nnz
+    yield 6, mod(lambda g: g.sizePtr.__setitem__(1, g.sizePtr[1] + 8)), nnz
+    yield 7, mod(lambda g: g.activeCols.__setitem__(2 * 16, K)), nnz           # sentinel, then a real column
+    yield 8, mod(lambda g: g.activeCols.__setitem__(2 * 16, K + 5)), nnz       # column > K
+    yield 9, mod(lambda g: g.activeCols.__setitem__(slice(0, 2), g.activeCols[[1, 0]])), nnz
+    yield 10, mod(lambda g: g.activeCols.__setitem__(15, K)), nnz              # sentinel in a non-last block
+    yield 11, mod(lambda g: pk(g).__setitem__(b0["colPtr"], 1)), nnz
+    yield 12, mod(lambda g: pk(g).__setitem__(b0["colPtr"] + 1, 3)), nnz
+    yield 13, mod(lambda g: pk(g).__setitem__(b0["rows"], 1)), nnz            # brick row >= TM/16
+    yield 15, mod(lambda g: pk(g).__setitem__(slice(b0["pat"], b0["pat"] + 8), 0)), nnz
+    yield 16, mod(lambda g: _set_bit(g, b2["pat"] + 8, 1)), nnz                # brick col 1, lc 1 is a sentinel
+    yield 17, mod(lambda g: _set_bit(g, b3["pat"], 60)), nnz                   # row 32 + 15 >= M = 40
+    yield 18, mod(lambda g: _set_bit(g, b0["pat"], 0, on=False)), nnz - 1      # full brick, popcount 3 (P:L522)
+    yield 19, mod(lambda g: g.sizePtr.__setitem__(4, g.sizePtr[4] + 16)), nnz
+    yield 20, mod(lambda g: pk(g).__setitem__(b3["rows"] + 2, 7)), nnz          # header pad (nbr = 1)
+    yield 21, mod(lambda g: pk(g).__setitem__(b3["end"] - 1, 7)), nnz           # tail pad
+    yield 23, h0, nnz + 1                                                      # conservation
+    # 14: rows not increasing inside a brick column (TM = 32: two brick rows)
+    rp, ci, v = to_csr(40, [(0, 1, 1.0), (1, 2, 2.0), (3, 3, 3.0), (5, 9, 1.0), (17, 2, 4.0), (33, 7, 1.0)])
+    h32 = oracle.csr_to_hrpb(40, 12, rp, ci, v, tm=32)
+    assert oracle.hrpb_check(h32, 6) == (0, "")
+    r = _blk(h32, 0)["rows"]
+    assert h32.packedBlocks[r:r + 2].tolist() == [0, 1]
+    g = copy.deepcopy(h32); g.packedBlocks[r + 1] = 0
+    yield 14, g, 6
+    # 22: a panel whose last block holds no real column (an empty block appended to a full one)
+    rp, ci, v = to_csr(16, [(i, i, 1.0) for i in range(16)])
+    h16 = oracle.csr_to_hrpb(16, 16, rp, ci, v)
+    s = int(h16.sizePtr[1])
+    g = oracle.Hrpb(16, 16, 16, 16, np.array([0, 2], np.uint32),
+                    np.concatenate([h16.activeCols, np.full(16, 16, np.uint32)]),
+                    np.array([0, s, s + 16], np.uint64), np.concatenate([h16.packedBlocks, np.zeros(16, np.uint8)]))
+    yield 22, g, 16
+
+
+def test_checker_every_code():
+    got = {}
+    for code, g, nnz in _o6_cases():
+        c, msg = oracle.hrpb_check(g, nnz)
+        assert c == code, (code, c, msg)
+        got[code] = msg
+    assert sorted(got) == list(range(1, 24))
+
+
+def test_csr_validate_every_code():
+    rp, ci, v = to_csr(3, [(0, 1, 1.0), (0, 3, 1.0), (2, 0, 1.0)])
+    bad = rp.copy(); bad[0] = 1
+    assert oracle.csr_validate(3, 4, bad, ci) == 1                               # row_ptr[0] != 0
+    assert oracle.csr_validate(3, 4, rp, np.append(ci, 0).astype(np.int32)) == 3  # row_ptr[M] != nnz
+    bad = ci.copy(); bad[2] = -1
+    assert oracle.csr_validate(3, 4, rp, bad) == 4                               # negative column
+
+
 def test_popcount_floor_tm16():
     # P:L522: with TM = brick_m each real column of a brick has >= 1 nnz -> popcount >= 4
     w = synth.make("c2a", scale=8)
