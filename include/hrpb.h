@@ -38,9 +38,15 @@ typedef enum {
 } hrpb_status_t;
 
 /* Tile parameters ("TM either 16 or 32", "TK is set to 16"). The hot path is
- * tm = 16, tk = 16. NULL config => {16, 16}. */
+ * tm = 16, tk = 16. NULL config => {16, 16}.
+ * Supported (tm, tk): tm in {16, 32, 64, 128} with tk = 16; tm in {16, 32, 64} with tk = 32 (NEXT-1: taller panels
+ * share gathered B rows between more output rows). Anything else => HRPB_ERROR_INVALID_VALUE, in every
+ * entry point, before any work.
+ * tm = 0 (automatic): the library samples the CSR on the device (one small kernel and one stream synchronization)
+ * and picks tm in {16, 64} from the blocks a sample of 64-row groups forms at each height (DESIGN.md NEXT-1). In
+ * hrpb_build_spmm / _async the choice is made on the first call of an argument set and kept for its replays. */
 typedef struct {
-  int32_t tm; /* rows per panel: 16 */
+  int32_t tm; /* rows per panel: 16 (0 = automatic) */
   int32_t tk; /* compacted columns per block: 16 */
 } hrpb_config_t;
 
@@ -67,7 +73,7 @@ typedef struct {
  *   row_ptr   : device int64 [M+1], row_ptr[0] = 0, non-decreasing, row_ptr[M] = nnz.
  *   col_idx   : device int32 [nnz], 0 <= col < K, strictly increasing within a row.
  *   values    : device float [nnz] (bits copied verbatim; explicit zeros are structural, R11).
- *   cfg       : NULL or {16, 16}.
+ *   cfg       : NULL ({16, 16}) or a supported (tm, tk) pair, tm = 0 for the automatic choice (see hrpb_config_t).
  *   stream    : all work is enqueued on it; the call synchronizes it once at the end to read
  *               back sizes and the validation status, so the CSR buffers may be freed on return.
  *   out       : receives the handle (set to NULL on any error).
@@ -92,7 +98,9 @@ hrpb_status_t hrpb_build(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
  * kernel adds them in CTA order: results are deterministic for a given (handle, N), but the bits of a split
  * panel's rows may differ between launch configurations (e.g. the chunked launches of hrpb_build_spmm_host).
  * Scratch (the split-panel workspace, a padded copy of B when its rows are not 16-B aligned) is allocated per
- * call, stream-ordered. Asynchronous on `stream`; no host synchronization.
+ * call, stream-ordered (so concurrent calls on different streams never share it). Asynchronous on `stream`; no
+ * host synchronization. A call on a stream other than the build stream is recorded on the handle so that
+ * hrpb_free orders the release after it.
  */
 hrpb_status_t hrpb_spmm(const hrpb_t A, const float* B, float* C, int64_t M, int64_t K, int64_t N,
                         hrpb_stream_t stream);
@@ -130,7 +138,8 @@ hrpb_status_t hrpb_build_spmm_async(int64_t M, int64_t K, int64_t N, int64_t nnz
 
 /*
  * hrpb_sync_status — synchronizes `stream`; returns INVALID_CSR if any asynchronous replay since the previous
- * call found an invalid CSR (then clears that state; the state is per device), else HRPB_SUCCESS.
+ * call found an invalid CSR (then clears that state; the state is per device and read-and-cleared in one device
+ * atomic, so a replay on another stream can never have its report erased), else HRPB_SUCCESS.
  *   phase_ms : NULL or float[2] receiving the build and SpMM phase times of this thread's most recent
  *              hrpb_build_spmm / hrpb_build_spmm_async call (CUDA events on its stream).
  */
@@ -149,7 +158,9 @@ hrpb_status_t hrpb_build_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz,
                                    const int32_t* col_idx_h, const float* values_h, const float* B_h, float* C_h,
                                    const hrpb_config_t* cfg, hrpb_stream_t stream);
 
-/* Releases the handle's device memory (stream-ordered on the build stream). NULL is a no-op. */
+/* Releases the handle's device memory, stream-ordered on the build stream after every hrpb_spmm recorded on
+ * other streams (event waits; more than 8 distinct streams: a device synchronization). Returns without waiting.
+ * NULL is a no-op. */
 hrpb_status_t hrpb_free(hrpb_t A);
 
 /* Fills *view with the handle's metadata and device pointers. */

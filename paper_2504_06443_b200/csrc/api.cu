@@ -25,17 +25,42 @@ hrpb_status_t cuda_status(cudaError_t e) {
   return HRPB_ERROR_CUDA;
 }
 
+bool first_on_device(std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return true;
+  const uint64_t bit = 1ull << dev;
+  return (done.fetch_or(bit) & bit) == 0;
+}
+
 static void keep_pool_memory() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;  // keep freed blocks cached in the stream-ordered pool
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  static std::atomic<uint64_t> done{0};
+  if (!first_on_device(done)) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;  // keep freed blocks cached in the stream-ordered pool
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
+static std::mutex g_use_mu;
+
+void note_use(hrpb_handle* h, cudaStream_t s) {
+  if (!h || s == h->stream) return;
+  std::lock_guard<std::mutex> lk(g_use_mu);
+  int i = 0;
+  while (i < h->n_use && h->use_st[i] != s) ++i;
+  if (i == h->n_use) {
+    if (i == hrpb_handle::kMaxUse || cudaEventCreateWithFlags(&h->use_ev[i], cudaEventDisableTiming) != cudaSuccess) {
+      h->use_overflow = true;
+      return;
     }
-  });
+    h->use_st[i] = s;
+    ++h->n_use;
+  }
+  cudaEventRecord(h->use_ev[i], s);
 }
 
 void* dalloc(size_t bytes, cudaStream_t s) {
@@ -76,11 +101,33 @@ static hrpb_status_t check_device() {
 static void release(hrpb_handle* h) {
   if (!h) return;
   cudaStream_t s = h->stream;
+  {
+    std::lock_guard<std::mutex> lk(g_use_mu);
+    // SpMMs on other streams may still read the arrays: order the frees after them
+    if (h->use_overflow) cudaDeviceSynchronize();
+    for (int i = 0; i < h->n_use; ++i) {
+      cudaStreamWaitEvent(s, h->use_ev[i], 0);
+      cudaEventDestroy(h->use_ev[i]);
+    }
+    h->n_use = 0;
+  }
   dfree(h->brp, s);
   dfree(h->ac, s);
   dfree(h->sp, s);
   dfree(h->packed, s);
   delete h;
+}
+
+static bool valid_tile(int32_t tm, int32_t tk) { return tm == 0 ? (tk == 16 || tk == 32) : tile_supported(tm, tk); }
+
+// tm == 0: automatic choice (choose_tm) for the CSR on the device
+static hrpb_status_t resolve_tm(int64_t M, int64_t K, int64_t nnz, const int64_t* rp, const int32_t* ci, int32_t tm,
+                                int32_t tk, cudaStream_t s, int32_t* out) {
+  *out = tm;
+  if (tm != 0) return HRPB_SUCCESS;
+  hrpb_status_t st = choose_tm(M, K, nnz, rp, ci, s, out, nullptr);
+  if (st == HRPB_SUCCESS && tk == 32 && *out > 64) *out = 64;
+  return st;
 }
 
 }  // namespace hrpb
@@ -95,13 +142,15 @@ hrpb_status_t hrpb_build(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   *out = nullptr;
   if (M < 0 || K < 0 || nnz < 0 || M >= (1ll << 31) || K >= (1ll << 31) || !row_ptr) return HRPB_ERROR_INVALID_VALUE;
   if (nnz > 0 && (!col_idx || !values)) return HRPB_ERROR_INVALID_VALUE;
-  const int32_t tm = cfg ? cfg->tm : 16, tk = cfg ? cfg->tk : 16;
-  if (!(tm == 16 || tm == 32 || tm == 64 || tm == 128) || !(tk == 16 || tk == 32)) return HRPB_ERROR_INVALID_VALUE;
+  const int32_t tm_req = cfg ? cfg->tm : 16, tk = cfg ? cfg->tk : 16;
+  if (!valid_tile(tm_req, tk)) return HRPB_ERROR_INVALID_VALUE;
   hrpb_status_t st = check_device();
   if (st != HRPB_SUCCESS) return st;
-  hrpb_handle* h = new (std::nothrow) hrpb_handle;
+  int32_t tm = tm_req;
+  st = resolve_tm(M, K, nnz, row_ptr, col_idx, tm_req, tk, (cudaStream_t)stream, &tm);
+  if (st != HRPB_SUCCESS) return st;
+  hrpb_handle* h = new (std::nothrow) hrpb_handle();
   if (!h) return HRPB_ERROR_OUT_OF_MEMORY;
-  std::memset(h, 0, sizeof(*h));
   st = build_impl(M, K, nnz, row_ptr, col_idx, values, tm, tk, (cudaStream_t)stream, h);
   if (st != HRPB_SUCCESS) {
     release(h);
@@ -119,7 +168,8 @@ namespace {
 struct BuildSpmmPlan {
   int64_t M = -1, K = -1, N = -1, nnz = -1;
   const void *rp = nullptr, *ci = nullptr, *va = nullptr, *B = nullptr, *C = nullptr;
-  int32_t tm = 0, tk = 0;
+  int32_t tm = -1, tk = 0;  // tm as requested (0 = automatic)
+  int32_t tm_res = 0;       // automatic TM resolved on the first call of this key (a planning decision, like the graph)
   cudaStream_t s = nullptr;
   int dev = -1;
   int hits = 0;
@@ -155,9 +205,22 @@ static hrpb_status_t enqueue_build_spmm(int64_t M, int64_t K, int64_t N, int64_t
   return st;
 }
 
-// pinned read-back buffer, phase events and the replay plan: one set per host thread
+// pinned read-back buffer, phase events (per device: an event records only on streams of its own device) and the
+// replay plan: one set per host thread
 static thread_local uint64_t* t_info = nullptr;
-static thread_local cudaEvent_t t_ev[3] = {nullptr, nullptr, nullptr};
+static thread_local cudaEvent_t t_ev_dev[64][3];
+static thread_local cudaEvent_t* t_ev = nullptr;  // the events of this thread's most recent build_spmm call
+
+static cudaEvent_t* device_events() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  cudaEvent_t* ev = t_ev_dev[dev];
+  if (!ev[0])
+    for (int i = 0; i < 3; ++i)
+      if (cudaEventCreate(&ev[i]) != cudaSuccess) return nullptr;
+  return ev;
+}
 
 static hrpb_status_t build_spmm_common(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr,
                                        const int32_t* col_idx, const float* values, const float* B, float* C,
@@ -168,8 +231,8 @@ static hrpb_status_t build_spmm_common(int64_t M, int64_t K, int64_t N, int64_t 
     return HRPB_ERROR_INVALID_VALUE;
   if ((nnz > 0 && (!col_idx || !values)) || (M > 0 && N > 0 && !C) || (K > 0 && N > 0 && !B))
     return HRPB_ERROR_INVALID_VALUE;
-  const int32_t tm = cfg ? cfg->tm : 16, tk = cfg ? cfg->tk : 16;
-  if (!(tm == 16 || tm == 32 || tm == 64 || tm == 128) || !(tk == 16 || tk == 32)) return HRPB_ERROR_INVALID_VALUE;
+  const int32_t tm_req = cfg ? cfg->tm : 16, tk = cfg ? cfg->tk : 16;
+  if (!valid_tile(tm_req, tk)) return HRPB_ERROR_INVALID_VALUE;
   hrpb_status_t st = check_device();
   if (st != HRPB_SUCCESS) return st;
   cudaStream_t s = (cudaStream_t)stream;
@@ -177,20 +240,26 @@ static hrpb_status_t build_spmm_common(int64_t M, int64_t K, int64_t N, int64_t 
   cudaGetDevice(&dev);
   static thread_local BuildSpmmPlan plan;
   static thread_local hrpb_handle plan_h;
-  if (!t_info) {
-    if (cudaMallocHost(&t_info, 4 * sizeof(uint64_t)) != cudaSuccess) return HRPB_ERROR_OUT_OF_MEMORY;
-    for (auto& e : t_ev) cudaEventCreate(&e);
-  }
+  if (!t_info && cudaMallocHost(&t_info, 4 * sizeof(uint64_t)) != cudaSuccess) return HRPB_ERROR_OUT_OF_MEMORY;
+  cudaEvent_t* ev = device_events();
+  if (!ev) return HRPB_ERROR_CUDA;
+  t_ev = ev;
   uint64_t* info = t_info;
-  cudaEvent_t* ev = t_ev;
   static const bool use_graph = [] {
     const char* e = getenv("HRPB_NO_GRAPH");  // debugging aid: always run eagerly
     return !(e && atoi(e));
   }();
-  const bool same = plan.same(M, K, N, nnz, row_ptr, col_idx, values, B, C, tm, tk, s, dev);
+  const bool same = plan.same(M, K, N, nnz, row_ptr, col_idx, values, B, C, tm_req, tk, s, dev);
+  int32_t tm = tm_req;
+  if (same && tm_req == 0 && plan.tm_res > 0) {
+    tm = plan.tm_res;
+  } else {
+    st = resolve_tm(M, K, nnz, row_ptr, col_idx, tm_req, tk, s, &tm);
+    if (st != HRPB_SUCCESS) return st;
+  }
   if (!out && use_graph && same && plan.hits >= 1) {
     if (!plan.exec) {  // capture the enqueue sequence once
-      std::memset(&plan_h, 0, sizeof(plan_h));
+      plan_h = hrpb_handle();
       const int64_t l0 = g_launches.load();
       cudaGraph_t g = nullptr;
       cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
@@ -216,8 +285,7 @@ static hrpb_status_t build_spmm_common(int64_t M, int64_t K, int64_t N, int64_t 
       if (async) return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);  // status: hrpb_sync_status
       if (e == cudaSuccess) e = cudaStreamSynchronize(s);
       if (e != cudaSuccess) return cuda_status(e);
-      hrpb_handle tmp;
-      std::memset(&tmp, 0, sizeof(tmp));
+      hrpb_handle tmp = hrpb_handle();
       st = build_finish(&tmp, info, HRPB_SUCCESS);
       if (st == HRPB_ERROR_INVALID_CSR) sticky_take(s);  // reported here: not again by hrpb_sync_status
       if (phase_ms && st == HRPB_SUCCESS) {
@@ -231,12 +299,12 @@ static hrpb_status_t build_spmm_common(int64_t M, int64_t K, int64_t N, int64_t 
     if (plan.exec) cudaGraphExecDestroy(plan.exec);
     plan = BuildSpmmPlan();
     plan.M = M; plan.K = K; plan.N = N; plan.nnz = nnz; plan.rp = row_ptr; plan.ci = col_idx; plan.va = values;
-    plan.B = B; plan.C = C; plan.tm = tm; plan.tk = tk; plan.s = s; plan.dev = dev;
+    plan.B = B; plan.C = C; plan.tm = tm_req; plan.tk = tk; plan.s = s; plan.dev = dev;
+    plan.tm_res = tm;
   }
   ++plan.hits;
-  hrpb_handle* h = new (std::nothrow) hrpb_handle;
+  hrpb_handle* h = new (std::nothrow) hrpb_handle();
   if (!h) return HRPB_ERROR_OUT_OF_MEMORY;
-  std::memset(h, 0, sizeof(*h));
   st = enqueue_build_spmm(M, K, N, nnz, row_ptr, col_idx, values, B, C, tm, tk, s, h, info, ev, false, false);
   const cudaError_t e = cudaStreamSynchronize(s);
   if (st == HRPB_SUCCESS && e != cudaSuccess) st = cuda_status(e);
@@ -269,7 +337,7 @@ hrpb_status_t hrpb_sync_status(hrpb_stream_t stream, float* phase_ms) {
   hrpb_status_t st = check_device();
   if (st != HRPB_SUCCESS) return st;
   st = sticky_take((cudaStream_t)stream);
-  if (phase_ms && st == HRPB_SUCCESS && t_ev[0]) {
+  if (phase_ms && st == HRPB_SUCCESS && t_ev) {
     cudaEventElapsedTime(&phase_ms[0], t_ev[0], t_ev[1]);
     cudaEventElapsedTime(&phase_ms[1], t_ev[1], t_ev[2]);
   }
@@ -283,7 +351,9 @@ hrpb_status_t hrpb_spmm(const hrpb_t A, const float* B, float* C, int64_t M, int
   if (N == 0 || M == 0) return HRPB_SUCCESS;
   if (!C || (!B && K > 0)) return HRPB_ERROR_INVALID_VALUE;
   if (N >= (1ll << 31)) return HRPB_ERROR_INVALID_VALUE;
-  return spmm_impl(A, B, N, C, N, (cudaStream_t)stream);
+  const hrpb_status_t st = spmm_impl(A, B, N, C, N, (cudaStream_t)stream);
+  if (st == HRPB_SUCCESS) note_use(A, (cudaStream_t)stream);
+  return st;
 }
 
 hrpb_status_t hrpb_build_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr_h,
@@ -292,18 +362,30 @@ hrpb_status_t hrpb_build_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz,
   if (M < 0 || K < 0 || N < 0 || nnz < 0 || !row_ptr_h || (nnz > 0 && (!col_idx_h || !values_h)) ||
       (M > 0 && N > 0 && !C_h) || (K > 0 && N > 0 && !B_h))
     return HRPB_ERROR_INVALID_VALUE;
+  if (M >= (1ll << 31) || K >= (1ll << 31) || N >= (1ll << 31)) return HRPB_ERROR_INVALID_VALUE;
+  if (!valid_tile(cfg ? cfg->tm : 16, cfg ? cfg->tk : 16)) return HRPB_ERROR_INVALID_VALUE;
   hrpb_status_t st = check_device();
   if (st != HRPB_SUCCESS) return st;
   cudaStream_t s = (cudaStream_t)stream;
   // Pipeline: copy engine H2D: CSR, then B in row chunks; the build runs as soon as the CSR is in;
   // C is produced in panel chunks, chunk c starting once the B rows up to its largest active column have
   // arrived; its rows go back D2H on a third stream while later B chunks still stream in (PCIe is full duplex).
-  static cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking);
-  });
+  // library copy streams, one pair per device (a stream belongs to the device current at its creation)
+  static cudaStream_t s_h2d_dev[64], s_d2h_dev[64];
+  static std::mutex s_mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return HRPB_ERROR_NOT_SUPPORTED;
+  cudaStream_t s_h2d, s_d2h;
+  {
+    std::lock_guard<std::mutex> lk(s_mu);
+    if (!s_h2d_dev[dev]) {
+      cudaStreamCreateWithFlags(&s_h2d_dev[dev], cudaStreamNonBlocking);
+      cudaStreamCreateWithFlags(&s_d2h_dev[dev], cudaStreamNonBlocking);
+    }
+    s_h2d = s_h2d_dev[dev];
+    s_d2h = s_d2h_dev[dev];
+  }
 #ifndef HRPB_E2E_BCH
 #define HRPB_E2E_BCH 32
 #define HRPB_E2E_CCH 16

@@ -18,6 +18,8 @@
 // first entry offset, base(p) = floor(e0 * nbk / tk) + 2 p nbk, which never overlaps the next panel's.
 #include <cstdio>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -1665,12 +1667,14 @@ __global__ void k_finalize(const int64_t* __restrict__ rp, int64_t M, int64_t nn
 
 template <int TM, int TK>
 static int wbuild_ctas() {  // resident CTAs of k_wbuild per SM (the ticket loop is persistent)
-  static int n = 0;
-  if (!n) {
+  static std::atomic<uint64_t> done{0};  // the shared-memory attribute is per device
+  static std::atomic<int> n{0};
+  if (first_on_device(done)) {
     const size_t smem = (size_t)warp_layout(TM, TK).bytes * kWWarps;
     cudaFuncSetAttribute(k_wbuild<TM, TK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_wbuild<TM, TK>, 32 * kWWarps, smem);
-    if (n < 1) n = 1;
+    int m = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k_wbuild<TM, TK>, 32 * kWWarps, smem);
+    n = m < 1 ? 1 : m;
   }
   return n;
 }
@@ -1753,11 +1757,8 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     cudaMemsetAsync(ctr, 0, 8 * sizeof(uint32_t), s);
     const size_t count_smem =
         (size_t)kSmallCap * (8 + 4 + 4 + 1) + (size_t)ceil_div(kSmallCap, tk) * nbk * sizeof(uint64_t);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};  // per device
+    if (first_on_device(attr)) cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const unsigned wgrid = (unsigned)ceil_div(P, kWWarps);
     const int mid_ctas = 8 * num_sms();
     cudaMemsetAsync(lb, 0, (P + 1) * sizeof(uint64_t), s);
@@ -1816,15 +1817,145 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   return build_finish(h, hinfo, st);
 }
 
+// read-and-clear of the sticky status word in one atomic (a replay on another stream that ORs its status in
+// between a separate read and clear would otherwise be lost)
+__global__ void k_sticky_take(unsigned int* sticky, unsigned int* out) { *out = atomicExch(sticky, 0u); }
+
 hrpb_status_t sticky_take(cudaStream_t s) {
   unsigned int* addr = nullptr;
   cudaError_t e = cudaGetSymbolAddress(reinterpret_cast<void**>(&addr), g_sticky_status);
+  unsigned int* word = (unsigned int*)dalloc(sizeof(unsigned int), s);
+  if (!word) return HRPB_ERROR_OUT_OF_MEMORY;
   unsigned int v = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&v, addr, sizeof(v), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) {
+    k_sticky_take<<<1, 1, 0, s>>>(addr, word);
+    note_launch();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&v, word, sizeof(v), cudaMemcpyDeviceToHost, s);
+  dfree(word, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e == cudaSuccess && v) e = cudaMemsetAsync(addr, 0, sizeof(v), s);
   if (e != cudaSuccess) return cuda_status(e);
   return v ? HRPB_ERROR_INVALID_CSR : HRPB_SUCCESS;
+}
+
+// ------------------------------------------------------------------ automatic TM (hrpb_config_t.tm = 0)
+// NEXT-1 ("TM either 16 or 32"; the beta reuse of P:L329-357): taller panels share gathered B rows between
+// more output rows but multiply zero-filled brick rows. The choice is made from B1 statistics of a sample: up to
+// kProbeSamples evenly spaced 64-row groups, each ranked as one TM = 64 panel and as four TM = 16 panels
+// (CTA radix sort of (column, sub-panel) keys, distinct columns counted per sub-panel and overall). Groups with
+// more than kProbeCap entries count as TM-neutral (their blocks at either TM ~ entries / TK).
+constexpr int kProbeThreads = 256, kProbeItems = 8, kProbeCap = kProbeThreads * kProbeItems;
+constexpr int64_t kProbeSamples = 1024;
+
+__global__ void __launch_bounds__(kProbeThreads) k_tm_probe(const int64_t* __restrict__ rp,
+                                                            const int32_t* __restrict__ ci, int64_t M, int64_t nnz,
+                                                            int64_t groups, int64_t samples, int key_bits,
+                                                            unsigned long long* __restrict__ acc) {
+  pdl_wait();
+  using Sort = cub::BlockRadixSort<unsigned long long, kProbeThreads, kProbeItems>;
+  __shared__ typename Sort::TempStorage tmp;
+  __shared__ unsigned long long s_keys[kProbeCap];
+  __shared__ int64_t s_rp[65];
+  __shared__ uint32_t s_cnt[5];  // distinct columns of the 64-row group, then of each 16-row sub-panel
+  for (int64_t i = blockIdx.x; i < samples; i += gridDim.x) {
+    const int64_t g = i * groups / samples;
+    const int64_t r0 = g * 64;
+    const int nrows = (int)min((int64_t)64, M - r0);
+    __syncthreads();
+    if (threadIdx.x <= nrows) {
+      const int64_t v = rp[r0 + threadIdx.x];
+      s_rp[threadIdx.x] = v < 0 ? 0 : (v > nnz ? nnz : v);
+    }
+    if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    const int64_t e0 = s_rp[0];
+    const int64_t E = s_rp[nrows] - e0;
+    if (E <= 0) continue;  // (CTA-uniform)
+    const int nsub = (nrows + 15) / 16;
+    if (E > kProbeCap) {
+      if (threadIdx.x == 0) {
+        const unsigned long long nb = (unsigned long long)((E + 15) / 16);
+        atomicAdd(&acc[0], nb);
+        atomicAdd(&acc[1], nb);
+        atomicAdd(&acc[2], (unsigned long long)nsub);
+      }
+      continue;
+    }
+    unsigned long long key[kProbeItems];
+#pragma unroll
+    for (int k = 0; k < kProbeItems; ++k) {
+      const int idx = threadIdx.x * kProbeItems + k;
+      key[k] = ~0ull;
+      if (idx < E) {
+        int lo = 0, hi = nrows - 1;  // local row of entry idx
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_rp[mid] - e0 <= idx) lo = mid; else hi = mid - 1;
+        }
+        const int32_t c = ci[e0 + idx];
+        key[k] = ((unsigned long long)(uint32_t)max(c, 0) << 2) | (unsigned long long)(lo >> 4);
+      }
+    }
+    Sort(tmp).Sort(key, 0, key_bits);
+#pragma unroll
+    for (int k = 0; k < kProbeItems; ++k) s_keys[threadIdx.x * kProbeItems + k] = key[k];
+    __syncthreads();
+    uint32_t n64 = 0, n16[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < kProbeItems; ++k) {
+      const int idx = threadIdx.x * kProbeItems + k;
+      if (idx >= E) continue;
+      const unsigned long long cur = key[k], prev = idx ? s_keys[idx - 1] : ~0ull;
+      if (idx == 0 || (cur >> 2) != (prev >> 2)) ++n64;
+      if (idx == 0 || cur != prev) ++n16[cur & 3];
+    }
+    if (n64) atomicAdd(&s_cnt[0], n64);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (n16[k]) atomicAdd(&s_cnt[1 + k], n16[k]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long nb16 = 0;
+      for (int k = 0; k < 4; ++k) nb16 += (s_cnt[1 + k] + 15) / 16;
+      atomicAdd(&acc[0], nb16);
+      atomicAdd(&acc[1], (unsigned long long)((s_cnt[0] + 15) / 16));
+      atomicAdd(&acc[2], (unsigned long long)nsub);
+    }
+  }
+}
+
+hrpb_status_t choose_tm(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                        cudaStream_t s, int32_t* tm_out, uint64_t* stats) {
+  *tm_out = 16;
+  const int64_t groups = ceil_div(M, 64);
+  if (groups == 0 || nnz == 0) return HRPB_SUCCESS;
+  unsigned long long* acc = (unsigned long long*)dalloc(4 * sizeof(unsigned long long), s);
+  if (!acc) return HRPB_ERROR_OUT_OF_MEMORY;
+  unsigned long long h[4] = {0, 0, 0, 0};
+  cudaError_t e = cudaMemsetAsync(acc, 0, 4 * sizeof(unsigned long long), s);
+  const int64_t samples = groups < kProbeSamples ? groups : kProbeSamples;
+  int kb = 2;
+  while (kb < 64 && (1ll << (kb - 2)) < K) ++kb;
+  if (e == cudaSuccess) {
+    const unsigned grid = (unsigned)(samples < 2 * num_sms() ? samples : 2 * num_sms());
+    e = launch_pdl(k_tm_probe, grid, kProbeThreads, 0, s, row_ptr, col_idx, M, nnz, groups, samples, kb, acc);
+    note_launch();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, s);
+  dfree(acc, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (stats) { stats[0] = h[0]; stats[1] = h[1]; stats[2] = h[2]; }
+  // Measured on B200 (profiles/r01/configs.md, DESIGN.md NEXT-1): the SpMM is bound by per-block work at both TM
+  // (a TM = 64 block costs ~1.5x a TM = 16 block), so TM = 64 pays when it cuts the blocks to < 2/3 (c2a: 0.40),
+  // or when TM = 16 panels hold about one block each, whose per-panel epilogue then dominates (c2b: 1.0 block per
+  // panel, 0.99 of the blocks). Otherwise (c1, c3, c4, c5: 0.68-1.0 of the blocks, 7-28 blocks per panel) TM = 16.
+  if (h[0] > 0) {
+    const double r = (double)h[1] / (double)h[0], bpp = (double)h[0] / (double)(h[2] ? h[2] : 1);
+    if (r < 0.67 || (bpp <= 1.5 && r <= 1.05)) *tm_out = 64;
+  }
+  return HRPB_SUCCESS;
 }
 
 hrpb_status_t build_finish(hrpb_handle* h, const uint64_t* info, hrpb_status_t st) {

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/hrpb.h"
 
 struct hrpb_handle {
@@ -13,6 +15,14 @@ struct hrpb_handle {
   uint64_t* sp;     // [NB_cap + 1]
   uint8_t* packed;  // [bytes_cap]
   cudaStream_t stream;  // build stream (frees are ordered on it)
+  // streams other than `stream` that ran hrpb_spmm on this handle, with an event recorded after their latest
+  // use: hrpb_free makes the build stream wait on them before the stream-ordered frees (kMaxUse distinct streams;
+  // beyond that hrpb_free synchronizes the device)
+  static constexpr int kMaxUse = 8;
+  int n_use;
+  bool use_overflow;
+  cudaStream_t use_st[kMaxUse];
+  cudaEvent_t use_ev[kMaxUse];
 };
 
 namespace hrpb {
@@ -29,6 +39,10 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
                          const float* values, int32_t tm, int32_t tk, cudaStream_t s, hrpb_handle* h,
                          uint64_t* deferred_info = nullptr, bool sticky = false);
 hrpb_status_t build_finish(hrpb_handle* h, const uint64_t* info, hrpb_status_t st);
+// automatic TM (cfg->tm == 0): one sampling kernel over the CSR + a stream sync; *tm_out in {16, 64}; stats (if
+// not NULL) = {sampled blocks at TM = 16, at TM = 64, sampled 16-row panels}
+hrpb_status_t choose_tm(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                        cudaStream_t s, int32_t* tm_out, uint64_t* stats);
 // synchronizes s, returns INVALID_CSR if any sticky build (sticky = true above) flagged its input since the
 // last call, and clears the flag
 hrpb_status_t sticky_take(cudaStream_t s);
@@ -41,5 +55,17 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
 hrpb_status_t chunk_maxcol(const hrpb_handle* h, int64_t per, int nchunks, int* dev_out, cudaStream_t s);
 
 int num_sms();
+
+// per-device one-time initialisation (kernel attributes, pools): true the first time it is called for the current
+// device with this flag word (always true on device ids >= 64)
+bool first_on_device(std::atomic<uint64_t>& done);
+// records that `s` read the handle (hrpb_spmm on a stream other than the build stream)
+void note_use(hrpb_handle* h, cudaStream_t s);
+
+// (tm, tk) pairs the builder and the SpMM both implement: tm in {16, 32, 64, 128} with tk = 16, tm in {16, 32, 64}
+// with tk = 32 (the decoder's brick-slot table has one lane per brick: (tm / 16) (tk / 4) <= 32)
+inline bool tile_supported(int32_t tm, int32_t tk) {
+  return (tk == 16 && (tm == 16 || tm == 32 || tm == 64 || tm == 128)) || (tk == 32 && (tm == 16 || tm == 32 || tm == 64));
+}
 
 }  // namespace hrpb

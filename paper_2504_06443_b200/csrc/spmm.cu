@@ -43,7 +43,7 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
     cudaError_t e = cudaMemsetAsync(C + r0 * N, 0, (size_t)(r1 - r0) * N * sizeof(float), s);
     return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);
   }
-  if (!(h->tm == 16 || h->tm == 32 || h->tm == 64) || !(h->tk == 16 || h->tk == 32)) return HRPB_ERROR_NOT_SUPPORTED;
+  if (!tile_supported(h->tm, h->tk)) return HRPB_ERROR_NOT_SUPPORTED;
   EncodeTiledFn enc = get_encode();
   if (!enc) return HRPB_ERROR_NOT_SUPPORTED;
   // per-call scratch, stream-ordered on s (a handle may serve concurrent calls on different streams): the padded
@@ -60,13 +60,16 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
     Bt = bpad;
     ld = ldp;
   }
-  const size_t ws_bytes = (size_t)num_sms() * 2 * 64 * 512 * sizeof(float);  // grid x 2 tiles x TM x 128 NT
-  float* ws = (float*)dalloc(ws_bytes + 64, s);
+  // grid x 2 tiles x TM x (128 NT) partial tiles (TM * 128 NT <= 64 * 512 for every instantiated pair), the
+  // split flag, and the grid's S1 ranges
+  const size_t ws_bytes = (size_t)num_sms() * 2 * 64 * 512 * sizeof(float);
+  float* ws = (float*)dalloc(ws_bytes + 64 + (size_t)num_sms() * 4 * sizeof(uint64_t), s);
   if (!ws) {
     dfree(bpad, s);
     return HRPB_ERROR_OUT_OF_MEMORY;
   }
-  Scratch scr{ws, reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ws) + ws_bytes), next_epoch()};
+  uint64_t* flag = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ws) + ws_bytes);
+  Scratch scr{ws, flag, next_epoch(), flag + 8};
   CUtensorMap tm;
   cuuint64_t gdim[2] = {(cuuint64_t)N, (cuuint64_t)h->K};
   cuuint64_t gstr[1] = {(cuuint64_t)ld * 4};
@@ -76,15 +79,17 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return HRPB_ERROR_INVALID_VALUE;
-  const int64_t ncols = h->tk == 32 ? 256 : 512;  // columns per launch (NT <= 4, or <= 2 at TK = 32)
+  // columns per launch: NT <= 4, or <= 2 at TK = 32 (twice the stage size) and TM = 128 (two TMEM slots of
+  // 2 x 128 columns fill the 512 TMEM columns)
+  const int64_t ncols = (h->tk == 32 || h->tm == 128) ? 256 : 512;
   for (int64_t n0 = 0; n0 < N; n0 += ncols) {
     const int64_t w = N - n0 < ncols ? N - n0 : ncols;
     const int nt = (int)ceil_div(w, 128);
     hrpb_status_t st;
-    static const int gm = [] {
-      const char* e = getenv("HRPB_GATHER");  // 0 = TMA gather4 (TK = 16 only), 1 = cp.async (default)
-      return e ? atoi(e) : 1;
-    }();
+    // B-row staging (S3): 1 = cp.async 16-B copies (default), 0 = TMA tile::gather4 (TK = 16 only; slower on
+    // every config measured, kept selectable per call and parity-tested)
+    const char* genv = getenv("HRPB_GATHER");
+    const int gm = genv ? atoi(genv) : 1;
     if (h->tk == 16) st = spmm_dispatch<16>(h, tm, Bt, ld, C, N, (int)n0, nt, gm, p_lo, p_hi, scr, s);
     else st = spmm_dispatch<32>(h, tm, Bt, ld, C, N, (int)n0, nt, 1, p_lo, p_hi, scr, s);
     if (st != HRPB_SUCCESS) {

@@ -45,6 +45,7 @@ struct Scratch {
   float* ws;
   uint64_t* flag;
   uint64_t epoch;
+  uint64_t* ranges;  // [grid][4]: every CTA's S1 range (CtaWork), read by k_spmm_fixup
 };
 inline uint64_t next_epoch() {
   static std::atomic<uint64_t> e{0};
@@ -62,6 +63,7 @@ struct SpmmParams {
   float* ws;           // split-panel partial tiles [G][2][TM][128 NT]
   uint64_t* split_flag;  // set to `epoch` by any CTA that writes a partial tile (k_spmm_fixup runs only then)
   uint64_t epoch;
+  uint64_t* ranges;      // [G][4] CtaWork of every CTA: {pa, pb, bB | bE << 32, first_full | last_full << 1}
   const float* B;  // row-major K x ldb (cp.async gather mode)
   int64_t K, ldb;
   int n0;      // first output column of this launch
@@ -129,7 +131,7 @@ struct SmemLayout {
 
 // S1 work assignment. Work units: panel p owns units [brp[p] + w p, brp[p+1] + w (p + 1)), w = kPanelW — one per block plus w for
 // its epilogue (so empty panels cost one unit). CTA c of G takes units [t_c, t_c+1) with t_c = c W / G snapped up
-// to the next panel start unless the panel containing it is "big" (more than a whole CTA share): such a panel
+// to the next panel start unless the panel containing it is "big" (more than two whole CTA shares): such a panel
 // is split between CTAs, each accumulating its blocks into a workspace tile, and k_spmm_fixup adds the partial
 // tiles in CTA order (deterministic) into C.
 // kPanelW: units per panel epilogue per 16 panel rows (the C store of TM rows), 1 = one block's worth
@@ -153,16 +155,6 @@ __host__ __device__ constexpr uint64_t panel_weight() {
 template <uint64_t PW>
 __device__ __forceinline__ uint64_t unit_of(const uint32_t* brp, int64_t p) {  // units before panel p
   return (uint64_t)brp[p] + PW * (uint64_t)p;
-}
-template <uint64_t PW>
-__device__ __forceinline__ int64_t panel_of_unit(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t t) {
-  // first p in [lo, hi) with brp[p + 1] + p + 1 > t (hi if none); binary search (one thread)
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (unit_of<PW>(brp, mid + 1) > t) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo;
 }
 template <uint64_t PW>
 __device__ __forceinline__ int64_t warp_panel_of_unit(const uint32_t* brp, int64_t lo, int64_t hi, uint64_t t) {
@@ -210,7 +202,9 @@ __device__ __forceinline__ uint64_t work_boundary(const uint32_t* brp, int64_t p
   if (p >= p_hi) return base + W;
   const uint64_t start = unit_of<PW>(brp, p), end = unit_of<PW>(brp, p + 1);
   if (t == start) return t;
-  if ((end - start) * G > W) return t;  // big panel (more than a whole CTA share): split here
+  // big panel (more than two whole CTA shares): split here. (At one share, launches with about one panel per CTA
+  // split every larger-than-average panel, and the fix-up then costs more than the imbalance it removes.)
+  if ((end - start) * G > 2 * W) return t;
   pt = p + 1;                               // small panel: round up to the next panel start
   return end;
 }
@@ -255,12 +249,6 @@ __device__ __forceinline__ CtaWork cta_work(const uint32_t* brp, int64_t p_lo, i
   }
   return w;
 }
-template <uint64_t PW>
-struct SerialFind {
-  __device__ int64_t operator()(const uint32_t* b, int64_t lo, int64_t hi, uint64_t t) const {
-    return panel_of_unit<PW>(b, lo, hi, t);
-  }
-};
 template <uint64_t PW>
 struct WarpFind {
   __device__ int64_t operator()(const uint32_t* b, int64_t lo, int64_t hi, uint64_t t) const {
@@ -372,6 +360,11 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       range[0] = cw.pa; range[1] = cw.pb; range[2] = cw.bB; range[3] = cw.bE;
       range[4] = cw.first_full; range[5] = cw.last_full;
       if (cw.bB < cw.bE && !(cw.first_full && cw.last_full)) *prm.split_flag = prm.epoch;
+      uint64_t* rg = prm.ranges + 4 * blockIdx.x;  // (the fix-up reads the ranges instead of re-deriving them)
+      rg[0] = (uint64_t)cw.pa;
+      rg[1] = (uint64_t)cw.pb;
+      rg[2] = (uint64_t)cw.bB | ((uint64_t)cw.bE << 32);
+      rg[3] = (uint64_t)cw.first_full | ((uint64_t)cw.last_full << 1);
     }
   }
   tc_fence_before();
@@ -722,23 +715,27 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       mbar_wait_acc(prm, &tfull[slot], (pc / L::kSlots) & 1, wacc);
       if (et == 0) trace_ev(prm, 5, pc);
       tc_fence_after();
+      constexpr int kRows = TMV < 64 ? TMV : 64;  // rows per tcgen05.wait (TM = 128: two halves, 64 registers)
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        uint32_t v[TMV / 16][16];  // all panel rows of this lane's column: one tcgen05.wait per 128-column tile
 #pragma unroll
-        for (int c16 = 0; c16 < TMV / 16; ++c16)
-          tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + slot * NT * TMV + t * TMV + c16 * 16, v[c16]);
-        tmem_ld_wait();
-        const int64_t c = 128 * t + 32 * qd + lane;
-        if (c < ncols && !(dbg(prm, 1))) {
-          float* dst = obase + c;
-          if (nrows == TMV) {
+        for (int h0 = 0; h0 < TMV; h0 += kRows) {
+          uint32_t v[kRows / 16][16];  // panel rows [h0, h0 + kRows) of this lane's column
 #pragma unroll
-            for (int r = 0; r < TMV; ++r) __stcs(dst + (int64_t)r * ostride, __uint_as_float(v[r >> 4][r & 15]));
-          } else {
+          for (int c16 = 0; c16 < kRows / 16; ++c16)
+            tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + slot * NT * TMV + t * TMV + h0 + c16 * 16, v[c16]);
+          tmem_ld_wait();
+          const int64_t c = 128 * t + 32 * qd + lane;
+          if (c < ncols && !(dbg(prm, 1))) {
+            float* dst = obase + c + (int64_t)h0 * ostride;
+            if (nrows == TMV) {
 #pragma unroll
-            for (int r = 0; r < TMV; ++r)
-              if (r < nrows) __stcs(dst + (int64_t)r * ostride, __uint_as_float(v[r >> 4][r & 15]));
+              for (int r = 0; r < kRows; ++r) __stcs(dst + (int64_t)r * ostride, __uint_as_float(v[r >> 4][r & 15]));
+            } else {
+#pragma unroll
+              for (int r = 0; r < kRows; ++r)
+                if (h0 + r < nrows) __stcs(dst + (int64_t)r * ostride, __uint_as_float(v[r >> 4][r & 15]));
+            }
           }
         }
       }
@@ -767,42 +764,58 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   }
 }
 
-// S1 fix-up: CTA c looks at boundary c; if a big panel q is split there and c is the first boundary inside q, it
-// sums the partial tiles of every CTA holding blocks of q, in CTA order, and writes q's rows of C.
+// S1 fix-up. CTA c reads the S1 ranges k_spmm published: if CTA c - 1's last panel q is split (boundary c lies
+// strictly inside q) and boundary c is the first one inside q (CTA c - 1 starts at or before q's start), it sums
+// the partial tiles of every CTA holding blocks of q, in CTA order (deterministic), and writes q's rows of C. The
+// contributing CTAs are listed once per CTA in shared memory (no per-element work search).
 template <int TMV>
-__global__ void __launch_bounds__(128) k_spmm_fixup(const uint32_t* __restrict__ brp, int64_t p_lo, int64_t p_hi,
+__global__ void __launch_bounds__(128) k_spmm_fixup(const uint32_t* __restrict__ brp, const uint64_t* __restrict__ ranges,
                                                     const float* __restrict__ ws, float* __restrict__ C, int64_t M,
                                                     int64_t N, int n0, int wcols, const uint64_t* split_flag,
                                                     uint64_t epoch) {
   pdl_wait();
-  constexpr uint64_t kPW = panel_weight<TMV>();
+  constexpr int kMaxSrc = 256;
+  __shared__ int s_src[kMaxSrc];  // (cc << 1) | workspace slot of each contributing CTA
+  __shared__ int s_n;
+  __shared__ int64_t s_q;
   const uint64_t G = gridDim.x, c = blockIdx.x;
   if (c == 0 || *split_flag != epoch) return;  // no split panel in this launch
-  int64_t pt;
-  const uint64_t t = work_boundary<kPW>(brp, p_lo, p_hi, c, G, pt, SerialFind<kPW>());
-  const uint64_t base = unit_of<kPW>(brp, p_lo);
-  if (t <= base) return;
-  const int64_t q = panel_of_unit<kPW>(brp, p_lo, p_hi, t - 1);
-  if (q >= p_hi) return;
-  const uint64_t qs = unit_of<kPW>(brp, q), qe = unit_of<kPW>(brp, q + 1);
-  if (t >= qe || t <= qs) return;  // boundary c is not inside q
-  if (c >= 2 && work_boundary<kPW>(brp, p_lo, p_hi, c - 1, G, pt, SerialFind<kPW>()) > qs) return;  // earlier one inside q
+  if (threadIdx.x == 0) {
+    s_n = 0;
+    const uint64_t* A = ranges + 4 * (c - 1);
+    const int64_t pa = (int64_t)A[0], pb = (int64_t)A[1];
+    const uint32_t bB = (uint32_t)A[2], bE = (uint32_t)(A[2] >> 32);
+    const bool ff = A[3] & 1, lf = (A[3] >> 1) & 1;
+    const int64_t q = pb - 1;
+    s_q = q;
+    if (bB < bE && !lf && (pa != q || ff)) {  // boundary c is the first one strictly inside panel q
+      const uint32_t q0 = brp[q], q1 = brp[q + 1];
+      for (uint64_t cc = c - 1; cc < G && s_n < kMaxSrc; ++cc) {
+        const uint64_t* W = ranges + 4 * cc;
+        const int64_t wpa = (int64_t)W[0];
+        if (wpa > q) break;
+        const uint32_t b0 = max(q0, (uint32_t)W[2]), b1 = min(q1, (uint32_t)(W[2] >> 32));
+        if (b0 >= b1) continue;  // no blocks of q in CTA cc
+        s_src[s_n++] = (int)(cc << 1) | (q == wpa ? 0 : 1);
+      }
+    }
+  }
+  __syncthreads();
+  const int n = s_n;
+  if (n == 0) return;
+  const int64_t q = s_q;
   const int64_t row0 = q * TMV;
   const int nrows = (int)min((int64_t)TMV, M - row0);
-  const int64_t ncols = min((int64_t)wcols, N - n0);
-  for (int64_t e = threadIdx.x; e < (int64_t)nrows * ncols; e += blockDim.x) {
-    const int r = (int)(e / ncols);
-    const int64_t col = e % ncols;
-    float acc = 0.f;
-    for (uint64_t cc = c - 1; cc < G; ++cc) {
-      const CtaWork w = cta_work<kPW>(brp, p_lo, p_hi, cc, G, SerialFind<kPW>());
-      if (w.pa > q) break;
-      const uint32_t b0 = max(brp[q], w.bB), b1 = min(brp[q + 1], w.bE);
-      if (b0 >= b1) continue;  // no blocks of q in CTA cc
-      acc += ws[((int64_t)(2 * cc + (q == w.pa ? 0 : 1)) * TMV + r) * wcols + col];
+  const int ncols = (int)min((int64_t)wcols, N - n0);
+  for (int r = 0; r < nrows; ++r)
+    for (int col = threadIdx.x; col < ncols; col += blockDim.x) {
+      float acc = 0.f;
+      for (int k = 0; k < n; ++k) {
+        const int src = s_src[k];
+        acc += ws[((int64_t)(2 * (src >> 1) + (src & 1)) * TMV + r) * wcols + col];
+      }
+      C[(row0 + r) * N + n0 + col] = acc;
     }
-    C[(row0 + r) * N + n0 + col] = acc;
-  }
 }
 
 template <int NT, int GM, int TMV, int TKV>
@@ -825,11 +838,13 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   if (stage_cap >= kDecWarps && stage_cap < stages) stages = stage_cap - stage_cap % kDecWarps;
   const size_t smem = smem_for(stages);
   if (smem > 227 * 1024) return HRPB_ERROR_NOT_SUPPORTED;  // (not reachable with the instantiated NT / TM / TK)
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};  // per device: an attribute applies to the current device only
+  if (first_on_device(attr_set)) {
     cudaError_t e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV, TKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return cuda_status(e);
-    attr_set = true;
+    if (e != cudaSuccess) {
+      attr_set = 0;
+      return cuda_status(e);
+    }
   }
   static const char* trace_path = kInstr ? getenv("HRPB_TRACE") : nullptr;
   long long* trace = nullptr;
@@ -844,10 +859,10 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   int grid = num_sms();
   if ((int64_t)grid > p_hi - p_lo) grid = (int)(p_hi > p_lo ? p_hi - p_lo : 1);
   SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, p_lo, p_hi, scr.ws, scr.flag, scr.epoch,
-                 B, h->K, ldb, n0, stages, trace, debug};
+                 scr.ranges, B, h->K, ldb, n0, stages, trace, debug};
   launch_pdl(k_spmm<NT, GM, TMV, TKV>, grid, kSpmmThreads, smem, s, tm, prm);
-  launch_pdl(k_spmm_fixup<TMV>, grid, 128, 0, s, h->brp, p_lo, p_hi, scr.ws, C, h->M, N, n0, 128 * NT, scr.flag,
-             scr.epoch);
+  launch_pdl(k_spmm_fixup<TMV>, grid, 128, 0, s, h->brp, (const uint64_t*)scr.ranges, scr.ws, C, h->M, N, n0, 128 * NT,
+             scr.flag, scr.epoch);
   note_launch(2);
   if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)
     static long long host[kTraceSlots * kTraceN];

@@ -35,13 +35,20 @@ def panel_weights(row_ptr: np.ndarray, tm: int = 16, weight: str = "nnz") -> np.
     raise ValueError(weight)
 
 
-def shard_plan(row_ptr: np.ndarray, world: int, tm: int = 16, weight: str = "nnz") -> list[Shard]:
-    """Contiguous panel ranges with ~equal weight per rank (deterministic)."""
+def shard_plan(row_ptr: np.ndarray, world: int, tm: int = 16, weight="nnz") -> list[Shard]:
+    """Contiguous panel ranges with ~equal weight per rank (deterministic). `weight` is 'nnz' (north star),
+    'rows', or an explicit per-panel weight array (e.g. HRPB blocks per panel from a GPU build: the cost-model
+    option of SURVEY §8(e), which tracks gathered bytes on low-alpha matrices)."""
     if world < 1:
         raise ValueError("world must be >= 1")
     rp = np.asarray(row_ptr, dtype=np.int64)
     M = rp.shape[0] - 1
-    w = panel_weights(rp, tm, weight)
+    if isinstance(weight, str):
+        w = panel_weights(rp, tm, weight)
+    else:
+        w = np.asarray(weight, dtype=np.int64)
+        if w.shape[0] != (M + tm - 1) // tm:
+            raise ValueError("one weight per panel expected")
     P = w.shape[0]
     W = np.zeros(P + 1, dtype=np.int64)
     W[1:] = np.cumsum(w)

@@ -34,7 +34,7 @@ class HrpbError(RuntimeError):
 
 
 class _Config(C.Structure):
-    _fields_ = [("tm", C.c_int32), ("tk", C.c_int32)]
+    _fields_ = [("tm", C.c_int32), ("tk", C.c_int32)]  # tm = 0: automatic (hrpb.h)
 
 
 class _View(C.Structure):
@@ -88,7 +88,7 @@ def _stream(stream):
     return C.c_void_p(s.cuda_stream)
 
 
-def _dev(t, dtype, name):
+def _dev(t, dtype, name, numel=None, device=None):
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor")
@@ -96,7 +96,46 @@ def _dev(t, dtype, name):
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, got {t.numel()}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
     return C.c_void_p(t.data_ptr())
+
+
+def _csr_dev(row_ptr, col_idx, values, M):
+    """Device pointers of a CSR (int64 row_ptr [M+1], int32 col_idx [nnz], float32 values [nnz], one device)."""
+    import torch
+    nnz = int(col_idx.numel()) if hasattr(col_idx, "numel") else -1
+    dev = row_ptr.device if hasattr(row_ptr, "device") else None
+    return (_dev(row_ptr, torch.int64, "row_ptr", M + 1), _dev(col_idx, torch.int32, "col_idx", None, dev),
+            _dev(values, torch.float32, "values", nnz, dev), nnz)
+
+
+def _out(out, M, N, B):
+    """The caller's C buffer: float32, contiguous, (M, N), on B's device — or a new one."""
+    import torch
+    if out is None:
+        return torch.empty((M, N), dtype=torch.float32, device=B.device)
+    if tuple(out.shape) != (M, N):
+        raise ValueError(f"out must be ({M}, {N}), got {tuple(out.shape)}")
+    _dev(out, torch.float32, "out", M * N, B.device)
+    return out
+
+
+def _host(a, dtype, name, shape):
+    """Host buffer pointer (numpy array or CPU tensor) with the exact dtype, shape and C-contiguity."""
+    import torch
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            raise TypeError(f"{name} must be a host buffer")
+        ok = a.dtype == {np.int64: torch.int64, np.int32: torch.int32, np.float32: torch.float32}[dtype]
+        if not ok or tuple(a.shape) != shape or not a.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous {np.dtype(dtype).name} buffer of shape {shape}")
+        return C.c_void_p(a.data_ptr())
+    if not isinstance(a, np.ndarray) or a.dtype != dtype or a.shape != shape or not a.flags.c_contiguous:
+        raise TypeError(f"{name} must be a C-contiguous {np.dtype(dtype).name} array of shape {shape}")
+    return C.c_void_p(a.ctypes.data)
 
 
 class Hrpb:
@@ -143,13 +182,11 @@ class Hrpb:
 
 
 def build(row_ptr, col_idx, values, M: int, K: int, tm: int = 16, tk: int = 16, stream=None) -> Hrpb:
-    """hrpb_build: CSR (CUDA tensors int64/int32/float32) -> HRPB handle."""
-    import torch
-    nnz = int(col_idx.numel())
+    """hrpb_build: CSR (CUDA tensors int64/int32/float32) -> HRPB handle. tm = 0: the library picks TM."""
+    rp, ci, va, nnz = _csr_dev(row_ptr, col_idx, values, M)
     cfg = _Config(tm, tk)
     h = C.c_void_p()
-    st = lib().hrpb_build(M, K, nnz, _dev(row_ptr, torch.int64, "row_ptr"), _dev(col_idx, torch.int32, "col_idx"),
-                          _dev(values, torch.float32, "values"), C.byref(cfg), _stream(stream), C.byref(h))
+    st = lib().hrpb_build(M, K, nnz, rp, ci, va, C.byref(cfg), _stream(stream), C.byref(h))
     _check(st, "hrpb_build")
     return Hrpb(h)
 
@@ -160,10 +197,7 @@ def spmm(A: Hrpb, B, out=None, stream=None):
     if B.dim() != 2 or B.shape[0] != A.K:
         raise ValueError(f"B must be ({A.K}, N)")
     N = int(B.shape[1])
-    if out is None:
-        out = torch.empty((A.M, N), dtype=torch.float32, device=B.device)
-    elif tuple(out.shape) != (A.M, N):
-        raise ValueError("out has the wrong shape")
+    out = _out(out, A.M, N, B)
     st = lib().hrpb_spmm(A.handle, _dev(B, torch.float32, "B"), _dev(out, torch.float32, "out"), A.M, A.K, N,
                          _stream(stream))
     _check(st, "hrpb_spmm")
@@ -178,16 +212,13 @@ def build_spmm(row_ptr, col_idx, values, B, M: int, K: int, out=None, tm: int = 
     if B.dim() != 2 or B.shape[0] != K:
         raise ValueError(f"B must be ({K}, N)")
     N = int(B.shape[1])
-    if out is None:
-        out = torch.empty((M, N), dtype=torch.float32, device=B.device)
-    nnz = int(col_idx.numel())
+    out = _out(out, M, N, B)
+    rp, ci, va, nnz = _csr_dev(row_ptr, col_idx, values, M)
     cfg = _Config(tm, tk)
     h = C.c_void_p()
     ms = (C.c_float * 2)()
-    st = lib().hrpb_build_spmm(M, K, N, nnz, _dev(row_ptr, torch.int64, "row_ptr"), _dev(col_idx, torch.int32, "col_idx"),
-                               _dev(values, torch.float32, "values"), _dev(B, torch.float32, "B"),
-                               _dev(out, torch.float32, "out"), C.byref(cfg), _stream(stream),
-                               C.byref(h) if keep else None, ms)
+    st = lib().hrpb_build_spmm(M, K, N, nnz, rp, ci, va, _dev(B, torch.float32, "B"), _dev(out, torch.float32, "out"),
+                               C.byref(cfg), _stream(stream), C.byref(h) if keep else None, ms)
     _check(st, "hrpb_build_spmm")
     return out, (Hrpb(h) if keep else None), (float(ms[0]), float(ms[1]))
 
@@ -199,12 +230,11 @@ def build_spmm_async(row_ptr, col_idx, values, B, M: int, K: int, out, tm: int =
     if B.dim() != 2 or B.shape[0] != K:
         raise ValueError(f"B must be ({K}, N)")
     N = int(B.shape[1])
-    nnz = int(col_idx.numel())
+    out = _out(out, M, N, B)
+    rp, ci, va, nnz = _csr_dev(row_ptr, col_idx, values, M)
     cfg = _Config(tm, tk)
-    st = lib().hrpb_build_spmm_async(M, K, N, nnz, _dev(row_ptr, torch.int64, "row_ptr"),
-                                     _dev(col_idx, torch.int32, "col_idx"), _dev(values, torch.float32, "values"),
-                                     _dev(B, torch.float32, "B"), _dev(out, torch.float32, "out"), C.byref(cfg),
-                                     _stream(stream))
+    st = lib().hrpb_build_spmm_async(M, K, N, nnz, rp, ci, va, _dev(B, torch.float32, "B"),
+                                     _dev(out, torch.float32, "out"), C.byref(cfg), _stream(stream))
     _check(st, "hrpb_build_spmm_async")
     return out
 
@@ -220,15 +250,15 @@ def sync_status(stream=None):
 
 def build_spmm_host(row_ptr, col_idx, values, B, M: int, K: int, out=None, tm: int = 16, tk: int = 16, stream=None):
     """hrpb_build_spmm_host: the whole hot path from host buffers (numpy or pinned CPU tensors)."""
-    def ptr(a):
-        return C.c_void_p(a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data)
     N = int(B.shape[1])
+    nnz = int(col_idx.shape[0])
     if out is None:
         out = np.empty((M, N), np.float32)
-    nnz = int(col_idx.shape[0])
     cfg = _Config(tm, tk)
-    st = lib().hrpb_build_spmm_host(M, K, N, nnz, ptr(row_ptr), ptr(col_idx), ptr(values), ptr(B), ptr(out),
-                                    C.byref(cfg), _stream(stream))
+    st = lib().hrpb_build_spmm_host(M, K, N, nnz, _host(row_ptr, np.int64, "row_ptr", (M + 1,)),
+                                    _host(col_idx, np.int32, "col_idx", (nnz,)),
+                                    _host(values, np.float32, "values", (nnz,)), _host(B, np.float32, "B", (K, N)),
+                                    _host(out, np.float32, "out", (M, N)), C.byref(cfg), _stream(stream))
     _check(st, "hrpb_build_spmm_host")
     return out
 

@@ -56,3 +56,13 @@ def test_binding_rejects_host_tensors():
     rp = torch.zeros(5, dtype=torch.int64)
     with pytest.raises(TypeError):
         hp.build(rp, torch.zeros(0, dtype=torch.int32), torch.zeros(0), 4, 4)
+
+
+def test_unsupported_tile_pairs_rejected_before_device_work():
+    lib = hp.hrpb.lib()
+    out = ctypes.c_void_p()
+    fake = ctypes.c_void_p(16)  # never dereferenced: the (tm, tk) check comes first
+    for tm, tk in [(128, 32), (48, 16), (16, 8), (-1, 16), (256, 16)]:
+        cfg = hp.hrpb._Config(tm, tk)
+        assert lib.hrpb_build(4, 4, 0, fake, None, None, ctypes.byref(cfg), None, ctypes.byref(out)) == 1
+        assert lib.hrpb_build_spmm_host(4, 4, 4, 0, fake, None, None, fake, fake, ctypes.byref(cfg), None) == 1

@@ -98,3 +98,35 @@ def test_sharded_cuda_path_single_process():
     for rank in range(2):
         shard, C = hd.sharded_spmm(w.row_ptr, w.col_idx, w.vals, w.M, w.K, B, rank, 2)
         assert np.array_equal(C.cpu().numpy(), full[shard.row0:shard.row0 + shard.nrows])
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_self_spawn_gloo(world):
+    """`bench.py --gpus N` with WORLD_SIZE unset re-launches itself through torch.distributed.run (one process per
+    rank, 127.0.0.1 rendezvous). --cpu-check runs that orchestration on CPU with gloo: shard_plan partition, the B
+    broadcast, max/sum over ranks and rank 0's single JSON line; each rank's rows are checked against the oracle."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--cpu-check", "--gpus", str(world)],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    d = lines[0]
+    assert d["world"] == world and d["parity"] is True and d["scaling"] == "strong"
+    assert d["rows"] == d["M"] and d["nnz"] == d["total_nnz"]  # the shards cover the matrix exactly once
+
+
+def test_shard_plan_explicit_weights():
+    w = synth.make("c3", scale=8)
+    P = (w.M + 15) // 16
+    wts = np.random.default_rng(0).integers(0, 50, P)
+    plan = hd.shard_plan(w.row_ptr, 4, 16, wts)
+    per = [int(wts[s.p0:s.p1].sum()) for s in plan]
+    assert plan[0].p0 == 0 and plan[-1].p1 == P and sum(per) == wts.sum()
+    assert max(per) - wts.sum() / 4 <= wts.max() + 1
+    with pytest.raises(ValueError):
+        hd.shard_plan(w.row_ptr, 4, 16, wts[:-1])

@@ -108,3 +108,55 @@ def test_config4_uniform_full():  # configs[3]: 2M^2, 8 nnz/row, N = 512
 @pytest.mark.parametrize("N", [32, 512])
 def test_config5_fem_full(N):  # configs[4]: FEM 500K^2, N sweep
     run_case("c5", N, 16, rows_sample=256, panels_sample=24, full_check=(N == 32))
+
+
+# --------------------------------------------------------------------------- whole-array HRPB at full size
+@pytest.mark.parametrize("name,tm", [("c2a", 64), ("c2a", 16), ("c2b", 64), ("c4", 16), ("c5", 16)])
+def test_full_size_hrpb_whole_array(name, tm):
+    """Every byte of blockedRowPtr / activeCols / sizePtr / packedBlocks against the oracle converter run on the
+    whole matrix (not sampled panels)."""
+    w = synth.make(name)
+    A = hp.build(dev(w.row_ptr), dev(w.col_idx), dev(w.vals), w.M, w.K, tm=tm)
+    ref = oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm)
+    brp, ac, sp, packed = A.to_host()
+    assert np.array_equal(brp, ref.blockedRowPtr)
+    assert np.array_equal(ac, ref.activeCols)
+    assert np.array_equal(sp, ref.sizePtr)
+    assert packed.tobytes() == ref.packedBlocks.tobytes()
+
+
+# --------------------------------------------------------------------------- the bench's exact step
+def bench_step_check(name, want_tm, rows_sample=2048, hub_rows=64):
+    """bench.py's step: hrpb_build_spmm_async with tm = 0 (library choice), graph-replayed back to back on a side
+    stream, full-size inputs resident in HBM; C (after the replays) against the FP64 oracle on sampled rows plus
+    the heaviest rows, within the north-star tolerance; every replay's CSR status clean."""
+    w = synth.make(name)
+    Bh = w.B()
+    rp, ci, v, B = dev(w.row_ptr), dev(w.col_idx), dev(w.vals), dev(Bh)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        C = torch.full((w.M, w.N), float("nan"), device="cuda")
+        _, A, _ = hp.build_spmm(rp, ci, v, B, w.M, w.K, out=C, tm=0, stream=side, keep=True)
+        assert A.tm == want_tm, A.tm
+        A.free()
+        for _ in range(3):  # eager, capture, replays
+            hp.build_spmm(rp, ci, v, B, w.M, w.K, out=C, tm=0, stream=side)
+        C.fill_(float("nan"))
+        for _ in range(5):  # the timed loop: replays without host synchronization
+            hp.build_spmm_async(rp, ci, v, B, w.M, w.K, C, tm=0, stream=side)
+        hp.sync_status(side)
+    rng = np.random.default_rng(5)
+    heavy = np.argsort(np.diff(w.row_ptr))[-hub_rows:]
+    rows = np.unique(np.concatenate([[0, w.M - 1], heavy, rng.choice(w.M, rows_sample, replace=False)])).astype(np.int64)
+    Cs = C[torch.from_numpy(rows).cuda()].cpu().numpy()
+    Cref, S = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, Bh, rows=rows, with_bound=True)
+    check_float(Cs, Cref, S, f"bench step {name}")
+    assert bool(torch.isfinite(C).all())
+
+
+def test_bench_step_c3_full():
+    bench_step_check("c3", 16)
+
+
+def test_bench_step_c2a_full():
+    bench_step_check("c2a", 64)

@@ -278,7 +278,7 @@ def test_spmm_deterministic():
 
 
 # --------------------------------------------------------------------------- TM > 16 panels (NEXT-1)
-@pytest.mark.parametrize("tm,tk", [(32, 16), (64, 16), (16, 32), (32, 32), (64, 32)])
+@pytest.mark.parametrize("tm,tk", [(32, 16), (64, 16), (128, 16), (16, 32), (32, 32), (64, 32)])
 @pytest.mark.parametrize("N", [8, 128, 200, 512])
 def test_spmm_exact_tm(tm, tk, N):
     w = synth.make("c1", scale=2, N=N)
@@ -289,7 +289,7 @@ def test_spmm_exact_tm(tm, tk, N):
                 f"tm={tm} tk={tk} N={N}")
 
 
-@pytest.mark.parametrize("tm,tk", [(32, 16), (64, 16), (16, 32), (64, 32)])
+@pytest.mark.parametrize("tm,tk", [(32, 16), (64, 16), (128, 16), (16, 32), (64, 32)])
 @pytest.mark.parametrize("name,scale,N", [("c2a", 4, 128), ("c3", 7, 256), ("c5", 3, 64)])
 def test_spmm_float_tm(tm, tk, name, scale, N):
     w = synth.make(name, scale=scale, N=N)
@@ -322,14 +322,14 @@ def test_host_entry_empty_and_zero_rows():
 
 
 # --------------------------------------------------------------------------- S1: split big panels + fix-up
-@pytest.mark.parametrize("tm", [16, 64])
+@pytest.mark.parametrize("tm", [16, 64, 128])
 @pytest.mark.parametrize("N", [32, 300])
 def test_spmm_split_hub_panels(tm, N):
     """A few hub panels each worth many CTAs' shares among thousands of small ones: the hubs are split between
     CTAs (partial tiles in the workspace, summed by k_spmm_fixup in CTA order). Exact mode, so C is bit-exact
     whatever the split; repeated calls are bitwise identical (deterministic fix-up order)."""
     rng = np.random.default_rng(5)
-    M, K = 64 * 400, 30000
+    M, K = 128 * 400, 30000
     lens = rng.integers(0, 6, M)
     for r in (tm * 7, tm * 7 + 3, tm * 200 + 1, M - 1):  # hub rows (two in one panel)
         lens[r] = 12000
@@ -452,3 +452,82 @@ def test_spmm_split_boundaries_everywhere(seed):
     A = gpu_build(M, K, rp, ci, v)
     C = hp.spmm(A, dev(Bh))
     check_exact(C.cpu().numpy(), oracle.csr_spmm(M, K, rp, ci, v, Bh), f"seed {seed}")
+
+
+# --------------------------------------------------------------------------- tile choice, staging alternatives
+def test_unsupported_tile_pair_rejected():
+    """(TM, TK) = (128, 32) would need 64 brick slots per block (the decoder gives one lane per slot): rejected by
+    every entry point before any work, like any other unsupported pair."""
+    w = synth.make("c1", scale=3, N=8)
+    for tm, tk in [(128, 32), (48, 16), (16, 8)]:
+        with pytest.raises(hp.HrpbError) as e:
+            gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm, tk=tk)
+        assert e.value.status == 1
+        with pytest.raises(hp.HrpbError) as e:
+            hp.build_spmm(dev(w.row_ptr), dev(w.col_idx), dev(w.vals), dev(w.B()), w.M, w.K, tm=tm, tk=tk)
+        assert e.value.status == 1
+        with pytest.raises(hp.HrpbError) as e:
+            hp.build_spmm_host(w.row_ptr, w.col_idx, w.vals, w.B(), w.M, w.K, tm=tm, tk=tk)
+        assert e.value.status == 1
+
+
+@pytest.mark.parametrize("name,scale,want", [("c2a", 3, 64), ("c2b", 3, 64), ("c3", 6, 16), ("c4", 4, 16),
+                                             ("c5", 2, 16), ("c1", 0, 16)])
+def test_auto_tm_choice_and_parity(name, scale, want):
+    """tm = 0: the library picks TM from a sampled B1 pass (DESIGN.md NEXT-1) -- the TM the measured sweep found
+    fastest for each structure -- and the result is the oracle's HRPB at that TM, C within the tolerance."""
+    w = synth.make(name, scale=scale)
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=0)
+    assert A.tm == want, (name, A.tm)
+    assert_same_hrpb(A, oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=A.tm), f"{name} auto")
+    B = w.B()
+    C = hp.spmm(A, dev(B)).cpu().numpy()
+    Cref, S = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B, with_bound=True)
+    if w.mode == synth.EXACT:
+        check_exact(C, Cref, f"{name} auto")
+    else:
+        check_float(C, Cref, S, f"{name} auto")
+
+
+@pytest.fixture
+def gather4(monkeypatch):
+    monkeypatch.setenv("HRPB_GATHER", "0")  # S3 through TMA tile::gather4 instead of cp.async (read per call)
+    yield
+
+
+@pytest.mark.parametrize("tm", [16, 64, 128])
+@pytest.mark.parametrize("N", [8, 33, 128, 256, 520])
+def test_spmm_gather4_exact(gather4, tm, N):
+    w = synth.make("c1", scale=2, N=N)
+    B = w.B()
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm)
+    check_exact(hp.spmm(A, dev(B)).cpu().numpy(), oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B),
+                f"gather4 tm={tm} N={N}")
+
+
+@pytest.mark.parametrize("name,scale,N", [("c3", 7, 256), ("c5", 3, 64), ("c2a", 4, 100)])
+def test_spmm_gather4_float(gather4, name, scale, N):
+    w = synth.make(name, scale=scale, N=N)
+    B = w.B()
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+    C = hp.spmm(A, dev(B)).cpu().numpy()
+    Cref, S = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B, with_bound=True)
+    check_float(C, Cref, S, f"gather4 {name}")
+
+
+def test_free_orders_after_spmm_on_other_streams():
+    """hrpb_free right after an SpMM on another stream (no synchronization): the release waits for that stream
+    (events recorded by hrpb_spmm), so the pool cannot hand the arrays to a new build while they are read."""
+    w = synth.make("c5", scale=3, N=256, mode=synth.EXACT)
+    B = dev(w.B())
+    Cref = oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, w.B())
+    s2 = torch.cuda.Stream()
+    for _ in range(3):
+        A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals)
+        C = torch.empty((w.M, w.N), device="cuda")
+        hp.spmm(A, B, out=C, stream=s2)
+        A.free()  # no sync
+        junk = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, np.full_like(w.vals, 7.0))  # reuses pool memory
+        s2.synchronize()
+        check_exact(C.cpu().numpy(), Cref, "spmm vs free on another stream")
+        junk.free()
