@@ -770,6 +770,33 @@ __device__ __forceinline__ void emit_block_meta(uint8_t* blkp, const unsigned lo
   for (uint32_t t = hdr + 8 * nbr + 4 * nz; t < size; t += 4) *tail++ = 0u;
 }
 
+// emit_block_meta with run-time brick shape (listed panels: one kernel for every TM / TK)
+__device__ __forceinline__ void emit_block_meta_dyn(uint8_t* blkp, const unsigned long long* pj, int nbc, int nbrow,
+                                                    uint32_t nbr, uint32_t nz, uint32_t size) {
+  uint64_t* blk = reinterpret_cast<uint64_t*>(blkp);
+  const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+  uint64_t acc = 0;
+  uint32_t nb = 1, k = 0, wi = 0;  // byte 0 = colPtr[0] = 0
+  for (int bc = 0; bc < nbc; ++bc) {
+    for (int br = 0; br < nbrow; ++br) k += pj[bc * nbrow + br] != 0ull;
+    acc |= (uint64_t)k << (8 * (nb & 7));
+    if ((++nb & 7) == 0) { blk[wi++] = acc; acc = 0; }
+  }
+  for (int bc = 0; bc < nbc; ++bc)
+    for (int br = 0; br < nbrow; ++br) {
+      if (!pj[bc * nbrow + br]) continue;
+      acc |= (uint64_t)br << (8 * (nb & 7));
+      if ((++nb & 7) == 0) { blk[wi++] = acc; acc = 0; }
+    }
+  if (nb & 7) blk[wi++] = acc;
+  for (int i = 0; i < nbc * nbrow; ++i) {
+    const uint64_t v = pj[i];
+    if (v) blk[wi++] = v;
+  }
+  uint32_t* tail = reinterpret_cast<uint32_t*>(blkp + hdr + 8 * nbr + 4 * nz);
+  for (uint32_t t = hdr + 8 * nbr + 4 * nz; t < size; t += 4) *tail++ = 0u;
+}
+
 #ifdef HRPB_BTRACE
 __device__ unsigned long long g_btrace[8];  // per-phase cycles summed over warps (diagnostic builds only)
 #define BT_MARK(k) do { const long long t_ = clock64(); bt[k] += t_ - bt_last; bt_last = t_; } while (0)
@@ -1042,240 +1069,244 @@ __global__ void __launch_bounds__(32 * kWWarps, HRPB_WB_MINB) k_wbuild(const int
 }
 
 // ------------------------------------------------------------------ pass A (CTA), listed panels with <= kSmallCap entries
-// One CTA per listed panel ("for row_panel in rowPanels_chunk"). q[e] = rank of col_idx[e] among the
-// panel's distinct columns (ascending, R23; "active_cols = uniq(cols[...])"), nblk = ceil(nact/TK)
-// (R1), brick patterns (bit = (r % 16) * 4 + q % 4, R3) and the panel's total block bytes.
-__global__ void __launch_bounds__(kSmallThreads) k_count(const int64_t* __restrict__ rp,
-                                                        const int32_t* __restrict__ ci, int64_t M, int64_t K,
-                                                        int64_t nnz, int tm, int tk, uint32_t* __restrict__ q,
-                                                        uint32_t* __restrict__ nact_out,
-                                                        uint32_t* __restrict__ nblk_out,
-                                                        uint32_t* __restrict__ pbytes_out,
-                                                        uint64_t* __restrict__ gpat,
-                                                        const uint32_t* __restrict__ midlist,
-                                                        const uint32_t* __restrict__ nmid,
-                                                        uint32_t* __restrict__ biglist,
-                                                        uint32_t* __restrict__ nbig, uint32_t* status) {
+// One CTA per listed panel, claimed dynamically ("for row_panel in rowPanels_chunk"). q[e] = rank of
+// col_idx[e] among the panel's distinct columns (ascending, R23; "active_cols = uniq(cols[...])"),
+// nblk = ceil(nact/TK) (R1), brick patterns (bit = (r % 16) * 4 + q % 4, R3) and the panel's total block bytes.
+// Ranking, by the panel's column layout:
+//  * windowed byte maps (clustered columns, e.g. FEM stencils, banded panels too wide for the warp path): the
+//    1024-column windows the panel touches are found from its row "breaks" only (the entries starting a row or a
+//    new window within a row: rows are sorted) through a window-occupancy bitmap over all K/1024 windows, whose
+//    popcount prefix gives each window its ordinal; each entry then marks a byte in its window's 1-KB byte map
+//    (plain stores: no same-word atomics), the byte maps become bitmap words, and rank = word prefix + popc;
+//  * more than kMaxWin windows (scattered columns, e.g. R-MAT) or K > 32M: a CTA radix sort (CUB) of the
+//    (column, entry) pairs, rank = number of distinct columns before the entry's in sorted order.
+constexpr int kMidThreads = 256;
+constexpr int kMidItems = kSmallCap / kMidThreads;  // 8 entries per thread in the sort path
+constexpr int kWinBits = 10;                        // window = 1024 columns = 32 bitmap words
+constexpr int kMaxWin = 16;                         // windows per panel on the windowed path
+constexpr int kOccWords = 1024;                     // window-occupancy words: K <= 2^(15 + kWinBits) = 32M
+using MidSort = cub::BlockRadixSort<uint32_t, kMidThreads, kMidItems, uint32_t, 6>;  // <= 2048 entries
+using MidSort2 = cub::BlockRadixSort<uint32_t, kMidThreads, 2, uint32_t, 6>;         // <= 512 entries
+struct MidWin {
+  uint8_t bmap[kMaxWin << kWinBits];  // byte map per window
+  uint32_t bits[kMaxWin * 32];        // bitmap words
+  uint32_t pre[kMaxWin * 32];         // exclusive popcount prefix per word
+};
+union MidUnion {
+  MidWin win;
+  typename MidSort::TempStorage sort;
+  typename MidSort2::TempStorage sort2;
+};
+struct MidSmem {
+  uint32_t col[kSmallCap];
+  uint32_t q[kSmallCap];  // window ordinal, then rank
+  uint8_t row[kSmallCap];
+  uint32_t occ[kOccWords];
+  uint32_t occpre[kOccWords];
+  uint32_t last_key[kMidThreads];
+  MidUnion u;
+  // brick patterns follow (dynamic size: (kSmallCap / tk + 1) * nbk * 8 bytes)
+};
+__host__ __device__ constexpr size_t mid_smem_bytes(int tm, int tk) {
+  return sizeof(MidSmem) + (size_t)(kSmallCap / tk + 1) * (tk / HRPB_BRICK_K) * (tm / HRPB_BRICK_M) * 8 + 16;
+}
+
+// rank of every entry among the distinct columns: radix sort of (column, entry), head flags, CTA scan
+template <typename SortT, int ITEMS>
+__device__ __forceinline__ uint32_t mid_sort_rank(MidSmem& S, typename SortT::TempStorage& tmp, int E, int kb,
+                                                  uint32_t* s_scan) {
+  const int tid = threadIdx.x;
+  uint32_t key[ITEMS], val[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const int i = tid * ITEMS + k;
+    key[k] = i < E ? S.col[i] : 0xFFFFFFFFu;
+    val[k] = (uint32_t)i;
+  }
+  SortT(tmp).Sort(key, val, 0, kb);
+  S.last_key[tid] = key[ITEMS - 1];
+  __syncthreads();
+  uint32_t heads = 0, nact = 0;
+  uint32_t prev = tid ? S.last_key[tid - 1] : 0xFFFFFFFFu;
+  bool hd[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const bool valid = val[k] < (uint32_t)E;
+    hd[k] = valid && (tid * ITEMS + k == 0 || key[k] != prev);
+    heads += hd[k];
+    prev = key[k];
+  }
+  uint32_t run = block_excl_scan<kMidThreads>(heads, &nact, s_scan);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    run += hd[k];
+    if (val[k] < (uint32_t)E) S.q[val[k]] = run - 1;
+  }
+  return nact;
+}
+
+__global__ void __launch_bounds__(kMidThreads) k_count(const int64_t* __restrict__ rp,
+                                                      const int32_t* __restrict__ ci, int64_t M, int64_t K,
+                                                      int64_t nnz, int tm, int tk, uint32_t* __restrict__ q,
+                                                      uint32_t* __restrict__ nact_out,
+                                                      uint32_t* __restrict__ nblk_out,
+                                                      uint32_t* __restrict__ pbytes_out,
+                                                      uint64_t* __restrict__ gpat,
+                                                      const uint32_t* __restrict__ midlist,
+                                                      const uint32_t* __restrict__ nmid,
+                                                      uint32_t* __restrict__ biglist,
+                                                      uint32_t* __restrict__ nbig, uint32_t* work, uint32_t* status) {
   pdl_wait();
   extern __shared__ __align__(16) uint8_t dsm[];
+  MidSmem& S = *reinterpret_cast<MidSmem*>(dsm);
+  unsigned long long* s_pat = reinterpret_cast<unsigned long long*>(dsm + ((sizeof(MidSmem) + 15) & ~(size_t)15));
   __shared__ int64_t s_rp[129];
-  __shared__ uint32_t s_scan[kSmallThreads / 32 + 1];
-  __shared__ int32_t s_mm[2 * kSmallThreads / 32];
-  uint64_t* s_keys = reinterpret_cast<uint64_t*>(dsm);                 // [kSmallCap] (also the bitmap)
-  uint32_t* s_col = reinterpret_cast<uint32_t*>(s_keys + kSmallCap);   // [kSmallCap]
-  uint32_t* s_q = s_col + kSmallCap;                                   // [kSmallCap]
-  uint8_t* s_row = reinterpret_cast<uint8_t*>(s_q + kSmallCap);        // [kSmallCap]
-  unsigned long long* s_pat = reinterpret_cast<unsigned long long*>(s_row + kSmallCap);  // [cap bricks]
-
+  __shared__ uint32_t s_scan[kMidThreads / 32 + 1];
+  __shared__ uint32_t s_t;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t count = *nmid;
-  for (uint32_t t = blockIdx.x; t < count; t += gridDim.x) {
-  const int64_t p = midlist[t];
-  load_panel_rows(rp, M, nnz, tm, p, s_rp, status);
-  const int nrows = (int)min((int64_t)tm, M - p * tm);
-  const int64_t e0 = s_rp[0];
-  const int E = (int)min((int64_t)kSmallCap + 1, s_rp[nrows] - e0);
-  if (E > kSmallCap) {  // CTA-uniform: handled by k_count_big
-    if (threadIdx.x == 0) biglist[atomicAdd(nbig, 1u)] = (uint32_t)p;
-    continue;
-  }
-  // entries -> shared memory (local row, column)
-  int32_t mn = INT32_MAX, mx = INT32_MIN;
-  for (int i = threadIdx.x; i < E; i += blockDim.x) {  // one flat pass: all loads in flight together
-    const int32_t c = ci[e0 + i];
-    s_col[i] = (uint32_t)c;
-    s_row[i] = (uint8_t)row_of(s_rp, nrows, e0 + i);
-    mn = min(mn, c);
-    mx = max(mx, c);
-  }
-  block_minmax<kSmallThreads>(mn, mx, s_mm);  // (contains __syncthreads)
-  for (int i = threadIdx.x; i < E; i += blockDim.x) {  // validation
-    const int32_t c = (int32_t)s_col[i];
-    if (c < 0 || c >= K) atomicOr(status, ST_COL_RANGE);
-    if (i > 0 && s_row[i - 1] == s_row[i] && (int32_t)s_col[i - 1] >= c) atomicOr(status, ST_COL_ORDER);
-  }
-  uint32_t nact = 0;
-  const int64_t span = (int64_t)mx - (int64_t)mn + 1;
-  if (span <= 32 * kSpanWords) {
-    // bitmap ranking: set bits, exclusive popcount prefix per word, rank = prefix + popc(word & below)
-    uint32_t* bm = reinterpret_cast<uint32_t*>(s_keys);
-    uint32_t* pre = bm + kSpanWords;
-    for (int i = threadIdx.x; i < kSpanWords; i += blockDim.x) bm[i] = 0;
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const int occ_words = (int)min((int64_t)kOccWords, ceil_div(ceil_div(K, 1 << kWinBits), 32));
+  const bool occ_ok = ceil_div(K, 1 << kWinBits) <= 32 * kOccWords;
+  int kb = 1;
+  while (kb < 32 && (1ll << kb) < K) ++kb;  // sort bits: columns < K <= 2^kb
+  while (true) {
+    if (tid == 0) s_t = atomicAdd(work, 1u);
     __syncthreads();
-    for (int i = threadIdx.x; i < E; i += blockDim.x) {
-      const uint32_t off = s_col[i] - (uint32_t)mn;
-      atomicOr(&bm[off >> 5], 1u << (off & 31));
+    const uint32_t t = s_t;
+    if (t >= count) break;
+    const int64_t p = midlist[t];
+    load_panel_rows(rp, M, nnz, tm, p, s_rp, status);  // (barriers: also orders s_t's read)
+    const int nrows = (int)min((int64_t)tm, M - p * tm);
+    const int64_t e0 = s_rp[0];
+    const int E = (int)min((int64_t)kSmallCap + 1, s_rp[nrows] - e0);
+    if (E > kSmallCap) {  // CTA-uniform: handled by k_count_big
+      if (tid == 0) biglist[atomicAdd(nbig, 1u)] = (uint32_t)p;
+      continue;
     }
+    // entries -> shared memory (column clamped into [0, K) for memory safety; invalid CSR is flagged), row map
+    bool bad_range = false;
+    for (int i = tid; i < E; i += kMidThreads) {
+      const int32_t c = ci[e0 + i];
+      if (c < 0 || c >= K) bad_range = true;
+      S.col[i] = (uint32_t)min(max(c, 0), (int32_t)(K - 1));
+    }
+    for (int i = tid; i < occ_words; i += kMidThreads) S.occ[i] = 0u;
+    for (int r = warp; r < nrows; r += kMidThreads / 32) {
+      const int b = (int)(s_rp[r] - e0), e = (int)(s_rp[r + 1] - e0);
+      for (int i = b + lane; i < e; i += 32) S.row[i] = (uint8_t)r;
+    }
+    if (__any_sync(0xffffffffu, bad_range) && lane == 0) atomicOr(status, ST_COL_RANGE);
     __syncthreads();
-    constexpr int kPer = kSpanWords / kSmallThreads;
-    uint32_t cnt[kPer], sum = 0;
+    // in-row order and the window breaks: a row's first entry or its first entry in a new window
+    bool bad_order = false;
+    for (int i = tid; i < E; i += kMidThreads) {
+      const uint32_t c = S.col[i];
+      const bool same_row = i > 0 && S.row[i - 1] == S.row[i];
+      if (same_row && S.col[i - 1] >= c) bad_order = true;
+      if (occ_ok && (!same_row || (S.col[i - 1] >> kWinBits) != (c >> kWinBits))) {
+        const uint32_t w = c >> kWinBits;
+        atomicOr(&S.occ[w >> 5], 1u << (w & 31));
+      }
+    }
+    if (__any_sync(0xffffffffu, bad_order) && lane == 0) atomicOr(status, ST_COL_ORDER);
+    __syncthreads();
+    uint32_t nwin = 0xFFFFFFFFu;
+    if (occ_ok) {  // window ordinals: exclusive popcount prefix over the occupancy words (<= 4 per thread)
+      uint32_t cnt[kOccWords / kMidThreads], sum = 0;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) { cnt[i] = __popc(bm[threadIdx.x * kPer + i]); sum += cnt[i]; }
-    uint32_t run = block_excl_scan<kSmallThreads>(sum, &nact, s_scan);
+      for (int k = 0; k < kOccWords / kMidThreads; ++k) {
+        const int wi = tid * (kOccWords / kMidThreads) + k;
+        cnt[k] = wi < occ_words ? __popc(S.occ[wi]) : 0u;
+        sum += cnt[k];
+      }
+      uint32_t run = block_excl_scan<kMidThreads>(sum, &nwin, s_scan);
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) { pre[threadIdx.x * kPer + i] = run; run += cnt[i]; }
-    __syncthreads();
-    for (int i = threadIdx.x; i < E; i += blockDim.x) {
-      const uint32_t off = s_col[i] - (uint32_t)mn;
-      const uint32_t w = off >> 5, b = off & 31;
-      s_q[i] = pre[w] + __popc(bm[w] & ((1u << b) - 1u));
+      for (int k = 0; k < kOccWords / kMidThreads; ++k) {
+        const int wi = tid * (kOccWords / kMidThreads) + k;
+        if (wi < occ_words) S.occpre[wi] = run;
+        run += cnt[k];
+      }
     }
-  } else {
-    // windowed bitmap (wide but clustered columns, e.g. FEM stencils: a few 1024-column windows): distinct windows
-    // via a shared hash set, ordered by counting, then one bitmap per window and a popcount prefix over all of
-    // them. More than kMaxWin windows (scattered columns): the sort below.
-    constexpr int kWinWords = 32, kMaxWin = 32, kHash = 256;
-    uint32_t* wbm = reinterpret_cast<uint32_t*>(s_keys);         // [kMaxWin * 32] window bitmaps
-    uint32_t* wpre = wbm + kMaxWin * kWinWords;                  // [kMaxWin * 32] word prefixes
-    int32_t* hkey = reinterpret_cast<int32_t*>(wpre + kMaxWin * kWinWords);  // [kHash] window ids (-1 empty)
-    int32_t* hidx = hkey + kHash;                                // [kHash] window order
-    int32_t* wlist = hidx + kHash;                               // [kMaxWin] distinct windows
-    __shared__ int s_nwin;
-    for (int i = threadIdx.x; i < kHash; i += blockDim.x) { hkey[i] = -1; hidx[i] = -1; }
-    for (int i = threadIdx.x; i < kMaxWin * kWinWords; i += blockDim.x) wbm[i] = 0u;
-    if (threadIdx.x == 0) s_nwin = 0;
-    __syncthreads();
-    auto slot_of = [&](int32_t wv, bool insert) -> int {
-      int h = (int)(((uint32_t)wv * 2654435761u) >> 24);
-      for (int k = 0; k < kHash; ++k, h = (h + 1) & (kHash - 1)) {
-        const int32_t cur = insert ? atomicCAS(&hkey[h], -1, wv) : hkey[h];
-        if (cur == wv) return h;
-        if (cur == -1) {
-          if (insert) { atomicAdd(&s_nwin, 1); return h; }
-          return -1;
-        }
-      }
-      return -1;
-    };
-    // (a negative column — invalid CSR, flagged above — is ranked as column 0 to keep every index in bounds)
-    for (int i = threadIdx.x; i < E; i += blockDim.x) {  // (stops once the windows overflow: scattered columns)
-      if (*reinterpret_cast<volatile int*>(&s_nwin) > kMaxWin) break;
-      slot_of(max((int32_t)s_col[i], 0) >> 10, true);
-    }
-    __syncthreads();
-    const int nwin = s_nwin;
-    bool windowed = nwin <= kMaxWin;
-    if (windowed) {
-      if (threadIdx.x == 0) s_nwin = 0;
-      __syncthreads();
-      for (int i = threadIdx.x; i < kHash; i += blockDim.x)
-        if (hkey[i] >= 0) wlist[atomicAdd(&s_nwin, 1)] = i;
-      __syncthreads();
-      if ((int)threadIdx.x < nwin) {  // order of each window = number of smaller window ids
-        const int32_t me = hkey[wlist[threadIdx.x]];
-        int ord = 0;
-        for (int k = 0; k < nwin; ++k) ord += hkey[wlist[k]] < me;
-        hidx[wlist[threadIdx.x]] = ord;
+    uint32_t nact = 0;
+    if (nwin <= (uint32_t)kMaxWin) {
+      // ---- windowed byte maps
+      uint32_t* bm32 = reinterpret_cast<uint32_t*>(S.u.win.bmap);
+      for (int i = tid; i < (int)nwin << (kWinBits - 2); i += kMidThreads) bm32[i] = 0u;
+      __syncthreads();  // (also publishes occpre)
+      for (int i = tid; i < E; i += kMidThreads) {
+        const uint32_t c = S.col[i], w = c >> kWinBits;
+        const uint32_t k = S.occpre[w >> 5] + __popc(S.occ[w >> 5] & ((1u << (w & 31)) - 1u));
+        S.q[i] = k;
+        S.u.win.bmap[(k << kWinBits) | (c & ((1u << kWinBits) - 1u))] = 1;
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < E; i += blockDim.x) {
-        const int32_t c = max((int32_t)s_col[i], 0);
-        const int wi = hidx[slot_of(c >> 10, false)], bit = c & 1023;
-        atomicOr(&wbm[wi * kWinWords + (bit >> 5)], 1u << (bit & 31));
-      }
-      __syncthreads();
-      constexpr int kPer = kMaxWin * kWinWords / kSmallThreads;
+      constexpr int kPer = kMaxWin * 32 / kMidThreads;  // bitmap words per thread
       uint32_t cnt[kPer], sum = 0;
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) { cnt[i] = __popc(wbm[threadIdx.x * kPer + i]); sum += cnt[i]; }
-      uint32_t run = block_excl_scan<kSmallThreads>(sum, &nact, s_scan);
+      for (int k = 0; k < kPer; ++k) {
+        const int wd = tid * kPer + k;
+        uint32_t word = 0;
+        if (wd < (int)nwin * 32) {
+          const uint4* src = reinterpret_cast<const uint4*>(S.u.win.bmap + 32 * wd);
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) { wpre[threadIdx.x * kPer + i] = run; run += cnt[i]; }
-      __syncthreads();
-      for (int i = threadIdx.x; i < E; i += blockDim.x) {
-        const int32_t c = max((int32_t)s_col[i], 0);
-        const int wi = hidx[slot_of(c >> 10, false)], bit = c & 1023;
-        const int wd = wi * kWinWords + (bit >> 5);
-        s_q[i] = wpre[wd] + __popc(wbm[wd] & ((1u << (bit & 31)) - 1u));
-      }
-      __syncthreads();
-    }
-    if (!windowed) {
-      // merge ranking. The panel's rows are sorted runs of (column, entry) keys (unique: the entry breaks ties);
-      // ceil(log2(rows)) levels of pairwise run merges place each key by one binary search in its partner run,
-      // then first occurrences of each column are counted (R23: ascending distinct columns). An unsorted row
-      // (invalid CSR, flagged above) only has to keep every index in bounds.
-      uint64_t* src = s_keys;
-      uint64_t* dst = reinterpret_cast<uint64_t*>(s_col);  // s_col + s_q: 2 kSmallCap words
-      int levels = 0;
-      while ((1 << levels) < nrows) ++levels;
-      if (levels & 1) { uint64_t* t2 = src; src = dst; dst = t2; }  // the last level lands in s_keys
-      uint32_t cv[kSmallCap / kSmallThreads];
+          for (int h = 0; h < 2; ++h) {
+            const uint4 v = src[h];
+            const uint32_t x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int k = 0; k < kSmallCap / kSmallThreads; ++k) {
-        const int i = threadIdx.x + k * kSmallThreads;
-        cv[k] = i < E ? s_col[i] : 0u;
-      }
-      __syncthreads();  // (src may overlay s_col)
-#pragma unroll
-      for (int k = 0; k < kSmallCap / kSmallThreads; ++k) {
-        const int i = threadIdx.x + k * kSmallThreads;
-        if (i < E) src[i] = ((uint64_t)cv[k] << 32) | (uint32_t)i;
-      }
-      __syncthreads();
-      for (int l = 0; l < levels; ++l) {
-        for (int x = threadIdx.x; x < E; x += blockDim.x) {
-          const uint64_t key = src[x];
-          if ((uint32_t)key >= (uint32_t)E) continue;  // (stale slot: only after an unsorted row)
-          const int r = s_row[(uint32_t)key];
-          const int g0 = (r >> (l + 1)) << (l + 1);
-          const int gm = min(g0 + (1 << l), nrows), g1 = min(g0 + (2 << l), nrows);
-          const int a0 = (int)(s_rp[g0] - e0), am = (int)(s_rp[gm] - e0), a1 = (int)(s_rp[g1] - e0);
-          const bool left = r < gm;
-          int lo = left ? am : a0, hi = left ? a1 : am;
-          const int base = lo;
-          while (lo < hi) {  // keys of the partner run below ours
-            const int mid = (lo + hi) >> 1;
-            if (src[mid] < key) lo = mid + 1; else hi = mid;
+            for (int j = 0; j < 4; ++j)  // bytes are 0 / 1: bits 0, 8, 16, 24 -> a nibble
+              word |= ((x[j] | (x[j] >> 7) | (x[j] >> 14) | (x[j] >> 21)) & 0xFu) << (16 * h + 4 * j);
           }
-          const int pos = a0 + (left ? x - a0 : x - am) + (lo - base);
-          if ((unsigned)pos < (unsigned)E) dst[pos] = key;  // (always, for sorted rows)
         }
-        __syncthreads();
-        uint64_t* t2 = src; src = dst; dst = t2;
+        cnt[k] = __popc(word);
+        sum += cnt[k];
+        if (wd < (int)nwin * 32) S.u.win.bits[wd] = word;
       }
-      // src == s_keys now; s_q (overlaid by the merge buffer) is rewritten below
-      for (int i = threadIdx.x; i < E; i += blockDim.x) s_q[i] = 0xFFFFFFFFu;
+      uint32_t run = block_excl_scan<kMidThreads>(sum, &nact, s_scan);
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int wd = tid * kPer + k;
+        if (wd < (int)nwin * 32) S.u.win.pre[wd] = run;
+        run += cnt[k];
+      }
       __syncthreads();
-      const int per = (E + kSmallThreads - 1) / kSmallThreads;
-      const int beg = threadIdx.x * per;
-      uint32_t sum = 0;
-      for (int i = beg; i < beg + per && i < E; ++i)
-        if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++sum;
-      uint32_t run = block_excl_scan<kSmallThreads>(sum, &nact, s_scan);
-      for (int i = beg; i < beg + per && i < E; ++i) {
-        if (i == 0 || (s_keys[i] >> 32) != (s_keys[i - 1] >> 32)) ++run;
-        if ((uint32_t)s_keys[i] < (uint32_t)E) s_q[(uint32_t)s_keys[i]] = run - 1;
+      for (int i = tid; i < E; i += kMidThreads) {
+        const uint32_t c = S.col[i];
+        const uint32_t wd = (S.q[i] << (kWinBits - 5)) | ((c >> 5) & ((1u << (kWinBits - 5)) - 1u));
+        S.q[i] = S.u.win.pre[wd] + __popc(S.u.win.bits[wd] & ((1u << (c & 31)) - 1u));
       }
-    }  // !windowed
-  }
-  // patterns (fill_brick_nnz_pattern): brick i = bc * (TM/16) + br in CSC order
-  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
-  const uint32_t nblk = (nact + tk - 1) / tk;
-  const int nbricks = (int)nblk * nbk;
-  for (int i = threadIdx.x; i < nbricks; i += blockDim.x) s_pat[i] = 0ull;
-  __syncthreads();
-  for (int i = threadIdx.x; i < E; i += blockDim.x) {
-    const uint32_t qq = s_q[i], r = s_row[i];
-    q[e0 + i] = qq;
-    if (qq >= nact) continue;  // (only for invalid CSR: an unsorted row in the merge ranking)
-    const uint32_t j = qq / tk, lc = qq % tk;
-    const int bit = (int)(((r & 15) << 2) | (lc & 3));
-    // 32-bit OR on the half holding the bit (a 64-bit shared atomicOr is a CAS loop on sm_100)
-    uint32_t* half = reinterpret_cast<uint32_t*>(&s_pat[j * nbk + (lc >> 2) * nbrow + (r >> 4)]) + (bit >> 5);
-    atomicOr(half, 1u << (bit & 31));
-  }
-  __syncthreads();
-  uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
-  for (int i = threadIdx.x; i < nbricks; i += blockDim.x) gp[i] = s_pat[i];
-  uint32_t bytes = 0;
-  for (uint32_t j = threadIdx.x; j < nblk; j += blockDim.x) {
-    uint32_t nbr = 0, nz = 0;
-    for (int i = 0; i < nbk; ++i) { const uint64_t v = s_pat[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
-    bytes += block_bytes(nbc, nbr, nz);
-  }
-  uint32_t total;
-  block_excl_scan<kSmallThreads>(bytes, &total, s_scan);
-  if (threadIdx.x == 0) { nact_out[p] = nact; nblk_out[p] = nblk; pbytes_out[p] = total; }
+    } else {
+      // ---- CTA radix sort of (column, entry); padding keys sort last (stable sort, entry >= E)
+      __syncthreads();  // (occpre readers done before the union is reused)
+      if (E <= 2 * kMidThreads) nact = mid_sort_rank<MidSort2, 2>(S, S.u.sort2, E, kb, s_scan);
+      else nact = mid_sort_rank<MidSort, kMidItems>(S, S.u.sort, E, kb, s_scan);
+    }
+    // patterns (fill_brick_nnz_pattern): brick i = bc * (TM/16) + br in CSC order
+    const uint32_t nblk = (nact + tk - 1) / tk;
+    const int nbricks = (int)nblk * nbk;
+    for (int i = tid; i < nbricks; i += kMidThreads) s_pat[i] = 0ull;
+    __syncthreads();
+    for (int i = tid; i < E; i += kMidThreads) {
+      const uint32_t qq = S.q[i], r = S.row[i];
+      q[e0 + i] = qq;
+      const uint32_t j = qq / tk, lc = qq % tk;
+      const int bit = (int)(((r & 15) << 2) | (lc & 3));
+      // 32-bit OR on the half holding the bit (a 64-bit shared atomicOr is a CAS loop on sm_100)
+      uint32_t* half = reinterpret_cast<uint32_t*>(&s_pat[j * nbk + (lc >> 2) * nbrow + (r >> 4)]) + (bit >> 5);
+      atomicOr(half, 1u << (bit & 31));
+    }
+    __syncthreads();
+    uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
+    for (int i = tid; i < nbricks; i += kMidThreads) gp[i] = s_pat[i];
+    uint32_t bytes = 0;
+    for (uint32_t j = tid; j < nblk; j += kMidThreads) {
+      uint32_t nbr = 0, nz = 0;
+      for (int i = 0; i < nbk; ++i) { const uint64_t v = s_pat[j * nbk + i]; nbr += v != 0ull; nz += __popcll(v); }
+      bytes += block_bytes(nbc, nbr, nz);
+    }
+    uint32_t total;
+    block_excl_scan<kMidThreads>(bytes, &total, s_scan);  // (barriers: shared state is free for the next panel)
+    if (tid == 0) { nact_out[p] = nact; nblk_out[p] = nblk; pbytes_out[p] = total; }
   }  // panel loop
 }
 
@@ -1448,128 +1479,501 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
   }
 }
 
-// ------------------------------------------------------------------ pass B (CTA), listed panels
-// One CTA per listed panel. Block j of panel p is global block b0 + j (b0 = blockedRowPtr[p]); its byte offset
-// is the panel offset plus the in-panel exclusive scan of block sizes (sizePtr). Header,
-// patterns and values follow the HRPB-v1 layout; value destination = values base + popcount of the
-// earlier bricks + popcount of the lower bits of its own brick.
-__global__ void __launch_bounds__(kEmitThreads) k_emit(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                                      const float* __restrict__ vals, int64_t M, int64_t K,
-                                                      int64_t nnz, int tm, int tk, const uint32_t* __restrict__ q,
-                                                      const uint32_t* __restrict__ nact_in,
-                                                      const uint32_t* __restrict__ brp,
-                                                      const uint64_t* __restrict__ poff,
-                                                      const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac,
-                                                      uint64_t* __restrict__ sp, uint8_t* __restrict__ packed,
-                                                      const uint32_t* __restrict__ midlist,
-                                                      const uint32_t* __restrict__ nmid,
-                                                      uint32_t* __restrict__ hublist, uint32_t* __restrict__ hubch,
-                                                      unsigned long long* __restrict__ nhub, uint32_t* work) {
-  pdl_wait();
-  __shared__ int64_t s_rp[129];
-  __shared__ uint32_t s_scan[kEmitThreads / 32 + 1];
-  __shared__ uint64_t s_vbase[kEmitThreads];     // byte offset of each block's values (single-chunk panels)
-  __shared__ uint64_t s_pt[kEmitThreads * 4];    // patterns (single-chunk panels with nbk <= 4)
-  const uint32_t count = *nmid;
-  __shared__ uint32_t s_tt;
-  while (true) {  // panels claimed dynamically (listed panels differ in size by orders of magnitude)
-    if (threadIdx.x == 0) s_tt = atomicAdd(work, 1u);
-    __syncthreads();
-    const uint32_t tt = s_tt;
-    __syncthreads();
-    if (tt >= count) break;
-  const int64_t p = midlist[tt];
-  const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0;
-  if (nblk == 0) continue;
-  const uint32_t nact = nact_in[p];
-  load_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);
-  const int nrows = (int)min((int64_t)tm, M - p * tm);
-  const int64_t e0 = s_rp[0];
-  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
-  const uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
-  // blocks: sizes, sizePtr, headers, patterns, padding (chunks of kEmitThreads blocks)
-  uint64_t carry = poff[p];
-  for (uint32_t c0 = 0; c0 < nblk; c0 += kEmitThreads) {
-    const uint32_t j = c0 + threadIdx.x;
-    uint32_t nbr = 0, nz = 0, size = 0;
-    if (j < nblk) {
-      for (int i = 0; i < nbk; ++i) {
-        const uint64_t v = gp[(int64_t)j * nbk + i];
-        nbr += v != 0ull;
-        nz += __popcll(v);
-      }
-      size = block_bytes(nbc, nbr, nz);
-    }
-    uint32_t tot;
-    const uint32_t ex = block_excl_scan<kEmitThreads>(size, &tot, s_scan);
-    if (j < nblk) {
-      const uint64_t off = carry + ex;
-      sp[b0 + j] = off;
-      uint8_t* blk = packed + off;
-      const uint64_t* pt = gp + (int64_t)j * nbk;
-      const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
-      uint32_t k = 0;
-      blk[0] = 0;
-      for (int bc = 0; bc < nbc; ++bc) {
-        for (int br = 0; br < nbrow; ++br) {
-          const uint64_t v = pt[bc * nbrow + br];
-          if (!v) continue;
-          blk[nbc + 1 + k] = (uint8_t)br;                 // rows[]
-          reinterpret_cast<uint64_t*>(blk + hdr)[k] = v;  // patterns[]
-          ++k;
-        }
-        blk[bc + 1] = (uint8_t)k;  // colPtr[]
-      }
-      for (uint32_t i = nbc + 1 + nbr; i < hdr; ++i) blk[i] = 0;
-      for (uint32_t i = hdr + 8 * nbr + 4 * nz; i < size; ++i) blk[i] = 0;
-      if (nblk <= kEmitThreads) {
-        s_vbase[j] = off + hdr + 8 * nbr;
-        if (nbk <= 4)
-          for (int i = 0; i < nbk; ++i) s_pt[j * nbk + i] = pt[i];
-      }
-    }
-    carry += tot;
+// ------------------------------------------------------------------ hub panels (> kSmallCap entries), dense passes
+// One CTA per hub panel (claimed dynamically, power-law sizes). The column space is walked in passes of
+// kHubPassCols columns with a dense bitmap in shared memory: set the bits of the pass's entries (per-row entry
+// ranges of each pass come from one boundary sweep: rows are sorted), popcount prefix per 32-word group (u32) and
+// per word within its group (u16), rank = prefix + popc(lower bits) (R23: ascending distinct columns). Ranks go to
+// q[e]; the ranks of a pass are one contiguous range, so its blocks' brick patterns are built in a shared-memory
+// window (shared atomics) and flushed to global memory once complete (a pass's last, incomplete block is carried
+// into the next pass), together with each block's panel-relative byte offset. Per panel the work is
+// O(entries + K / 32) shared-memory operations and no global atomics. k_emit_hub writes the blocks and values
+// once the global scan has placed the panel.
+constexpr int kHubThreads = 512;
+constexpr int kEmitNT = 256;  // threads of the emission kernels (k_emit, k_emit_hub)
+constexpr int kHubPassWords = 32768;                 // bitmap words per pass
+constexpr int64_t kHubPassCols = 32 * kHubPassWords;  // 2^20 columns per pass
+constexpr int kHubGroups = kHubPassWords / 8;        // 4096 groups of 8 words (u8 prefix within a group)
+constexpr int kHubPatSlots = 2048;                   // brick-pattern window (u64 slots)
+constexpr int kHubBndWords = 1024;                   // per-row pass boundaries: TM x (passes + 1) <= this
+constexpr int kHubMetaChunk = 256;                   // blocks per metadata work item of k_emit_hub
+constexpr int kHubEntryChunk = 4096;                 // entries per value work item of k_emit_hub
+struct HubSmem {
+  uint32_t bits[kHubPassWords];
+  uint8_t pre8[kHubPassWords];  // popcount of the earlier words of the word's 8-word group (<= 224)
+  uint32_t gpre[kHubGroups];    // ranks before the group (panel-wide)
+  unsigned long long pat[kHubPatSlots];
+  uint32_t bnd[kHubBndWords];  // bnd[r * (npass + 1) + k] = first entry (panel-relative) of row r in pass >= k
+  uint32_t off[129];           // pass entries: exclusive prefix over rows
+  int64_t rp[129];
+  uint32_t scan[kHubThreads / 32 + 1];
+  uint32_t t;
+};
+__host__ __device__ inline bool hub_dense_ok(int64_t K, int tm) {
+  return (int64_t)tm * (ceil_div(K, kHubPassCols) + 1) <= kHubBndWords;
+}
+__device__ __forceinline__ int64_t rel_base(int64_t e0, int64_t p, int tk) { return e0 / tk + 2 * p; }
+
+// row of flattened pass item i: largest r with off[r] <= i (off[0] = 0, nondecreasing)
+__device__ __forceinline__ int hub_row_of(const uint32_t* off, int nrows, uint32_t i) {
+  int lo = 0, hi = nrows - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= i) lo = mid; else hi = mid - 1;
   }
-  for (int64_t t = nact + threadIdx.x; t < (int64_t)nblk * tk; t += blockDim.x) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
-  __syncthreads();  // sizePtr entries / staged metadata of this panel are visible to the whole CTA
-  const bool staged = nblk <= kEmitThreads && nbk <= 4;
-  const int64_t e1 = s_rp[nrows];
-  if (e1 - e0 > kHubEmit) {  // a hub's values are spread over every CTA by k_emit_hubvals (critical path)
-    if (threadIdx.x == 0) {  // one 64-bit atomic: (hub count << 32 | chunk count), so chunk bases rise with t
-      const unsigned long long nch = (unsigned long long)((e1 - e0 + kHubChunk - 1) / kHubChunk);
-      const unsigned long long old = atomicAdd(nhub, (1ull << 32) + nch);
+  return lo;
+}
+
+__global__ void __launch_bounds__(kHubThreads) k_count_hub(const int64_t* __restrict__ rp,
+                                                          const int32_t* __restrict__ ci, int64_t M, int64_t K,
+                                                          int64_t nnz, int tm, int tk, uint32_t* __restrict__ q,
+                                                          uint32_t* __restrict__ nact_out,
+                                                          uint32_t* __restrict__ nblk_out,
+                                                          uint32_t* __restrict__ pbytes_out,
+                                                          uint64_t* __restrict__ gpat, uint32_t* __restrict__ relb,
+                                                          const uint32_t* __restrict__ biglist,
+                                                          const uint32_t* __restrict__ nbig, uint32_t* work,
+                                                          uint32_t* __restrict__ hublist, uint32_t* __restrict__ hubch,
+                                                          unsigned long long* __restrict__ nhub, uint32_t* status) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  HubSmem& S = *reinterpret_cast<HubSmem*>(dsm);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t count = *nbig;
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const int npass = (int)ceil_div(K, kHubPassCols);
+  const int cap_blk = kHubPatSlots / nbk;  // blocks in the pattern window
+  const int tk_sh = tk == 16 ? 4 : 5;
+  while (true) {
+    if (tid == 0) S.t = atomicAdd(work, 1u);
+    __syncthreads();
+    const uint32_t t = S.t;
+    if (t >= count) break;
+    const int64_t p = biglist[t];
+    load_panel_rows(rp, M, nnz, tm, p, S.rp, status);  // (barriers)
+    const int nrows = (int)min((int64_t)tm, M - p * tm);
+    const int64_t e0 = S.rp[0], e1 = S.rp[nrows];
+    const int nb1 = npass + 1;
+    // (1) validation and the per-row pass boundaries: entry e starts pass k's range of its row for every
+    // k in (pass(e - 1), pass(e)] (the row's first entry: k in [0, pass(e)]); rows end at their last pass
+    for (int r = tid; r < nrows; r += kHubThreads) {
+      const uint32_t b = (uint32_t)(S.rp[r] - e0), e = (uint32_t)(S.rp[r + 1] - e0);
+      S.bnd[r * nb1 + npass] = e;
+      if (b == e)
+        for (int k = 0; k < npass; ++k) S.bnd[r * nb1 + k] = e;
+    }
+    __syncthreads();
+    bool bad_range = false, bad_order = false;
+    for (int64_t e = e0 + tid; e < e1; e += kHubThreads) {
+      const int32_t c = ci[e];
+      if (c < 0 || c >= K) bad_range = true;
+      const int r = row_of(S.rp, nrows, e);
+      const bool first = e == S.rp[r];
+      const int32_t cp = first ? 0 : ci[e - 1];
+      if (!first && cp >= c) bad_order = true;
+      const int kc = (int)(min(max(c, 0), (int32_t)(K - 1)) / kHubPassCols);
+      const int kp = first ? -1 : (int)(min(max(cp, 0), (int32_t)(K - 1)) / kHubPassCols);
+      // (an unsorted row may step back: kc < kp then sets nothing; its entries are still clamped into range)
+      for (int k = kp + 1; k <= kc; ++k) S.bnd[r * nb1 + k] = (uint32_t)(e - e0);
+      if (e + 1 == S.rp[r + 1])  // last entry: the row has nothing in later passes
+        for (int k = kc + 1; k < npass; ++k) S.bnd[r * nb1 + k] = (uint32_t)(e + 1 - e0);
+    }
+    if (__any_sync(0xffffffffu, bad_range) && lane == 0) atomicOr(status, ST_COL_RANGE);
+    if (__any_sync(0xffffffffu, bad_order) && lane == 0) atomicOr(status, ST_COL_ORDER);
+    __syncthreads();
+    uint32_t base = 0;         // ranks of earlier passes
+    uint32_t jw = 0;           // first block of the pattern window (blocks < jw are flushed; jw may hold carried bits)
+    uint32_t bytes = 0;        // panel-relative byte offset of block jw
+    for (int i = tid; i < cap_blk * nbk; i += kHubThreads) S.pat[i] = 0ull;
+    uint32_t* rel = relb + rel_base(e0, p, tk);
+    unsigned long long* gp = reinterpret_cast<unsigned long long*>(gpat + pat_base(e0, p, nbk, tk));
+    for (int k = 0; k < npass; ++k) {
+      // entries of pass k: rows' ranges [bnd[r][k], bnd[r][k+1]), flattened by an exclusive prefix over rows
+      if (tid < 32) {
+        uint32_t carry = 0;
+        for (int r0 = 0; r0 < nrows; r0 += 32) {
+          const int r = r0 + lane;
+          uint32_t len = 0;
+          if (r < nrows) {
+            const uint32_t b = S.bnd[r * nb1 + k], e = S.bnd[r * nb1 + k + 1];
+            len = e > b ? e - b : 0u;
+          }
+          uint32_t tot;
+          const uint32_t ex = warp_excl_scan(len, &tot);
+          if (r < nrows) S.off[r] = carry + ex;
+          carry += tot;
+        }
+        if (lane == 0) S.off[nrows] = carry;
+      }
+      __syncthreads();
+      const uint32_t npe = S.off[nrows];
+      const bool last = k == npass - 1;
+      if (npe == 0 && !last) continue;  // (CTA-uniform)
+      const int64_t c0 = (int64_t)k * kHubPassCols;
+      for (int i = tid; i < kHubPassWords; i += kHubThreads) S.bits[i] = 0u;
+      __syncthreads();
+      for (uint32_t i = tid; i < npe; i += kHubThreads) {  // set bits (warp-merged per word: dense hub rows)
+        const int r = hub_row_of(S.off, nrows, i);
+        const uint32_t e = S.bnd[r * nb1 + k] + (i - S.off[r]);
+        const int64_t c = min(max((int64_t)ci[e0 + e], (int64_t)0), K - 1) - c0;
+        const uint32_t w = (uint32_t)min(max(c, (int64_t)0), kHubPassCols - 1);
+        atomicOr(&S.bits[w >> 5], 1u << (w & 31));
+      }
+      __syncthreads();
+      {  // warp w: groups [256 w, 256 w + 256) of 8 words, 32 at a time (lane = group, two conflict-free 128-bit
+         // loads): u8 prefix per word, group totals scanned across the warp, warp totals across the CTA
+        constexpr int GPW = kHubGroups / (kHubThreads / 32);  // groups per warp (256)
+        const int w = tid >> 5;
+        uint32_t gsum[GPW / 32];
+#pragma unroll
+        for (int h = 0; h < GPW / 32; ++h) {
+          const int g = w * GPW + h * 32 + lane;
+          const uint4 a = *reinterpret_cast<const uint4*>(&S.bits[8 * g]);
+          const uint4 b = *reinterpret_cast<const uint4*>(&S.bits[8 * g + 4]);
+          const uint32_t c[8] = {(uint32_t)__popc(a.x), (uint32_t)__popc(a.y), (uint32_t)__popc(a.z),
+                                 (uint32_t)__popc(a.w), (uint32_t)__popc(b.x), (uint32_t)__popc(b.y),
+                                 (uint32_t)__popc(b.z), (uint32_t)__popc(b.w)};
+          uint32_t run = 0, lo = 0, hi = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i < 4) lo |= run << (8 * i); else hi |= run << (8 * (i - 4));
+            run += c[i];
+          }
+          *reinterpret_cast<uint2*>(&S.pre8[8 * g]) = make_uint2(lo, hi);
+          gsum[h] = run;
+        }
+        uint32_t incl[GPW / 32];  // inclusive scans across the warp, the 8 rounds interleaved
+#pragma unroll
+        for (int h = 0; h < GPW / 32; ++h) incl[h] = gsum[h];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+          for (int h = 0; h < GPW / 32; ++h) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl[h], o);
+            if (lane >= o) incl[h] += y;
+          }
+        }
+        uint32_t wtot = 0, hbase[GPW / 32];
+#pragma unroll
+        for (int h = 0; h < GPW / 32; ++h) {
+          hbase[h] = wtot;
+          wtot += __shfl_sync(0xffffffffu, incl[h], 31);
+        }
+        uint32_t tot;
+        const uint32_t wex = block_excl_scan<kHubThreads>(lane == 0 ? wtot : 0u, &tot, S.scan);
+        const uint32_t wbase = base + __shfl_sync(0xffffffffu, wex, 0);
+#pragma unroll
+        for (int h = 0; h < GPW / 32; ++h) S.gpre[w * GPW + h * 32 + lane] = wbase + hbase[h] + incl[h] - gsum[h];
+        __syncthreads();
+        // ranks (in the panel) of the pass's entries, and their brick-pattern bits: blocks in the shared window
+        // [jw, jw + cap_blk) by shared atomics, later blocks (huge passes) by global atomics into gp
+        const uint32_t jend = (base + tot + tk - 1) >> tk_sh;  // blocks touched after this pass
+        const uint32_t jwe = jw + cap_blk;
+        for (uint32_t j = max(jw, jwe) + tid; j < jend; j += kHubThreads)  // (beyond the window: zero, then OR)
+          for (int i = 0; i < nbk; ++i) gp[(int64_t)j * nbk + i] = 0ull;
+        __syncthreads();
+        for (uint32_t i = tid; i < npe; i += kHubThreads) {
+          const int r = hub_row_of(S.off, nrows, i);
+          const uint32_t e = S.bnd[r * nb1 + k] + (i - S.off[r]);
+          const int64_t c = min(max((int64_t)ci[e0 + e], (int64_t)0), K - 1) - c0;
+          const uint32_t w = (uint32_t)min(max(c, (int64_t)0), kHubPassCols - 1), wd = w >> 5;
+          const uint32_t qq = S.gpre[wd >> 3] + S.pre8[wd] + __popc(S.bits[wd] & ((1u << (w & 31)) - 1u));
+          q[e0 + e] = qq;
+          const uint32_t j = qq >> tk_sh, lc = qq & (tk - 1);
+          const int bit = ((r & 15) << 2) | (int)(lc & 3);
+          const int slot = (int)(lc >> 2) * nbrow + (r >> 4);
+          if (j < jwe) {
+            uint32_t* half = reinterpret_cast<uint32_t*>(&S.pat[(j - jw) * nbk + slot]) + (bit >> 5);
+            atomicOr(half, 1u << (bit & 31));
+          } else {
+            atomicOr(&gp[(int64_t)j * nbk + slot], 1ull << bit);
+          }
+        }
+        base += tot;
+      }
+      __threadfence_block();
+      __syncthreads();
+      // flush the blocks complete after this pass: patterns (window blocks from shared memory), sizes, relative
+      // offsets; the pass's incomplete last block is carried into the window's slot 0
+      const uint32_t jend = (base + tk - 1) >> tk_sh;
+      const uint32_t jcomplete = last ? jend : (base >> tk_sh);
+      const uint32_t jwe = jw + cap_blk;
+      for (uint32_t c2 = jw; c2 < jcomplete; c2 += kHubThreads) {
+        const uint32_t j = c2 + tid;
+        uint32_t size = 0;
+        if (j < jcomplete) {
+          uint32_t nbr = 0, nz = 0;
+          for (int i = 0; i < nbk; ++i) {
+            unsigned long long v;
+            if (j < jwe) {
+              v = S.pat[(j - jw) * nbk + i];
+              gp[(int64_t)j * nbk + i] = v;
+            } else {
+              v = __ldcg(&gp[(int64_t)j * nbk + i]);
+            }
+            nbr += v != 0ull;
+            nz += __popcll(v);
+          }
+          size = block_bytes(nbc, nbr, nz);
+        }
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan<kHubThreads>(size, &tot, S.scan);
+        if (j < jcomplete) rel[j] = bytes + ex;
+        bytes += tot;
+      }
+      __syncthreads();
+      if (jcomplete < jend) {  // carry block jcomplete
+        unsigned long long keep = 0ull;
+        if (tid < nbk)
+          keep = jcomplete < jwe ? S.pat[(jcomplete - jw) * nbk + tid] : __ldcg(&gp[(int64_t)jcomplete * nbk + tid]);
+        __syncthreads();
+        for (int i = tid; i < cap_blk * nbk; i += kHubThreads) S.pat[i] = i < nbk ? keep : 0ull;
+      } else {
+        for (int i = tid; i < cap_blk * nbk; i += kHubThreads) S.pat[i] = 0ull;
+      }
+      jw = jcomplete;
+      __syncthreads();
+    }
+    const uint32_t nact = base, nblk = (nact + tk - 1) >> tk_sh;
+    if (tid == 0) {
+      nact_out[p] = nact;
+      nblk_out[p] = nblk;
+      pbytes_out[p] = bytes;
+      // work items of k_emit_hub: block-metadata chunks, then value chunks
+      const unsigned long long items =
+          (unsigned long long)(ceil_div(nblk, kHubMetaChunk) + ceil_div(e1 - e0, kHubEntryChunk));
+      const unsigned long long old = atomicAdd(nhub, (1ull << 32) + items);
       hublist[old >> 32] = (uint32_t)p;
       hubch[old >> 32] = (uint32_t)old;
     }
-    continue;
   }
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const uint32_t qq = q[e];
-    const int32_t c = ci[e];
-    const float v = vals[e];
-    if (qq >= nact) continue;  // only for invalid CSR input
-    const int r = row_of(s_rp, nrows, e);
-    const uint32_t j = qq / tk, lc = qq % tk;
-    ac[((int64_t)b0 + j) * tk + lc] = (uint32_t)c;
-    const int bit = ((r & 15) << 2) | (lc & 3);
-    const int mine = (lc >> 2) * nbrow + (r >> 4);
-    const uint64_t* pt = staged ? s_pt + j * nbk : gp + (int64_t)j * nbk;
-    uint32_t nbr = 0, off = 0;
-    for (int i = 0; i < nbk; ++i) {
-      const uint64_t w = pt[i];
-      nbr += w != 0ull;
-      if (i < mine) off += __popcll(w);
+}
+
+// Hub panels' output, after the global scan: every CTA takes items of one flat list (per hub: its block-metadata
+// chunks — sizePtr = panel offset + relative offset, HRPB-v1 headers, patterns, padding, sentinel activeCols —
+// then its 4096-entry value chunks — activeCols and values at popcount ranks).
+__global__ void __launch_bounds__(kEmitNT) k_emit_hub(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                     const float* __restrict__ vals, int64_t M, int64_t K,
+                                                     int64_t nnz, int tm, int tk, const uint32_t* __restrict__ q,
+                                                     const uint32_t* __restrict__ nact_in,
+                                                     const uint32_t* __restrict__ brp,
+                                                     const uint64_t* __restrict__ poff,
+                                                     const uint64_t* __restrict__ gpat,
+                                                     const uint32_t* __restrict__ relb, uint32_t* __restrict__ ac,
+                                                     uint64_t* __restrict__ sp, uint8_t* __restrict__ packed,
+                                                     const uint32_t* __restrict__ hublist,
+                                                     const uint32_t* __restrict__ hubch,
+                                                     const unsigned long long* __restrict__ nhub) {
+  pdl_wait();
+  __shared__ int64_t s_rp[129];
+  const unsigned long long hc = *nhub;
+  const uint32_t count = (uint32_t)(hc >> 32), total = (uint32_t)hc;
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const int tk_sh = tk == 16 ? 4 : 5;
+  for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
+    uint32_t lo = 0, hi = count - 1;  // last hub t with hubch[t] <= g
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (hubch[mid] <= g) lo = mid; else hi = mid - 1;
     }
-    off += __popcll(pt[mine] & ((1ull << bit) - 1ull));
-    uint64_t vb;
-    if (staged) {
-      vb = s_vbase[j];
-    } else {
+    const int64_t p = hublist[lo];
+    const uint32_t item = g - hubch[lo];
+    load_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);  // (barriers)
+    const int nrows = (int)min((int64_t)tm, M - p * tm);
+    const int64_t e0 = s_rp[0], e1 = s_rp[nrows];
+    const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0, nact = nact_in[p];
+    const uint64_t pbase = poff[p];
+    const uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
+    const uint32_t* rel = relb + rel_base(e0, p, tk);
+    const uint32_t nmeta = (uint32_t)ceil_div(nblk, kHubMetaChunk);
+    if (item < nmeta) {
+      const uint32_t j = item * kHubMetaChunk + threadIdx.x;
+      if (j < nblk) {
+        const unsigned long long* pj = reinterpret_cast<const unsigned long long*>(gp) + (int64_t)j * nbk;
+        uint32_t nbr = 0, nz = 0;
+        for (int i = 0; i < nbk; ++i) { nbr += pj[i] != 0ull; nz += __popcll(pj[i]); }
+        const uint64_t off = pbase + rel[j];
+        sp[b0 + j] = off;
+        emit_block_meta_dyn(packed + off, pj, nbc, nbrow, nbr, nz, block_bytes(nbc, nbr, nz));
+        if (j + 1 == nblk)
+          for (uint32_t t = nact; t < nblk * (uint32_t)tk; ++t) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
+      }
+      continue;
+    }
+    const int64_t c0e = e0 + (int64_t)(item - nmeta) * kHubEntryChunk;
+    const int64_t c1e = min(e1, c0e + kHubEntryChunk);
+    for (int64_t e = c0e + threadIdx.x; e < c1e; e += kEmitNT) {
+      const uint32_t qq = q[e];
+      const int32_t c = ci[e];
+      const float v = vals[e];
+      if (qq >= nact) continue;  // only for invalid CSR input
+      const int r = row_of(s_rp, nrows, e);
+      const uint32_t j = qq >> tk_sh, lc = qq & (tk - 1);
+      ac[((int64_t)b0 + j) * tk + lc] = (uint32_t)c;
+      const int bit = ((r & 15) << 2) | (lc & 3);
+      const int mine = (lc >> 2) * nbrow + (r >> 4);
+      const uint64_t* pt = gp + (int64_t)j * nbk;
+      uint32_t nbr = 0, off = 0;
+      for (int i = 0; i < nbk; ++i) {
+        const uint64_t w = pt[i];
+        nbr += w != 0ull;
+        if (i < mine) off += __popcll(w);
+      }
+      off += __popcll(pt[mine] & ((1ull << bit) - 1ull));
       const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
-      vb = sp[b0 + j] + hdr + 8 * nbr;
+      reinterpret_cast<float*>(packed + pbase + rel[j] + hdr + 8 * nbr)[off] = v;
     }
-    reinterpret_cast<float*>(packed + vb)[off] = v;
   }
+}
+
+// ------------------------------------------------------------------ pass B (CTA), listed panels
+// One CTA per listed panel (claimed dynamically: listed panels differ in size by orders of magnitude). Block j of
+// panel p is global block b0 + j (b0 = blockedRowPtr[p]); its byte offset is the panel offset plus the in-panel
+// exclusive scan of block sizes (sizePtr). Header, patterns and values follow the HRPB-v1 layout; value
+// destination = values base + popcount of the earlier bricks + popcount of the lower bits of its own brick
+// (P:L211-219). Panels with <= kSmallCap entries stage their blocks' patterns, brick value offsets and value bases
+// in shared memory and map entries to rows through a row map, so each entry costs its three coalesced loads (rank,
+// column, value) and two stores; hub panels (> kHubEmit entries) only get their block metadata here, their values
+// are scattered by every CTA in k_emit_hubvals.
+__host__ __device__ constexpr size_t emit_smem_bytes(int tm, int tk) {
+  return (size_t)(kSmallCap / tk + 1) * ((tk / HRPB_BRICK_K) * (tm / HRPB_BRICK_M) * 10 + 8) + kSmallCap + 64;
+}
+
+__global__ void __launch_bounds__(kEmitNT) k_emit(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                 const float* __restrict__ vals, int64_t M, int64_t K,
+                                                 int64_t nnz, int tm, int tk, const uint32_t* __restrict__ q,
+                                                 const uint32_t* __restrict__ nact_in,
+                                                 const uint32_t* __restrict__ brp,
+                                                 const uint64_t* __restrict__ poff,
+                                                 const uint64_t* __restrict__ gpat, uint32_t* __restrict__ ac,
+                                                 uint64_t* __restrict__ sp, uint8_t* __restrict__ packed,
+                                                 const uint32_t* __restrict__ midlist,
+                                                 const uint32_t* __restrict__ nmid,
+                                                 uint32_t* __restrict__ hublist, uint32_t* __restrict__ hubch,
+                                                 unsigned long long* __restrict__ nhub, uint32_t* work,
+                                                 int hubs_done) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ int64_t s_rp[129];
+  __shared__ uint32_t s_scan[kEmitNT / 32 + 1];
+  __shared__ uint32_t s_tt;
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const int cap_blk = kSmallCap / tk + 1;
+  unsigned long long* s_pt = reinterpret_cast<unsigned long long*>(dsm);       // [cap_blk * nbk] patterns
+  uint64_t* s_vb = reinterpret_cast<uint64_t*>(s_pt + (size_t)cap_blk * nbk);  // [cap_blk] value base (bytes)
+  uint16_t* s_so = reinterpret_cast<uint16_t*>(s_vb + cap_blk);                 // [cap_blk * nbk] value offsets
+  uint8_t* s_row = reinterpret_cast<uint8_t*>(s_so + (size_t)cap_blk * nbk);    // [kSmallCap] row map
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t count = *nmid;
+  while (true) {
+    if (tid == 0) s_tt = atomicAdd(work, 1u);
+    __syncthreads();
+    const uint32_t tt = s_tt;
+    if (tt >= count) break;
+    const int64_t p = midlist[tt];
+    const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0;
+    if (nblk == 0) {
+      __syncthreads();
+      continue;
+    }
+    const uint32_t nact = nact_in[p];
+    load_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);
+    const int nrows = (int)min((int64_t)tm, M - p * tm);
+    const int64_t e0 = s_rp[0], e1 = s_rp[nrows];
+    const uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
+    const bool small = e1 - e0 <= kSmallCap;  // (CTA-uniform; then nblk <= cap_blk)
+    if (!small && hubs_done) continue;        // (k_count_hub + k_emit_hub own the hub panels)
+    if (small) {
+      for (int i = tid; i < (int)nblk * nbk; i += kEmitNT) s_pt[i] = gp[i];
+      for (int r = warp; r < nrows; r += kEmitNT / 32) {
+        const int b = (int)(s_rp[r] - e0), e = (int)(s_rp[r + 1] - e0);
+        for (int i = b + lane; i < e; i += 32) s_row[i] = (uint8_t)r;
+      }
+      __syncthreads();
+    }
+    // blocks: sizes, sizePtr, headers, patterns, padding (chunks of kEmitNT blocks)
+    uint64_t carry = poff[p];
+    for (uint32_t c0 = 0; c0 < nblk; c0 += kEmitNT) {
+      const uint32_t j = c0 + tid;
+      uint32_t nbr = 0, nz = 0, size = 0;
+      if (j < nblk) {
+        for (int i = 0; i < nbk; ++i) {
+          const uint64_t v = small ? s_pt[j * nbk + i] : gp[(int64_t)j * nbk + i];
+          if (small) s_so[j * nbk + i] = (uint16_t)nz;  // values of the earlier bricks of the block (CSC order)
+          nbr += v != 0ull;
+          nz += __popcll(v);
+        }
+        size = block_bytes(nbc, nbr, nz);
+      }
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<kEmitNT>(size, &tot, s_scan);
+      if (j < nblk) {
+        const uint64_t off = carry + ex;
+        sp[b0 + j] = off;
+        const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+        if (small) {
+          s_vb[j] = off + hdr + 8 * nbr;
+          if (nbc == 4 && nbrow == 1) {
+            emit_block_meta<4, 1>(packed + off, s_pt + j * nbk, nbr, nz, size);
+          } else {
+            emit_block_meta_dyn(packed + off, s_pt + j * nbk, nbc, nbrow, nbr, nz, size);
+          }
+        } else {
+          emit_block_meta_dyn(packed + off, reinterpret_cast<const unsigned long long*>(gp) + (int64_t)j * nbk, nbc,
+                              nbrow, nbr, nz, size);
+        }
+      }
+      carry += tot;
+    }
+    for (int64_t t = nact + tid; t < (int64_t)nblk * tk; t += kEmitNT) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
+    __syncthreads();  // sizePtr entries / staged metadata of this panel are visible to the whole CTA
+    if (e1 - e0 > kHubEmit) {  // a hub's values are spread over every CTA by k_emit_hubvals (critical path)
+      if (tid == 0) {  // one 64-bit atomic: (hub count << 32 | chunk count), so chunk bases rise with t
+        const unsigned long long nch = (unsigned long long)((e1 - e0 + kHubChunk - 1) / kHubChunk);
+        const unsigned long long old = atomicAdd(nhub, (1ull << 32) + nch);
+        hublist[old >> 32] = (uint32_t)p;
+        hubch[old >> 32] = (uint32_t)old;
+      }
+      continue;
+    }
+    if (small) {
+      const int E = (int)(e1 - e0);
+      for (int i = tid; i < E; i += kEmitNT) {  // values at popcount ranks, activeCols
+        const uint32_t qq = q[e0 + i];
+        const int32_t c = ci[e0 + i];
+        const float v = vals[e0 + i];
+        if (qq >= nact) continue;  // only for invalid CSR input
+        const int r = s_row[i];
+        const uint32_t j = qq / tk, lc = qq % tk;
+        ac[((int64_t)b0 + j) * tk + lc] = (uint32_t)c;
+        const int bit = ((r & 15) << 2) | (lc & 3);
+        const int slot = (int)j * nbk + (lc >> 2) * nbrow + (r >> 4);
+        const uint32_t off = s_so[slot] + __popcll(s_pt[slot] & ((1ull << bit) - 1ull));
+        reinterpret_cast<float*>(packed + s_vb[j])[off] = v;
+      }
+      continue;
+    }
+    for (int64_t e = e0 + tid; e < e1; e += kEmitNT) {  // mid-size hubs: metadata from global memory
+      const uint32_t qq = q[e];
+      const int32_t c = ci[e];
+      const float v = vals[e];
+      if (qq >= nact) continue;  // only for invalid CSR input
+      const int r = row_of(s_rp, nrows, e);
+      const uint32_t j = qq / tk, lc = qq % tk;
+      ac[((int64_t)b0 + j) * tk + lc] = (uint32_t)c;
+      const int bit = ((r & 15) << 2) | (lc & 3);
+      const int mine = (lc >> 2) * nbrow + (r >> 4);
+      const uint64_t* pt = gp + (int64_t)j * nbk;
+      uint32_t nbr = 0, off = 0;
+      for (int i = 0; i < nbk; ++i) {
+        const uint64_t w = pt[i];
+        nbr += w != 0ull;
+        if (i < mine) off += __popcll(w);
+      }
+      off += __popcll(pt[mine] & ((1ull << bit) - 1ull));
+      const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+      reinterpret_cast<float*>(packed + sp[b0 + j] + hdr + 8 * nbr)[off] = v;
+    }
   }  // panel loop
 }
 
@@ -1730,19 +2134,31 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   // panel lists: big (> kSmallCap entries, hub bitmap) | L1 (not on the warp path: CTA count + CTA emit)
   uint32_t* biglist = (uint32_t*)dalloc(3 * (P + 1) * sizeof(uint32_t), s);
   uint32_t* l1 = biglist + (P + 1);
-  uint32_t* ctr = (uint32_t*)dalloc(8 * sizeof(uint32_t), s);  // nbig, nl1, ticket, -, status
+  // nbig, nl1, ticket, hub work, status, emit work, hub (count << 32 | chunks) x2, count work
+  uint32_t* ctr = (uint32_t*)dalloc(16 * sizeof(uint32_t), s);
   uint64_t* lb = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t), s);  // look-back states (blocks << 34 | bytes)
   uint8_t* listed = (uint8_t*)dalloc(P + 1, s);
   uint64_t* info = (uint64_t*)dalloc(4 * sizeof(uint64_t), s);  // [3] = status word | hub count
   const int big_ctas = HRPB_BIG_CTAS_PER_SM * num_sms();
   const int64_t words = ceil_div(K, 32) + 2;
-  uint32_t* bigscr = (uint32_t*)dalloc((size_t)big_ctas * (2 * words + 2 * ((words + 31) / 32)) * sizeof(uint32_t), s);
+  // hub panels: dense shared-memory passes (k_count_hub / k_emit_hub) when the per-row pass boundaries fit, else
+  // the global occupancy-bitmap kernel (k_count_big, with k_emit / k_emit_hubvals)
+  static const bool force_old_hub = [] {
+    const char* e = getenv("HRPB_HUB_GLOBAL");  // experiments: the global-bitmap hub path
+    return e && atoi(e);
+  }();
+  const bool hub_dense = hub_dense_ok(K, tm) && !force_old_hub;
+  uint32_t* bigscr = hub_dense ? (uint32_t*)dalloc(16, s)
+                               : (uint32_t*)dalloc((size_t)big_ctas * (2 * words + 2 * ((words + 31) / 32)) *
+                                                   sizeof(uint32_t), s);
+  uint32_t* relb = (uint32_t*)dalloc((nnz / tk + 2 * P + 4) * sizeof(uint32_t), s);  // hub blocks' relative offsets
+  uint32_t* hub2 = (uint32_t*)dalloc(2 * (P + 1) * sizeof(uint32_t), s);
   hrpb_status_t st = HRPB_SUCCESS;
   // the fused look-back packs (blocks, bytes) into 62 bits
   if (nb_cap >= (1ll << 28) || bytes_cap >= (1ll << 34)) {
     st = HRPB_ERROR_NOT_SUPPORTED;
   } else if (!h->brp || !h->ac || !h->sp || !h->packed || !q || !cnt || !poff || !gpat || !biglist || !info ||
-             !bigscr || !ctr || !lb || !listed) {
+             !bigscr || !ctr || !lb || !listed || !relb || !hub2) {
     st = HRPB_ERROR_OUT_OF_MEMORY;
   }
   uint64_t hinfo[3] = {0, 0, 0};
@@ -1753,31 +2169,48 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     unsigned long long* nhub = reinterpret_cast<unsigned long long*>(ctr + 6);  // (hubs << 32 | chunks)
     uint32_t* hublist = biglist;  // (the big list is consumed by k_count_big before k_emit reuses it)
     uint32_t* hubch = biglist + 2 * (P + 1);
+    // dense hub path: its own (hub, work-item prefix) list, written by k_count_hub while it still reads the big list
+    uint32_t* hublist2 = hub2;
+    uint32_t* hubch2 = hub2 + (P + 1);
+    unsigned long long* nhub2 = reinterpret_cast<unsigned long long*>(ctr + 10);
     uint32_t* status = ctr + 4;
-    cudaMemsetAsync(ctr, 0, 8 * sizeof(uint32_t), s);
-    const size_t count_smem =
-        (size_t)kSmallCap * (8 + 4 + 4 + 1) + (size_t)ceil_div(kSmallCap, tk) * nbk * sizeof(uint64_t);
+    cudaMemsetAsync(ctr, 0, 16 * sizeof(uint32_t), s);
+    const size_t count_smem = mid_smem_bytes(tm, tk), emit_smem = emit_smem_bytes(tm, tk);
     static std::atomic<uint64_t> attr{0};  // per device
-    if (first_on_device(attr)) cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (first_on_device(attr)) {
+      cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_count_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HubSmem));
+    }
     const unsigned wgrid = (unsigned)ceil_div(P, kWWarps);
     const int mid_ctas = 8 * num_sms();
+    const int count_ctas = (int)(227 * 1024 / (count_smem + 1024)) * num_sms();
+    const int emit_ctas = (int)min((size_t)8, 227 * 1024 / (emit_smem + 1024)) * num_sms();
     cudaMemsetAsync(lb, 0, (P + 1) * sizeof(uint64_t), s);
     cudaMemsetAsync(h->brp, 0, sizeof(uint32_t), s);  // P == 0: blockedRowPtr = {0}
     cudaMemsetAsync(poff, 0, sizeof(uint64_t), s);
     if (P > 0) {
       // classification; listed panels counted by a CTA (<= kSmallCap entries) or the hub bitmap kernel
       launch_wclassify(tm, tk, wgrid, s, row_ptr, col_idx, M, nnz, P, listed, l1, nl1);
-      launch_pdl(k_count, mid_ctas, kSmallThreads, count_smem, s, row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
-                                                          pbytes, gpat, l1, nl1, biglist, nbig, status);
-      launch_pdl(k_count_big, big_ctas, kBigThreads, 0, s, row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk, pbytes, gpat,
-                                                    biglist, nbig, bigscr, words, ctr + 3, status);
+      launch_pdl(k_count, count_ctas, kMidThreads, count_smem, s, row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
+                 pbytes, gpat, l1, nl1, biglist, nbig, ctr + 8, status);
+      if (hub_dense)
+        launch_pdl(k_count_hub, num_sms(), kHubThreads, sizeof(HubSmem), s, row_ptr, col_idx, M, K, nnz, tm, tk, q,
+                   nact, nblk, pbytes, gpat, relb, biglist, nbig, ctr + 3, hublist2, hubch2, nhub2, status);
+      else
+        launch_pdl(k_count_big, big_ctas, kBigThreads, 0, s, row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
+                   pbytes, gpat, biglist, nbig, bigscr, words, ctr + 3, status);
       // B1-B5 for warp-path panels + the single-pass scans B2 / B4 for all panels
       launch_wbuild(tm, tk, s, row_ptr, col_idx, values, M, K, nnz, P, listed, nblk, pbytes, ticket, lb, h->brp,
                     poff, h->ac, h->sp, h->packed, status);
-      launch_pdl(k_emit, mid_ctas, kEmitThreads, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp, poff,
-                                               gpat, h->ac, h->sp, h->packed, l1, nl1, hublist, hubch, nhub, ctr + 5);
-      launch_pdl(k_emit_hubvals, mid_ctas, kEmitThreads, 0, s, row_ptr, col_idx, values, M, nnz, tm, tk, q, nact, h->brp,
-                                                       gpat, h->ac, h->sp, h->packed, hublist, hubch, nhub);
+      launch_pdl(k_emit, emit_ctas, kEmitNT, emit_smem, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp,
+                 poff, gpat, h->ac, h->sp, h->packed, l1, nl1, hublist, hubch, nhub, ctr + 5, (int)hub_dense);
+      if (hub_dense)
+        launch_pdl(k_emit_hub, mid_ctas, kEmitNT, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp,
+                   poff, gpat, relb, h->ac, h->sp, h->packed, hublist2, hubch2, nhub2);
+      else
+        launch_pdl(k_emit_hubvals, mid_ctas, kEmitThreads, 0, s, row_ptr, col_idx, values, M, nnz, tm, tk, q, nact,
+                   h->brp, gpat, h->ac, h->sp, h->packed, hublist, hubch, nhub);
       note_launch(6);
     }
     unsigned int* sticky_p = nullptr;
@@ -1808,7 +2241,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
 #endif
   }
   dfree(q, s); dfree(cnt, s); dfree(poff, s); dfree(gpat, s); dfree(biglist, s); dfree(info, s);
-  dfree(bigscr, s);
+  dfree(bigscr, s); dfree(relb, s); dfree(hub2, s);
   dfree(ctr, s); dfree(lb, s); dfree(listed, s);
   if (deferred_info) {
     h->NB = -1;  // unknown until build_finish

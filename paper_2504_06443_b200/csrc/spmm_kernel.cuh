@@ -298,6 +298,10 @@ struct PanelCursor {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
+__device__ __forceinline__ void cp_async16_hint(uint32_t dst, const void* src, uint32_t src_bytes, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src), "r"(src_bytes),
+               "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -385,6 +389,10 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     // contiguous 512-B row segment (lane = 16-B chunk); lanes 0..15 prefetch the block's activeCols 8 blocks
     // ahead and the row index is broadcast by shuffle.
     const uint64_t pol_a = policy_evict_first();
+#ifdef HRPB_HOT_EXP
+    uint64_t pol_hot, pol_cold = pol_a;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_hot));
+#endif
     const int na_eff = (int)min((int64_t)L::kNA, ceil_div(N - n0, 32));  // 32-col atoms with a column < N
     const int64_t b_begin = cbB, b_end = cbE;
     const int pw = warp;
@@ -479,10 +487,19 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
           const bool real = rk < Kr && !(dbg(prm, 16));  // sentinel K -> zero fill (src-size 0)
           const float* src = Blane + (uint64_t)(real ? rk : 0u) * ldb32;
           const uint32_t rowb = bt + (rw >> 2) * (L::kNA * 512) + (rw & 3) * 128;
+#ifdef HRPB_HOT_EXP  // experiment: L2 priority by an R-MAT popularity proxy (few one bits in the id)
+          const uint64_t pol = __popc(rk) <= HRPB_HOT_EXP ? pol_hot : pol_cold;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (t * 4 < na_eff)
+              cp_async16_hint(rowb + doff[t][rw & 3], src + 128 * t, (real && col_ok[t]) ? 16u : 0u, pol);
+          }
+#else
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             if (t * 4 < na_eff) cp_async16(rowb + doff[t][rw & 3], src + 128 * t, (real && col_ok[t]) ? 16u : 0u);
           }
+#endif
         }
         if (dbg(prm, 32)) mbar_arrive(&full_b[s]);
         else cp_async_arrive_noinc(&full_b[s]);
