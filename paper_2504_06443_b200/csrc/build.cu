@@ -1496,6 +1496,7 @@ constexpr int64_t kHubPassCols = 32 * kHubPassWords;  // 2^20 columns per pass
 constexpr int kHubGroups = kHubPassWords / 8;        // 4096 groups of 8 words (u8 prefix within a group)
 constexpr int kHubPatSlots = 2048;                   // brick-pattern window (u64 slots)
 constexpr int kHubBndWords = 1024;                   // per-row pass boundaries: TM x (passes + 1) <= this
+constexpr int kHubU = 4;                             // entries per thread in flight in the entry loops
 constexpr int kHubMetaChunk = 256;                   // blocks per metadata work item of k_emit_hub
 constexpr int kHubEntryChunk = 4096;                 // entries per value work item of k_emit_hub
 struct HubSmem {
@@ -1564,12 +1565,23 @@ __global__ void __launch_bounds__(kHubThreads) k_count_hub(const int64_t* __rest
     }
     __syncthreads();
     bool bad_range = false, bad_order = false;
-    for (int64_t e = e0 + tid; e < e1; e += kHubThreads) {
-      const int32_t c = ci[e];
+    for (int64_t eb = e0; eb < e1; eb += kHubThreads * kHubU) {
+     int32_t cvs[kHubU], cps[kHubU];
+#pragma unroll
+     for (int u = 0; u < kHubU; ++u) {  // (kHubU entries' loads in flight per thread)
+       const int64_t e = eb + u * kHubThreads + tid;
+       cvs[u] = e < e1 ? ci[e] : 0;
+       cps[u] = e < e1 && e > e0 ? ci[e - 1] : 0;
+     }
+#pragma unroll
+     for (int u = 0; u < kHubU; ++u) {
+      const int64_t e = eb + u * kHubThreads + tid;
+      if (e >= e1) continue;
+      const int32_t c = cvs[u];
       if (c < 0 || c >= K) bad_range = true;
       const int r = row_of(S.rp, nrows, e);
       const bool first = e == S.rp[r];
-      const int32_t cp = first ? 0 : ci[e - 1];
+      const int32_t cp = first ? 0 : cps[u];
       if (!first && cp >= c) bad_order = true;
       const int kc = (int)(min(max(c, 0), (int32_t)(K - 1)) / kHubPassCols);
       const int kp = first ? -1 : (int)(min(max(cp, 0), (int32_t)(K - 1)) / kHubPassCols);
@@ -1577,6 +1589,7 @@ __global__ void __launch_bounds__(kHubThreads) k_count_hub(const int64_t* __rest
       for (int k = kp + 1; k <= kc; ++k) S.bnd[r * nb1 + k] = (uint32_t)(e - e0);
       if (e + 1 == S.rp[r + 1])  // last entry: the row has nothing in later passes
         for (int k = kc + 1; k < npass; ++k) S.bnd[r * nb1 + k] = (uint32_t)(e + 1 - e0);
+     }
     }
     if (__any_sync(0xffffffffu, bad_range) && lane == 0) atomicOr(status, ST_COL_RANGE);
     if (__any_sync(0xffffffffu, bad_order) && lane == 0) atomicOr(status, ST_COL_ORDER);
@@ -1612,12 +1625,24 @@ __global__ void __launch_bounds__(kHubThreads) k_count_hub(const int64_t* __rest
       const int64_t c0 = (int64_t)k * kHubPassCols;
       for (int i = tid; i < kHubPassWords; i += kHubThreads) S.bits[i] = 0u;
       __syncthreads();
-      for (uint32_t i = tid; i < npe; i += kHubThreads) {  // set bits (warp-merged per word: dense hub rows)
-        const int r = hub_row_of(S.off, nrows, i);
-        const uint32_t e = S.bnd[r * nb1 + k] + (i - S.off[r]);
-        const int64_t c = min(max((int64_t)ci[e0 + e], (int64_t)0), K - 1) - c0;
-        const uint32_t w = (uint32_t)min(max(c, (int64_t)0), kHubPassCols - 1);
-        atomicOr(&S.bits[w >> 5], 1u << (w & 31));
+      for (uint32_t i0 = 0; i0 < npe; i0 += kHubThreads * kHubU) {  // set bits (kHubU loads in flight per thread)
+        int32_t cv[kHubU];
+#pragma unroll
+        for (int u = 0; u < kHubU; ++u) {
+          const uint32_t i = i0 + u * kHubThreads + tid;
+          cv[u] = -1;
+          if (i < npe) {
+            const int r = hub_row_of(S.off, nrows, i);
+            cv[u] = ci[e0 + S.bnd[r * nb1 + k] + (i - S.off[r])];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kHubU; ++u) {
+          if (i0 + u * kHubThreads + tid >= npe) continue;
+          const int64_t c = min(max((int64_t)cv[u], (int64_t)0), K - 1) - c0;
+          const uint32_t w = (uint32_t)min(max(c, (int64_t)0), kHubPassCols - 1);
+          atomicOr(&S.bits[w >> 5], 1u << (w & 31));
+        }
       }
       __syncthreads();
       {  // warp w: groups [256 w, 256 w + 256) of 8 words, 32 at a time (lane = group, two conflict-free 128-bit
@@ -1672,10 +1697,28 @@ __global__ void __launch_bounds__(kHubThreads) k_count_hub(const int64_t* __rest
         for (uint32_t j = max(jw, jwe) + tid; j < jend; j += kHubThreads)  // (beyond the window: zero, then OR)
           for (int i = 0; i < nbk; ++i) gp[(int64_t)j * nbk + i] = 0ull;
         __syncthreads();
-        for (uint32_t i = tid; i < npe; i += kHubThreads) {
-          const int r = hub_row_of(S.off, nrows, i);
-          const uint32_t e = S.bnd[r * nb1 + k] + (i - S.off[r]);
-          const int64_t c = min(max((int64_t)ci[e0 + e], (int64_t)0), K - 1) - c0;
+        for (uint32_t i0 = 0; i0 < npe; i0 += kHubThreads * kHubU) {
+         int rr[kHubU];
+         uint32_t ee[kHubU];
+         int32_t cv[kHubU];
+#pragma unroll
+         for (int u = 0; u < kHubU; ++u) {  // (kHubU entries' loads in flight per thread)
+           const uint32_t i = i0 + u * kHubThreads + tid;
+           rr[u] = 0;
+           ee[u] = 0;
+           cv[u] = 0;
+           if (i < npe) {
+             rr[u] = hub_row_of(S.off, nrows, i);
+             ee[u] = S.bnd[rr[u] * nb1 + k] + (i - S.off[rr[u]]);
+             cv[u] = ci[e0 + ee[u]];
+           }
+         }
+#pragma unroll
+         for (int u = 0; u < kHubU; ++u) {
+          if (i0 + u * kHubThreads + tid >= npe) continue;
+          const int r = rr[u];
+          const uint32_t e = ee[u];
+          const int64_t c = min(max((int64_t)cv[u], (int64_t)0), K - 1) - c0;
           const uint32_t w = (uint32_t)min(max(c, (int64_t)0), kHubPassCols - 1), wd = w >> 5;
           const uint32_t qq = S.gpre[wd >> 3] + S.pre8[wd] + __popc(S.bits[wd] & ((1u << (w & 31)) - 1u));
           q[e0 + e] = qq;
@@ -1688,6 +1731,7 @@ __global__ void __launch_bounds__(kHubThreads) k_count_hub(const int64_t* __rest
           } else {
             atomicOr(&gp[(int64_t)j * nbk + slot], 1ull << bit);
           }
+         }
         }
         base += tot;
       }

@@ -84,7 +84,12 @@ constexpr int kTraceSlots = 10;  // slot 8: per warp of CTA 0 {cycles waiting on
 #define HRPB_INSTRUMENT 0
 #endif
 constexpr bool kInstr = HRPB_INSTRUMENT != 0;
-__device__ __forceinline__ bool dbg(const SpmmParams& p, int bit) { return kInstr && (p.debug & bit); }
+#ifndef HRPB_EXP_SKIP
+#define HRPB_EXP_SKIP 0  // experiments only: HRPB_DEBUG bits compiled in as constants (no instrumentation overhead)
+#endif
+__device__ __forceinline__ bool dbg(const SpmmParams& p, int bit) {
+  return (HRPB_EXP_SKIP & bit) != 0 || (kInstr && (p.debug & bit));
+}
 __device__ __forceinline__ bool tracing(const SpmmParams& p) { return kInstr && p.trace != nullptr; }
 __device__ __forceinline__ void trace_ev(const SpmmParams& p, int slot, uint32_t i) {
   if (tracing(p) && blockIdx.x == 0 && i < kTraceN) p.trace[slot * kTraceN + i] = clock64();
@@ -391,7 +396,13 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     const uint64_t pol_a = policy_evict_first();
 #ifdef HRPB_HOT_EXP
     uint64_t pol_hot, pol_cold = pol_a;
+#if HRPB_HOT_POL == 0
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_hot));
+#elif HRPB_HOT_POL == 1
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_hot));
+#else
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 0.5;" : "=l"(pol_hot));
+#endif
 #endif
     const int na_eff = (int)min((int64_t)L::kNA, ceil_div(N - n0, 32));  // 32-col atoms with a column < N
     const int64_t b_begin = cbB, b_end = cbE;
