@@ -1846,6 +1846,53 @@ __global__ void __launch_bounds__(kEmitNT) k_emit_hub(const int64_t* __restrict_
     }
     const int64_t c0e = e0 + (int64_t)(item - nmeta) * kHubEntryChunk;
     const int64_t c1e = min(e1, c0e + kHubEntryChunk);
+    if (nbk == 4) {  // TM = TK = 16: kHubU entries per thread, each stage's loads issued before they are used
+      for (int64_t eb = c0e; eb < c1e; eb += kEmitNT * kHubU) {
+        uint32_t qq[kHubU];
+        int32_t cv[kHubU];
+        float vv[kHubU];
+#pragma unroll
+        for (int u = 0; u < kHubU; ++u) {
+          const int64_t e = eb + u * kEmitNT + threadIdx.x;
+          qq[u] = 0xFFFFFFFFu;
+          if (e < c1e) {
+            qq[u] = q[e];
+            cv[u] = ci[e];
+            vv[u] = vals[e];
+          }
+        }
+        uint64_t w[kHubU][4];
+        uint32_t rl[kHubU];
+#pragma unroll
+        for (int u = 0; u < kHubU; ++u) {
+          const uint32_t j = qq[u] < nact ? qq[u] >> tk_sh : 0u;
+          const uint64_t* pt = gp + (int64_t)j * 4;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) w[u][i] = pt[i];
+          rl[u] = rel[j];
+        }
+#pragma unroll
+        for (int u = 0; u < kHubU; ++u) {
+          if (qq[u] >= nact) continue;  // (padding items; invalid CSR input)
+          const int64_t e = eb + u * kEmitNT + threadIdx.x;
+          const int r = row_of(s_rp, nrows, e);
+          const uint32_t j = qq[u] >> tk_sh, lc = qq[u] & (tk - 1);
+          ac[((int64_t)b0 + j) * tk + lc] = (uint32_t)cv[u];
+          const int bit = ((r & 15) << 2) | (lc & 3);
+          const int mine = (int)(lc >> 2);
+          uint32_t nbr = 0, off = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            nbr += w[u][i] != 0ull;
+            if (i < mine) off += __popcll(w[u][i]);
+          }
+          off += __popcll(w[u][mine & 3] & ((1ull << bit) - 1ull));
+          const uint32_t hdr = (nbc + 1 + nbr + 7) & ~7u;
+          reinterpret_cast<float*>(packed + pbase + rl[u] + hdr + 8 * nbr)[off] = vv[u];
+        }
+      }
+      continue;
+    }
     for (int64_t e = c0e + threadIdx.x; e < c1e; e += kEmitNT) {
       const uint32_t qq = q[e];
       const int32_t c = ci[e];
