@@ -124,7 +124,12 @@ struct SmemLayout {
   static constexpr int kARawBytes = ((((kNbc + 1 + kNbk + 7) & ~7) + 8 * kNbk + 4 * TMV * TKV) + 127) & ~127;
   static constexpr int kATileBytes = TMV * TKV * 4;  // TM x TK fp32 decoded block
   static constexpr int kLbo = TMV * 16;              // bytes between 4-column K groups of the decoded tile
-  static constexpr int kStage = kBTile + kARawBytes + kATileBytes;
+  // decode in place (the tile overwrites its own raw block) when a lane holds all its items' values at once: the
+  // stage then needs no separate tile (c2a at TM = 64: 12 -> 16 stages; the kernel is latency-bound on its ring)
+  static constexpr int kItems = TMV * kNbc / 32;
+  static constexpr bool kInPlace = kItems <= 8;
+  static_assert(!kInPlace || kARawBytes >= kATileBytes, "the raw slot must hold the decoded tile");
+  static constexpr int kStage = kBTile + kARawBytes + (kInPlace ? 0 : kATileBytes);
   // TMEM accumulator slots (panels in flight between the MMA warp and the epilogue): up to 4
   static constexpr int kSlots = 4 * NT * TMV <= 512 ? 4 : 2;
   static_assert(kSlots % (NT <= 2 ? kMmaWarps : 1) == 0, "a TMEM slot must always be used by the same MMA warp");
@@ -327,8 +332,9 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   const int S = prm.stages;
   uint8_t* btile0 = smem;                                 // S x kBTile (1024-aligned)
   uint8_t* araw0 = smem + (size_t)S * L::kBTile;          // S x kARawBytes
-  uint8_t* atile0 = araw0 + (size_t)S * kARawBytes;       // S x kATileBytes
-  uint64_t* bars = (uint64_t*)(atile0 + (size_t)S * kATileBytes);
+  uint8_t* atile0 = L::kInPlace ? araw0 : araw0 + (size_t)S * kARawBytes;  // decoded tiles (in place: the raw slots)
+  constexpr int kATileStride = L::kInPlace ? kARawBytes : kATileBytes;
+  uint64_t* bars = (uint64_t*)(araw0 + (size_t)S * kARawBytes + (L::kInPlace ? 0 : (size_t)S * kATileBytes));
   uint64_t* full_a = bars;
   uint64_t* full_b = bars + S;
   uint64_t* empty = bars + 2 * S;
@@ -542,7 +548,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
         continue;
       }
       const uint8_t* blk = araw0 + (size_t)s * kARawBytes;
-      float* tile = reinterpret_cast<float*>(atile0 + (size_t)s * kATileBytes);
+      float* tile = reinterpret_cast<float*>(atile0 + (size_t)s * kATileStride);
       const uint64_t cp = *reinterpret_cast<const uint64_t*>(blk);  // colPtr[0..7] (bytes)
       const uint32_t nbr = blk[L::kNbc];                            // colPtr[nbc] = stored bricks
       const uint32_t hdr = (L::kNbc + 1 + nbr + 7) & ~7u;
@@ -582,11 +588,8 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       // nibble of the brick pattern selects up to 4 values at prefix-popcount ranks; one 16-B store
       // per item into the K-major tile. Branch-free: every item's loads are issued before any is consumed, so a
       // block costs ~3 dependent shared-memory round trips (a divergent per-item branch serialised them).
-      constexpr int kItems = TMV * L::kNbc / 32;
-#ifndef HRPB_DEC_CHUNK
-#define HRPB_DEC_CHUNK 8
-#endif
-      constexpr int kChunk = kItems < HRPB_DEC_CHUNK ? kItems : HRPB_DEC_CHUNK;  // items in flight per lane
+      constexpr int kItems = L::kItems;
+      constexpr int kChunk = kItems < 8 ? kItems : 8;  // items in flight per lane (all of them when in place)
       const uint32_t* __restrict__ uvals = reinterpret_cast<const uint32_t*>(vals);
 #pragma unroll
       for (int j0 = 0; j0 < kItems; j0 += kChunk) {
@@ -611,6 +614,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
           iv[jj] = make_uint4(uvals[i0], uvals[i1], uvals[i2], uvals[i3]);
           inib[jj] = nib;
         }
+        if constexpr (L::kInPlace) __syncwarp();  // every lane has read the raw block before the tile overwrites it
 #pragma unroll
         for (int jj = 0; jj < kChunk; ++jj) {
           const int q = lane + 32 * (j0 + jj), r = q % TMV, bc = q / TMV;
@@ -697,11 +701,13 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
             mbar_arrive(&empty[s]);
           } else {
             const uint64_t ad = adesc0 + (uint64_t)(st * (uint32_t)(L::kBTile >> 4));
-            const uint64_t bd = bdesc0 + (uint64_t)(st * (uint32_t)(kATileBytes >> 4));
+            const uint64_t bd = bdesc0 + (uint64_t)(st * (uint32_t)(kATileStride >> 4));
+            // K step outer, N tile inner: consecutive MMAs write different accumulators (independent), so the
+            // tensor pipe need not wait for one accumulation before starting the next
 #pragma unroll
-            for (int t = 0; t < NT; ++t) {
+            for (int g = 0; g < TKV / 8; ++g) {
 #pragma unroll
-              for (int g = 0; g < TKV / 8; ++g)
+              for (int t = 0; t < NT; ++t)
                 umma_tf32(dcol + t * TMV, ad + (uint64_t)(((2 * g * L::kNA + 4 * t) * 512) >> 4),
                           bd + (uint64_t)((g * 2 * L::kLbo) >> 4), kIdesc, (b > bb || g > 0) ? 1u : 0u);
             }
