@@ -598,6 +598,7 @@ __device__ __forceinline__ void warp_panel_patterns(const WarpPanel& w, uint8_t*
   uint32_t* pat32 = reinterpret_cast<uint32_t*>(my + L.off_pat);
   constexpr int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
   constexpr int tk_sh = tk == 16 ? 4 : 5;
+  __syncwarp();  // every lane is done reading the previous chunk's patterns
   for (int i = lane; i < 2 * (int)nb * (nbk + 1); i += 32) pat32[i] = 0u;
   __syncwarp();
   const uint32_t q0 = jb0 * tk, q1 = min((jb0 + nb) * tk, w.nact);

@@ -305,6 +305,9 @@ struct PanelCursor {
   }
 };
 
+// cross-warp progress words of the MMA issuers: shared-memory atomics (a plain volatile flag is a data race)
+__device__ __forceinline__ void st_relaxed_cta(uint32_t* p, uint32_t v) { atomicExch(p, v); }
+__device__ __forceinline__ uint32_t ld_relaxed_cta(uint32_t* p) { return atomicAdd(p, 0u); }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   uint64_t* tempty = tfull + 4;
   uint32_t* misc = (uint32_t*)(tempty + 4);  // [0] tmem base
   int64_t* range = (int64_t*)(misc + 2);     // CtaWork: pa, pb, bB, bE, first_full, last_full
-  volatile uint32_t* mma_prog = (volatile uint32_t*)(range + 6);  // [kMmaWarps] next block each MMA warp waits for
+  uint32_t* mma_prog = (uint32_t*)(range + 6);  // [kMmaWarps] next block each MMA warp waits for (relaxed atomics)
   // per decoder warp: brick-slot table (pattern, value offset) of the block being decoded
   uint64_t* slot_pat = (uint64_t*)(range + 6 + kMmaWarps);     // [kDecWarps][kNbk]
   uint32_t* slot_off = (uint32_t*)(slot_pat + kDecWarps * L::kNbk);  // [kDecWarps][kNbk]
@@ -365,7 +368,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     for (int i = 0; i < L::kSlots; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     fence_mbar_init();
 
-    for (int m = 0; m < kMmaWarps; ++m) mma_prog[m] = 0u;
+    for (int m = 0; m < kMmaWarps; ++m) st_relaxed_cta(&mma_prog[m], 0u);
     prefetch_tmap(&tmB);
   }
   if (warp == kMmaWarp) tmem_alloc(&misc[0], tmem_cols);
@@ -673,14 +676,14 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       uint32_t i = (uint32_t)(bb - b_begin);  // block index within this CTA's range
       uint32_t st = i % Su, ph = (i / Su) & 1u;
       if (kSplit > 1 && lane == 0) {
-        mma_prog[mw] = i;  // all of this warp's blocks before its new panel are consumed
+        st_relaxed_cta(&mma_prog[mw], i);  // all of this warp's blocks before its new panel are consumed
         const uint32_t last = i + (be - bb) - 1u;
         if (last >= Su) {
           const long long tg = tracing(prm) ? clock64() : 0;
 #pragma unroll
           for (int m = 0; m < kSplit; ++m)
             if (m != mw)
-              while (mma_prog[m] <= last - Su) {
+              while (ld_relaxed_cta(&mma_prog[m]) <= last - Su) {
               }
           if (tracing(prm)) wacc += clock64() - tg;
         }
@@ -691,7 +694,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       const uint32_t dcol = tbase + slot * NT * TMV;
       for (uint32_t b = bb; b < be; ++b, ++i) {
         const int s = (int)st;
-        if (kSplit > 1 && lane == 0) mma_prog[mw] = i;
+        if (kSplit > 1 && lane == 0) st_relaxed_cta(&mma_prog[mw], i);
         mbar_wait_acc(prm, &full_b[s], ph, wacc);
         tc_fence_after();
         if (lane == 0) {
@@ -721,7 +724,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       __syncwarp();
       ++pc;
     }
-    if (kMmaWarps > 1 && lane == 0) mma_prog[mw] = 0xFFFFFFFFu;
+    if (kMmaWarps > 1 && lane == 0) st_relaxed_cta(&mma_prog[mw], 0xFFFFFFFFu);
   } else {
     // ---------------------------------------------------------------- epilogue (last 4 warps)
     const int qd = warp & 3;            // TMEM lane quadrant accessible to this warp
@@ -870,7 +873,9 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     return e ? atoi(e) : 0;
   }();
   if (stage_cap >= kDecWarps && stage_cap < stages) stages = stage_cap - stage_cap % kDecWarps;
-  const size_t smem = smem_for(stages);
+  // at least half of the SM's shared memory: one CTA per SM, so a second resident CTA can never block in
+  // tcgen05.alloc on the TMEM columns the first one holds (TM = 128 at N > 128 allocates all 512)
+  const size_t smem = smem_for(stages) > 116 * 1024 ? smem_for(stages) : 116 * 1024;
   if (smem > 227 * 1024) return HRPB_ERROR_NOT_SUPPORTED;  // (not reachable with the instantiated NT / TM / TK)
   static std::atomic<uint64_t> attr_set{0};  // per device: an attribute applies to the current device only
   if (first_on_device(attr_set)) {
