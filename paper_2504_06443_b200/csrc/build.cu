@@ -1093,8 +1093,19 @@ struct MidWin {
   uint32_t bits[kMaxWin * 32];        // bitmap words
   uint32_t pre[kMaxWin * 32];         // exclusive popcount prefix per word
 };
+// two-level bitmap over the whole column space (K <= 32 * 32 * kWordOccWords): occ2 = one bit per 32-column word,
+// the occupied words get dense ordinals (popcount prefix, u16: <= kSmallCap of them), mask[ordinal] = the word's
+// column bits, mpre = exclusive popcount prefix over the masks; rank = mpre[ord] + popc(mask[ord] & lower bits)
+constexpr int kWordOccWords = 4096;  // K <= 2^22
+struct Mid2L {
+  uint32_t occ2[kWordOccWords];
+  uint16_t opre[kWordOccWords];
+  uint32_t mask[kSmallCap];
+  uint16_t mpre[kSmallCap];
+};
 union MidUnion {
   MidWin win;
+  Mid2L two;
   typename MidSort::TempStorage sort;
   typename MidSort2::TempStorage sort2;
 };
@@ -1278,6 +1289,66 @@ __global__ void __launch_bounds__(kMidThreads, HRPB_COUNT_MINB) k_count(const in
         const uint32_t c = S.col[i];
         const uint32_t wd = (S.q[i] << (kWinBits - 5)) | ((c >> 5) & ((1u << (kWinBits - 5)) - 1u));
         S.q[i] = S.u.win.pre[wd] + __popc(S.u.win.bits[wd] & ((1u << (c & 31)) - 1u));
+      }
+    } else if (K <= 32ll * 32 * kWordOccWords) {
+      // ---- two-level bitmap (scattered columns, e.g. R-MAT): O(E + K / 1024) shared-memory work per panel
+      Mid2L& T = S.u.two;
+      __syncthreads();  // (occpre readers done before the union is reused)
+      for (int i = tid; i < kWordOccWords / 4; i += kMidThreads) reinterpret_cast<uint4*>(T.occ2)[i] = make_uint4(0, 0, 0, 0);
+      for (int i = tid; i < E; i += kMidThreads) T.mask[i] = 0u;
+      __syncthreads();
+      for (int i = tid; i < E; i += kMidThreads) {
+        const uint32_t w = S.col[i] >> 5;
+        atomicOr(&T.occ2[w >> 5], 1u << (w & 31));
+      }
+      __syncthreads();
+      constexpr int kPer = kWordOccWords / kMidThreads;  // occupancy words per thread (16)
+      {
+        uint32_t cnt[kPer], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kPer / 4; ++k) {
+          const uint4 v = reinterpret_cast<const uint4*>(T.occ2)[tid * (kPer / 4) + k];
+          cnt[4 * k] = __popc(v.x); cnt[4 * k + 1] = __popc(v.y); cnt[4 * k + 2] = __popc(v.z); cnt[4 * k + 3] = __popc(v.w);
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) sum += cnt[k];
+        uint32_t nocc;
+        uint32_t run = block_excl_scan<kMidThreads>(sum, &nocc, s_scan);
+#pragma unroll
+        for (int k = 0; k < kPer; k += 2) {
+          reinterpret_cast<uint32_t*>(T.opre)[(tid * kPer + k) >> 1] = run | ((run + cnt[k]) << 16);
+          run += cnt[k] + cnt[k + 1];
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < E; i += kMidThreads) {
+        const uint32_t c = S.col[i], w = c >> 5;
+        const uint32_t o = T.opre[w >> 5] + __popc(T.occ2[w >> 5] & ((1u << (w & 31)) - 1u));
+        S.q[i] = o;
+        atomicOr(&T.mask[o], 1u << (c & 31));
+      }
+      __syncthreads();
+      {
+        constexpr int kPerM = kSmallCap / kMidThreads;  // masks per thread (8)
+        uint32_t cnt[kPerM], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kPerM; ++k) {
+          const int o = tid * kPerM + k;
+          cnt[k] = o < E ? __popc(T.mask[o]) : 0u;
+          sum += cnt[k];
+        }
+        uint32_t run = block_excl_scan<kMidThreads>(sum, &nact, s_scan);
+#pragma unroll
+        for (int k = 0; k < kPerM; ++k) {
+          const int o = tid * kPerM + k;
+          if (o < E) T.mpre[o] = (uint16_t)run;
+          run += cnt[k];
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < E; i += kMidThreads) {
+        const uint32_t c = S.col[i], o = S.q[i];
+        S.q[i] = T.mpre[o] + __popc(T.mask[o] & ((1u << (c & 31)) - 1u));
       }
     } else {
       // ---- CTA radix sort of (column, entry); padding keys sort last (stable sort, entry >= E)
@@ -1797,6 +1868,257 @@ __global__ void __launch_bounds__(kHubThreads) k_count_hub(const int64_t* __rest
   }
 }
 
+// ------------------------------------------------------------------ hub panels, two-level bitmap (K <= 2^23)
+// One CTA per hub panel (claimed dynamically). Ranks (R23: ascending distinct columns) from a two-level
+// bitmap over the whole column space instead of dense passes: occ2 holds one bit per 32-column word, the occupied
+// words get dense ordinals (popcount prefix over occ2), mask[ordinal] collects the word's column bits and
+// mpre[ordinal] = ranks before the word, so rank = mpre[o] + popc(mask[o] & lower bits). Work per panel is
+// O(entries + K / 1024) shared-memory operations: three passes over the entries (word bits; column bits; ranks and
+// brick patterns) plus two prefix scans. Entries are staged in shared memory when they fit (kH2Stage), the masks
+// when the occupied words fit (kH2OrdCap, else this CTA's global scratch). Brick patterns of the first blocks
+// go to a shared-memory window, later blocks to global memory by atomics. Outputs as k_count_hub (q, patterns,
+// block-relative byte offsets, counts, k_emit_hub work items).
+constexpr int kH2Threads = 512;
+constexpr int kH2OccWords = 8192;  // one bit per 32-column word: K <= 2^23
+constexpr int kH2OrdCap = 8192;    // occupied words whose masks stay in shared memory
+constexpr int kH2Stage = 8192;     // entries staged in shared memory
+constexpr int kH2PatSlots = 2048;  // brick-pattern window (u64 slots)
+constexpr int kH2U = 4;            // entries per thread in flight in the global entry loops
+struct Hub2Smem {
+  uint32_t occ2[kH2OccWords];
+  uint32_t opre[kH2OccWords];
+  uint32_t mask[kH2OrdCap];
+  uint32_t mpre[kH2OrdCap];
+  uint32_t col[kH2Stage];
+  unsigned long long pat[kH2PatSlots];
+  uint8_t row[kH2Stage];
+  int64_t rp[129];
+  uint32_t scan[kH2Threads / 32 + 1];
+  uint32_t t;
+};
+__host__ __device__ inline bool hub2_ok(int64_t K) { return K <= 32ll * 32 * kH2OccWords; }
+
+__global__ void __launch_bounds__(kH2Threads, 1) k_count_hub2(const int64_t* __restrict__ rp,
+                                                             const int32_t* __restrict__ ci, int64_t M, int64_t K,
+                                                             int64_t nnz, int tm, int tk, uint32_t* __restrict__ q,
+                                                             uint32_t* __restrict__ nact_out,
+                                                             uint32_t* __restrict__ nblk_out,
+                                                             uint32_t* __restrict__ pbytes_out,
+                                                             uint64_t* __restrict__ gpat, uint32_t* __restrict__ relb,
+                                                             const uint32_t* __restrict__ biglist,
+                                                             const uint32_t* __restrict__ nbig, uint32_t* work,
+                                                             uint32_t* __restrict__ hublist,
+                                                             uint32_t* __restrict__ hubch,
+                                                             unsigned long long* __restrict__ nhub,
+                                                             uint32_t* __restrict__ scratch, uint32_t* status) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  Hub2Smem& S = *reinterpret_cast<Hub2Smem*>(dsm);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t count = *nbig;
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const int tk_sh = tk == 16 ? 4 : 5;
+  const int cap_blk = kH2PatSlots / nbk;  // blocks in the pattern window
+  const int64_t W = ceil_div(K, 32);      // 32-column words
+  uint32_t* const gmask = scratch + (size_t)blockIdx.x * 2 * W;  // masks / prefixes beyond kH2OrdCap words
+  uint32_t* const gmpre = gmask + W;
+  constexpr int kPer = kH2OccWords / kH2Threads;  // occupancy words per thread in the prefix scan (16)
+  for (int i = tid; i < kH2OccWords / 4; i += kH2Threads) reinterpret_cast<uint4*>(S.occ2)[i] = make_uint4(0, 0, 0, 0);
+  while (true) {
+    if (tid == 0) S.t = atomicAdd(work, 1u);
+    __syncthreads();
+    const uint32_t t = S.t;
+    if (t >= count) break;
+    const int64_t p = biglist[t];
+    load_panel_rows(rp, M, nnz, tm, p, S.rp, status);  // (barriers: also orders S.t's read and occ2's clearing)
+    const int nrows = (int)min((int64_t)tm, M - p * tm);
+    const int64_t e0 = S.rp[0], e1 = S.rp[nrows];
+    const uint32_t E = (uint32_t)(e1 - e0);
+    const bool staged = E <= (uint32_t)kH2Stage;
+    // (1) validation, staging, word-occupancy bits; each thread's entries ascend, so its row only
+    // moves forward
+    {
+      bool bad_range = false, bad_order = false;
+      int r = 0;
+      for (uint32_t i0 = 0; i0 < E; i0 += kH2Threads * kH2U) {
+        int32_t cv[kH2U], pv[kH2U];
+#pragma unroll
+        for (int u = 0; u < kH2U; ++u) {
+          const uint32_t i = i0 + u * kH2Threads + tid;
+          cv[u] = i < E ? ci[e0 + i] : 0;
+          pv[u] = (lane == 0 && i < E && i > 0) ? ci[e0 + i - 1] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kH2U; ++u) {
+          const uint32_t i = i0 + u * kH2Threads + tid;
+          const int32_t up = __shfl_up_sync(0xffffffffu, cv[u], 1);  // entry i - 1 (lane 0: loaded)
+          if (i >= E) continue;
+          const int64_t e = e0 + i;
+          while (S.rp[r + 1] <= e) ++r;
+          const int32_t c = cv[u];
+          if (c < 0 || c >= K) bad_range = true;
+          if (e != S.rp[r] && (lane ? up : pv[u]) >= c) bad_order = true;
+          const uint32_t cc = (uint32_t)min(max(c, 0), (int32_t)(K - 1));
+          if (staged) {
+            S.col[i] = cc;
+            S.row[i] = (uint8_t)r;
+          }
+          const uint32_t w = cc >> 5;
+          atomicOr(&S.occ2[w >> 5], 1u << (w & 31));
+        }
+      }
+      if (__any_sync(0xffffffffu, bad_range) && lane == 0) atomicOr(status, ST_COL_RANGE);
+      if (__any_sync(0xffffffffu, bad_order) && lane == 0) atomicOr(status, ST_COL_ORDER);
+    }
+    __syncthreads();
+    // (2) dense ordinals of the occupied words (thread: kPer consecutive occupancy words)
+    uint32_t nocc;
+    {
+      uint32_t cnt[kPer], sum = 0;
+#pragma unroll
+      for (int k = 0; k < kPer / 4; ++k) {
+        const uint4 v = reinterpret_cast<const uint4*>(S.occ2)[tid * (kPer / 4) + k];
+        cnt[4 * k] = __popc(v.x); cnt[4 * k + 1] = __popc(v.y); cnt[4 * k + 2] = __popc(v.z); cnt[4 * k + 3] = __popc(v.w);
+      }
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) sum += cnt[k];
+      uint32_t run = block_excl_scan<kH2Threads>(sum, &nocc, S.scan);
+#pragma unroll
+      for (int k = 0; k < kPer / 4; ++k) {
+        uint4 v;
+        v.x = run; run += cnt[4 * k];
+        v.y = run; run += cnt[4 * k + 1];
+        v.z = run; run += cnt[4 * k + 2];
+        v.w = run; run += cnt[4 * k + 3];
+        reinterpret_cast<uint4*>(S.opre)[tid * (kPer / 4) + k] = v;
+      }
+    }
+    const bool in_smem = nocc <= (uint32_t)kH2OrdCap;
+    uint32_t* const mask = in_smem ? S.mask : gmask;
+    uint32_t* const mpre = in_smem ? S.mpre : gmpre;
+    for (uint32_t o = tid; o < nocc; o += kH2Threads) mask[o] = 0u;
+    __syncthreads();
+    auto ordinal = [&](uint32_t c) {
+      const uint32_t w = c >> 5;
+      return S.opre[w >> 5] + __popc(S.occ2[w >> 5] & ((1u << (w & 31)) - 1u));
+    };
+    // (3) column bits of the occupied words
+    if (staged) {
+      for (uint32_t i = tid; i < E; i += kH2Threads) {
+        const uint32_t c = S.col[i];
+        atomicOr(&S.mask[ordinal(c)], 1u << (c & 31));  // (staged: nocc <= E <= kH2OrdCap)
+      }
+    } else {
+      for (uint32_t i0 = 0; i0 < E; i0 += kH2Threads * kH2U) {
+        int32_t cv[kH2U];
+#pragma unroll
+        for (int u = 0; u < kH2U; ++u) {
+          const uint32_t i = i0 + u * kH2Threads + tid;
+          cv[u] = i < E ? ci[e0 + i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kH2U; ++u) {
+          if (i0 + u * kH2Threads + tid >= E) continue;
+          const uint32_t c = (uint32_t)min(max(cv[u], 0), (int32_t)(K - 1));
+          atomicOr(&mask[ordinal(c)], 1u << (c & 31));
+        }
+      }
+    }
+    __syncthreads();
+    // (4) ranks before each occupied word (thread: a contiguous range of ordinals)
+    uint32_t nact;
+    {
+      const uint32_t per = (nocc + kH2Threads - 1) / kH2Threads;
+      const uint32_t o0 = min((uint32_t)tid * per, nocc), o1 = min(o0 + per, nocc);
+      uint32_t sum = 0;
+      for (uint32_t o = o0; o < o1; ++o) sum += __popc(mask[o]);
+      uint32_t run = block_excl_scan<kH2Threads>(sum, &nact, S.scan);
+      for (uint32_t o = o0; o < o1; ++o) {
+        const uint32_t v = __popc(mask[o]);
+        mpre[o] = run;
+        run += v;
+      }
+    }
+    const uint32_t nblk = (nact + tk - 1) >> tk_sh;
+    unsigned long long* gp = reinterpret_cast<unsigned long long*>(gpat + pat_base(e0, p, nbk, tk));
+    for (int i = tid; i < cap_blk * nbk; i += kH2Threads) S.pat[i] = 0ull;
+    for (int64_t i = (int64_t)cap_blk * nbk + tid; i < (int64_t)nblk * nbk; i += kH2Threads) gp[i] = 0ull;
+    __syncthreads();
+    // (5) ranks and brick patterns (bit (r % 16) * 4 + q % 4 of brick (q % TK / 4, r / 16), R3 / R4)
+    auto rank_entry = [&](uint32_t i, uint32_t c, int r) {
+      const uint32_t o = ordinal(c);
+      const uint32_t qq = mpre[o] + __popc(mask[o] & ((1u << (c & 31)) - 1u));
+      q[e0 + i] = qq;
+      const uint32_t j = qq >> tk_sh, lc = qq & (tk - 1);
+      const int bit = ((r & 15) << 2) | (int)(lc & 3);
+      const int slot = (int)(lc >> 2) * nbrow + (r >> 4);
+      if (j < (uint32_t)cap_blk)
+        atomicOr(reinterpret_cast<uint32_t*>(&S.pat[j * nbk + slot]) + (bit >> 5), 1u << (bit & 31));
+      else
+        atomicOr(&gp[(int64_t)j * nbk + slot], 1ull << bit);
+    };
+    if (staged) {
+      for (uint32_t i = tid; i < E; i += kH2Threads) rank_entry(i, S.col[i], S.row[i]);
+    } else {
+      int r = 0;
+      for (uint32_t i0 = 0; i0 < E; i0 += kH2Threads * kH2U) {
+        int32_t cv[kH2U];
+#pragma unroll
+        for (int u = 0; u < kH2U; ++u) {
+          const uint32_t i = i0 + u * kH2Threads + tid;
+          cv[u] = i < E ? ci[e0 + i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kH2U; ++u) {
+          const uint32_t i = i0 + u * kH2Threads + tid;
+          if (i >= E) continue;
+          while (S.rp[r + 1] <= e0 + (int64_t)i) ++r;
+          rank_entry(i, (uint32_t)min(max(cv[u], 0), (int32_t)(K - 1)), r);
+        }
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    // (6) block sizes and panel-relative byte offsets; the window's patterns go out to global memory
+    uint32_t* rel = relb + rel_base(e0, p, tk);
+    uint32_t bytes = 0;
+    for (uint32_t c2 = 0; c2 < nblk; c2 += kH2Threads) {
+      const uint32_t j = c2 + tid;
+      uint32_t size = 0;
+      if (j < nblk) {
+        uint32_t nbr = 0, nz = 0;
+        for (int i = 0; i < nbk; ++i) {
+          unsigned long long v;
+          if (j < (uint32_t)cap_blk) {
+            v = S.pat[j * nbk + i];
+            gp[(int64_t)j * nbk + i] = v;
+          } else {
+            v = __ldcg(&gp[(int64_t)j * nbk + i]);
+          }
+          nbr += v != 0ull;
+          nz += __popcll(v);
+        }
+        size = block_bytes(nbc, nbr, nz);
+      }
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<kH2Threads>(size, &tot, S.scan);
+      if (j < nblk) rel[j] = bytes + ex;
+      bytes += tot;
+    }
+    __syncthreads();
+    for (int i = tid; i < kH2OccWords / 4; i += kH2Threads) reinterpret_cast<uint4*>(S.occ2)[i] = make_uint4(0, 0, 0, 0);
+    if (tid == 0) {
+      nact_out[p] = nact;
+      nblk_out[p] = nblk;
+      pbytes_out[p] = bytes;
+      const unsigned long long items = (unsigned long long)(ceil_div(nblk, kHubMetaChunk) + ceil_div(E, kHubEntryChunk));
+      const unsigned long long old = atomicAdd(nhub, (1ull << 32) + items);
+      hublist[old >> 32] = (uint32_t)p;
+      hubch[old >> 32] = (uint32_t)old;
+    }
+  }
+}
+
 // Hub panels' output, after the global scan: every CTA takes items of one flat list (per hub: its block-metadata
 // chunks — sizePtr = panel offset + relative offset, HRPB-v1 headers, patterns, padding, sentinel activeCols —
 // then its 4096-entry value chunks — activeCols and values at popcount ranks).
@@ -2243,10 +2565,12 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     const char* e = getenv("HRPB_HUB_GLOBAL");  // experiments: the global-bitmap hub path
     return e && atoi(e);
   }();
-  const bool hub_dense = hub_dense_ok(K, tm) && !force_old_hub;
-  uint32_t* bigscr = hub_dense ? (uint32_t*)dalloc(16, s)
-                               : (uint32_t*)dalloc((size_t)big_ctas * (2 * words + 2 * ((words + 31) / 32)) *
-                                                   sizeof(uint32_t), s);
+  const bool hub_2l = hub2_ok(K) && !force_old_hub;
+  const bool hub_dense = (hub_2l || hub_dense_ok(K, tm)) && !force_old_hub;
+  uint32_t* bigscr = hub_2l ? (uint32_t*)dalloc((size_t)num_sms() * 2 * ceil_div(K, 32) * sizeof(uint32_t) + 16, s)
+                     : hub_dense ? (uint32_t*)dalloc(16, s)
+                                 : (uint32_t*)dalloc((size_t)big_ctas * (2 * words + 2 * ((words + 31) / 32)) *
+                                                     sizeof(uint32_t), s);
   uint32_t* relb = (uint32_t*)dalloc((nnz / tk + 2 * P + 4) * sizeof(uint32_t), s);  // hub blocks' relative offsets
   uint32_t* hub2 = (uint32_t*)dalloc(2 * (P + 1) * sizeof(uint32_t), s);
   hrpb_status_t st = HRPB_SUCCESS;
@@ -2277,6 +2601,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
       cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(k_count_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HubSmem));
+      cudaFuncSetAttribute(k_count_hub2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Hub2Smem));
     }
     const unsigned wgrid = (unsigned)ceil_div(P, kWWarps);
     const int mid_ctas = 8 * num_sms();
@@ -2290,7 +2615,10 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
       launch_wclassify(tm, tk, wgrid, s, row_ptr, col_idx, M, nnz, P, listed, l1, nl1);
       launch_pdl(k_count, count_ctas, kMidThreads, count_smem, s, row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
                  pbytes, gpat, l1, nl1, biglist, nbig, ctr + 8, status);
-      if (hub_dense)
+      if (hub_2l)
+        launch_pdl(k_count_hub2, num_sms(), kH2Threads, sizeof(Hub2Smem), s, row_ptr, col_idx, M, K, nnz, tm, tk, q,
+                   nact, nblk, pbytes, gpat, relb, biglist, nbig, ctr + 3, hublist2, hubch2, nhub2, bigscr, status);
+      else if (hub_dense)
         launch_pdl(k_count_hub, num_sms(), kHubThreads, sizeof(HubSmem), s, row_ptr, col_idx, M, K, nnz, tm, tk, q,
                    nact, nblk, pbytes, gpat, relb, biglist, nbig, ctr + 3, hublist2, hubch2, nhub2, status);
       else

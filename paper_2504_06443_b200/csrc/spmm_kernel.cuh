@@ -38,7 +38,15 @@ constexpr int kMmaWarps = HRPB_MMA_WARPS;                  // non-empty panel pc
 constexpr int kEpiWarp0 = kMmaWarp + kMmaWarps;            // warps 10..13: epilogue
 constexpr int kSpmmThreads = 32 * (kEpiWarp0 + 4);        // 448
 constexpr int kMaxStages = 24;
-constexpr int kPfRing = 8;  // producer look-ahead in own blocks (x4 producer warps = 32 blocks)
+#ifndef HRPB_L2PF
+#define HRPB_L2PF 0
+#endif
+// experiment (off): L2 prefetch distance in own blocks — the producer bulk-prefetches the B rows of its block kL2Pf
+// blocks ahead into L2 (cp.async.bulk.prefetch.L2, no shared memory held). Measured slower at every distance
+// (2 / 4 / 8: c4 5.68 -> 8.3 / 10.0 / 10.0 ms, c2a TM = 64 0.247 -> 0.338 ms, c3 19.1 -> 19.4 ms): the prefetches
+// queue in the same bulk-copy path as the A blocks
+constexpr int kL2Pf = HRPB_L2PF;
+constexpr int kPfRing = 8 + kL2Pf;  // producer look-ahead ring in own blocks (x4 producer warps)
 
 // per-call scratch of hrpb_spmm: split-panel workspace, its flag word and this call's epoch
 struct Scratch {
@@ -315,6 +323,9 @@ __device__ __forceinline__ void cp_async16_hint(uint32_t dst, const void* src, u
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src), "r"(src_bytes),
                "l"(pol) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {  // bytes: multiple of 16
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -463,11 +474,22 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
 #pragma unroll
     for (int q = 0; q < kPfRing; ++q) fetch(b + 4 * q, q);
     int q = 0;
+    // prefetched row segment: this CTA's columns [n0, n0 + 128 NT) of a B row, whole 16-B chunks only
+    const int64_t pf_cols = min((int64_t)(128 * NT), prm.N - n0);
+    const uint32_t pf_bytes = (uint32_t)((pf_cols * 4) & ~15ll);
 #pragma unroll 1
     for (; b < b_end; b += 4) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(kPfRing - 1) : "memory");
+      // the groups of blocks b .. b + 4 kL2Pf are complete (one group per block, kPfRing committed ahead)
+      asm volatile("cp.async.wait_group %0;" ::"n"(kPfRing - 1 - kL2Pf) : "memory");
       __syncwarp();
       const uint32_t* slot = myring + q * kSlotW;
+      if constexpr (kL2Pf > 0) {
+        const int qp = q + kL2Pf < kPfRing ? q + kL2Pf : q + kL2Pf - kPfRing;
+        if (lane < TKV && b + 4 * kL2Pf < b_end && pf_bytes) {
+          const uint32_t rk = myring[qp * kSlotW + 4 + lane];
+          if (rk < Kr) prefetch_l2_bulk(Bsrc + (uint64_t)rk * ldb32, pf_bytes);
+        }
+      }
       mbar_wait_acc(prm, &empty[s], ph ^ 1, wacc);
       if (lane == 0) {
         trace_ev(prm, 0, (uint32_t)(b - b_begin));

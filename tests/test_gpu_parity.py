@@ -111,6 +111,56 @@ def test_builder_span_boundaries(tm):
     assert_same_hrpb(A, oracle.csr_to_hrpb(M, K, rp, ci, v, tm=tm), f"spans tm={tm}")
 
 
+@pytest.mark.parametrize("K,tm", [(10 ** 6 + 7, 16), (10 ** 6 + 7, 64), (10 ** 6 + 7, 128), (2 ** 22 + 3, 16),
+                                  (2 ** 23, 32), (2 ** 23 + 5, 16)])
+def test_builder_listed_and_hub_paths(K, tm):
+    # scattered (R-MAT-like) panels of every listed size class: CTA path (<= 2048 entries: windowed, two-level
+    # word bitmap for K <= 2^22, else radix sort) and hub panels (two-level bitmap for K <= 2^23 with staged /
+    # streamed entries, masks in shared / global memory, brick patterns in the window / by global atomics;
+    # dense column passes above 2^23); panel sizes straddle the class boundaries
+    rng = np.random.default_rng(K % 1000 + tm)
+    per_row_total = [300, 2047, 2049, 8000, 8300, 20000, 40000]
+    cols = []
+    for tot in per_row_total:
+        for r in range(tm):
+            k = max(1, tot // tm + int(rng.integers(-2, 3)))
+            lo = 0 if r % 3 else K // 2  # hub-like rows next to rows confined to the upper half
+            c = np.sort(rng.choice(K - lo, min(k, K - lo), replace=False)) + lo
+            cols.append(c.astype(np.int32))
+    M = len(cols) + 5  # ragged tail: 5 empty rows
+    cols += [np.zeros(0, np.int32)] * 5
+    rp = np.zeros(M + 1, np.int64)
+    rp[1:] = np.cumsum([len(c) for c in cols])
+    ci = np.concatenate(cols)
+    v = rng.standard_normal(ci.size).astype(np.float32)
+    A = gpu_build(M, K, rp, ci, v, tm=tm)
+    assert_same_hrpb(A, oracle.csr_to_hrpb(M, K, rp, ci, v, tm=tm), f"K={K} tm={tm}")
+
+
+@pytest.mark.parametrize("E", [4000, 12000])
+@pytest.mark.parametrize("defect", ["unsorted", "duplicate", "range"])
+def test_builder_hub2_rejects_invalid_csr(E, defect):
+    # the two-level hub path with staged (4000) and streamed (12000) entries: every defect is reported
+    rng = np.random.default_rng(E)
+    K = 3 * 10 ** 6
+    cols = [np.sort(rng.choice(K, E // 16, replace=False)).astype(np.int32) for _ in range(16)]
+    r = cols[9].copy()
+    if defect == "unsorted":
+        r[40], r[41] = r[41], r[40]
+    elif defect == "duplicate":
+        r[41] = r[40]
+    else:
+        r[-1] = K
+    cols[9] = r
+    rp = np.zeros(17, np.int64)
+    rp[1:] = np.cumsum([len(c) for c in cols])
+    ci = np.concatenate(cols)
+    v = rng.standard_normal(ci.size).astype(np.float32)
+    with pytest.raises(hp.HrpbError) as e:
+        gpu_build(16, K, rp, ci, v)
+    assert e.value.status == 2
+
+
 def test_builder_rejects_invalid_csr():
     M, K = 40, 50
     rp, ci, v = rand_csr(M, K, 0.2, 1)
