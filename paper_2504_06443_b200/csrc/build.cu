@@ -1170,7 +1170,8 @@ __global__ void __launch_bounds__(kMidThreads, HRPB_COUNT_MINB) k_count(const in
                                                       const uint32_t* __restrict__ midlist,
                                                       const uint32_t* __restrict__ nmid,
                                                       uint32_t* __restrict__ biglist,
-                                                      uint32_t* __restrict__ nbig, uint32_t* work, uint32_t* status) {
+                                                      uint32_t* __restrict__ nbig, uint32_t* work, uint32_t* status,
+                                                      uint32_t* __restrict__ nhuge, int64_t huge_cap, int64_t P) {
   pdl_wait();
   extern __shared__ __align__(16) uint8_t dsm[];
   MidSmem& S = *reinterpret_cast<MidSmem*>(dsm);
@@ -1195,8 +1196,12 @@ __global__ void __launch_bounds__(kMidThreads, HRPB_COUNT_MINB) k_count(const in
     const int nrows = (int)min((int64_t)tm, M - p * tm);
     const int64_t e0 = s_rp[0];
     const int E = (int)min((int64_t)kSmallCap + 1, s_rp[nrows] - e0);
-    if (E > kSmallCap) {  // CTA-uniform: handled by k_count_big
-      if (tid == 0) biglist[atomicAdd(nbig, 1u)] = (uint32_t)p;
+    if (E > kSmallCap) {  // CTA-uniform: handled by the hub kernel
+      // (huge_cap > 0: panels above it are listed from the end of biglist, so the hub kernel claims them first)
+      if (tid == 0) {
+        if (huge_cap > 0 && s_rp[nrows] - e0 > huge_cap) biglist[P - atomicAdd(nhuge, 1u)] = (uint32_t)p;
+        else biglist[atomicAdd(nbig, 1u)] = (uint32_t)p;
+      }
       continue;
     }
     // entries -> shared memory (column clamped into [0, K) for memory safety; invalid CSR is flagged), row map
@@ -1878,12 +1883,22 @@ __global__ void __launch_bounds__(kHubThreads) k_count_hub(const int64_t* __rest
 // when the occupied words fit (kH2OrdCap, else this CTA's global scratch). Brick patterns of the first blocks
 // go to a shared-memory window, later blocks to global memory by atomics. Outputs as k_count_hub (q, patterns,
 // block-relative byte offsets, counts, k_emit_hub work items).
-constexpr int kH2Threads = 512;
+#ifndef HRPB_H2_THREADS
+#define HRPB_H2_THREADS 1024  // (512: c3 hub 1.84 ms, 1024: 1.57 ms)
+#endif
+constexpr int kH2Threads = HRPB_H2_THREADS;
+#ifndef HRPB_H2_MINB
+#define HRPB_H2_MINB 1             // CTAs per SM (2 with 4096-entry caps: c3 hub 2.03 -> 2.34 ms)
+#endif
 constexpr int kH2OccWords = 8192;  // one bit per 32-column word: K <= 2^23
 constexpr int kH2OrdCap = 8192;    // occupied words whose masks stay in shared memory
 constexpr int kH2Stage = 8192;     // entries staged in shared memory
 constexpr int kH2PatSlots = 2048;  // brick-pattern window (u64 slots)
-constexpr int kH2U = 4;            // entries per thread in flight in the global entry loops
+constexpr int64_t kH2Huge = 65536; // panels with more entries are claimed first (the critical path of the kernel)
+#ifndef HRPB_H2_U
+#define HRPB_H2_U 4
+#endif
+constexpr int kH2U = HRPB_H2_U;    // entries per thread in flight in the global entry loops
 struct Hub2Smem {
   uint32_t occ2[kH2OccWords];
   uint32_t opre[kH2OccWords];
@@ -1898,7 +1913,7 @@ struct Hub2Smem {
 };
 __host__ __device__ inline bool hub2_ok(int64_t K) { return K <= 32ll * 32 * kH2OccWords; }
 
-__global__ void __launch_bounds__(kH2Threads, 1) k_count_hub2(const int64_t* __restrict__ rp,
+__global__ void __launch_bounds__(kH2Threads, HRPB_H2_MINB) k_count_hub2(const int64_t* __restrict__ rp,
                                                              const int32_t* __restrict__ ci, int64_t M, int64_t K,
                                                              int64_t nnz, int tm, int tk, uint32_t* __restrict__ q,
                                                              uint32_t* __restrict__ nact_out,
@@ -1910,12 +1925,13 @@ __global__ void __launch_bounds__(kH2Threads, 1) k_count_hub2(const int64_t* __r
                                                              uint32_t* __restrict__ hublist,
                                                              uint32_t* __restrict__ hubch,
                                                              unsigned long long* __restrict__ nhub,
-                                                             uint32_t* __restrict__ scratch, uint32_t* status) {
+                                                             uint32_t* __restrict__ scratch, uint32_t* status,
+                                                             const uint32_t* __restrict__ nhuge, int64_t P) {
   pdl_wait();
   extern __shared__ __align__(16) uint8_t dsm[];
   Hub2Smem& S = *reinterpret_cast<Hub2Smem*>(dsm);
-  const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t count = *nbig;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nh = *nhuge, count = *nbig + nh;
   const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
   const int tk_sh = tk == 16 ? 4 : 5;
   const int cap_blk = kH2PatSlots / nbk;  // blocks in the pattern window
@@ -1929,7 +1945,7 @@ __global__ void __launch_bounds__(kH2Threads, 1) k_count_hub2(const int64_t* __r
     __syncthreads();
     const uint32_t t = S.t;
     if (t >= count) break;
-    const int64_t p = biglist[t];
+    const int64_t p = t < nh ? biglist[P - t] : biglist[t - nh];  // the largest panels first (listed from the end)
     load_panel_rows(rp, M, nnz, tm, p, S.rp, status);  // (barriers: also orders S.t's read and occ2's clearing)
     const int nrows = (int)min((int64_t)tm, M - p * tm);
     const int64_t e0 = S.rp[0], e1 = S.rp[nrows];
@@ -2025,18 +2041,30 @@ __global__ void __launch_bounds__(kH2Threads, 1) k_count_hub2(const int64_t* __r
       }
     }
     __syncthreads();
-    // (4) ranks before each occupied word (thread: a contiguous range of ordinals)
+    // (4) ranks before each occupied word: warp w scans a contiguous range of ordinals, 32 consecutive at a time
     uint32_t nact;
     {
-      const uint32_t per = (nocc + kH2Threads - 1) / kH2Threads;
-      const uint32_t o0 = min((uint32_t)tid * per, nocc), o1 = min(o0 + per, nocc);
+      constexpr int kWarps = kH2Threads / 32;
+      const uint32_t per = ((nocc + kWarps - 1) / kWarps + 31) & ~31u;
+      const uint32_t o0 = min((uint32_t)warp * per, nocc), o1 = min(o0 + per, nocc);
       uint32_t sum = 0;
-      for (uint32_t o = o0; o < o1; ++o) sum += __popc(mask[o]);
-      uint32_t run = block_excl_scan<kH2Threads>(sum, &nact, S.scan);
-      for (uint32_t o = o0; o < o1; ++o) {
-        const uint32_t v = __popc(mask[o]);
-        mpre[o] = run;
-        run += v;
+#pragma unroll 4
+      for (uint32_t o = o0 + lane; o < o1; o += 32) sum += __popc(mask[o]);
+#pragma unroll
+      for (int k = 16; k; k >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, k);
+      uint32_t run = block_excl_scan<kH2Threads>(lane == 0 ? sum : 0u, &nact, S.scan);
+      run = __shfl_sync(0xffffffffu, run, 0);
+      for (uint32_t ob = o0; ob < o1; ob += 32) {
+        const uint32_t o = ob + lane;
+        const uint32_t v = o < o1 ? __popc(mask[o]) : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int k = 1; k < 32; k <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, k);
+          if (lane >= k) x += y;
+        }
+        if (o < o1) mpre[o] = run + x - v;
+        run += __shfl_sync(0xffffffffu, x, 31);
       }
     }
     const uint32_t nblk = (nact + tk - 1) >> tk_sh;
@@ -2136,19 +2164,30 @@ __global__ void __launch_bounds__(kEmitNT) k_emit_hub(const int64_t* __restrict_
                                                      const unsigned long long* __restrict__ nhub) {
   pdl_wait();
   __shared__ int64_t s_rp[129];
+  __shared__ uint32_t s_hub;
   const unsigned long long hc = *nhub;
   const uint32_t count = (uint32_t)(hc >> 32), total = (uint32_t)hc;
   const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
   const int tk_sh = tk == 16 ? 4 : 5;
   for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
-    uint32_t lo = 0, hi = count - 1;  // last hub t with hubch[t] <= g
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi + 1) >> 1;
-      if (hubch[mid] <= g) lo = mid; else hi = mid - 1;
+    if (threadIdx.x < 32) {  // last hub t with hubch[t] <= g: 32-way search by warp 0 (3 dependent loads at 12K hubs)
+      const int lane = threadIdx.x;
+      uint32_t lo = 0, n = count;  // answer in [lo, lo + n)
+      while (n > 1) {
+        const uint32_t step = (n + 31) / 32;
+        const uint32_t i = lo + lane * step;
+        const bool le = i < lo + n && hubch[i] <= g;
+        const uint32_t k = 31 - __clz(__ballot_sync(0xffffffffu, le) | 1u);  // last probe <= g (probe 0 always is)
+        lo += k * step;
+        n = min(step, n - k * step);
+      }
+      if (lane == 0) s_hub = lo;
     }
-    const int64_t p = hublist[lo];
-    const uint32_t item = g - hubch[lo];
-    load_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);  // (barriers)
+    __syncthreads();
+    const uint32_t hub = s_hub;
+    const int64_t p = hublist[hub];
+    const uint32_t item = g - hubch[hub];
+    load_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);  // (barriers: also orders s_hub's reads before its reuse)
     const int nrows = (int)min((int64_t)tm, M - p * tm);
     const int64_t e0 = s_rp[0], e1 = s_rp[nrows];
     const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0, nact = nact_in[p];
@@ -2173,6 +2212,7 @@ __global__ void __launch_bounds__(kEmitNT) k_emit_hub(const int64_t* __restrict_
     const int64_t c0e = e0 + (int64_t)(item - nmeta) * kHubEntryChunk;
     const int64_t c1e = min(e1, c0e + kHubEntryChunk);
     if (nbk == 4) {  // TM = TK = 16: kHubU entries per thread, each stage's loads issued before they are used
+      int r = row_of(s_rp, nrows, c0e + threadIdx.x < c1e ? c0e + threadIdx.x : c0e);  // then only moves forward
       for (int64_t eb = c0e; eb < c1e; eb += kEmitNT * kHubU) {
         uint32_t qq[kHubU];
         int32_t cv[kHubU];
@@ -2201,7 +2241,7 @@ __global__ void __launch_bounds__(kEmitNT) k_emit_hub(const int64_t* __restrict_
         for (int u = 0; u < kHubU; ++u) {
           if (qq[u] >= nact) continue;  // (padding items; invalid CSR input)
           const int64_t e = eb + u * kEmitNT + threadIdx.x;
-          const int r = row_of(s_rp, nrows, e);
+          while (s_rp[r + 1] <= e) ++r;
           const uint32_t j = qq[u] >> tk_sh, lc = qq[u] & (tk - 1);
           ac[((int64_t)b0 + j) * tk + lc] = (uint32_t)cv[u];
           const int bit = ((r & 15) << 2) | (lc & 3);
@@ -2567,7 +2607,8 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   }();
   const bool hub_2l = hub2_ok(K) && !force_old_hub;
   const bool hub_dense = (hub_2l || hub_dense_ok(K, tm)) && !force_old_hub;
-  uint32_t* bigscr = hub_2l ? (uint32_t*)dalloc((size_t)num_sms() * 2 * ceil_div(K, 32) * sizeof(uint32_t) + 16, s)
+  const int hub2_ctas = HRPB_H2_MINB * num_sms();
+  uint32_t* bigscr = hub_2l ? (uint32_t*)dalloc((size_t)hub2_ctas * 2 * ceil_div(K, 32) * sizeof(uint32_t) + 16, s)
                      : hub_dense ? (uint32_t*)dalloc(16, s)
                                  : (uint32_t*)dalloc((size_t)big_ctas * (2 * words + 2 * ((words + 31) / 32)) *
                                                      sizeof(uint32_t), s);
@@ -2614,10 +2655,11 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
       // classification; listed panels counted by a CTA (<= kSmallCap entries) or the hub bitmap kernel
       launch_wclassify(tm, tk, wgrid, s, row_ptr, col_idx, M, nnz, P, listed, l1, nl1);
       launch_pdl(k_count, count_ctas, kMidThreads, count_smem, s, row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
-                 pbytes, gpat, l1, nl1, biglist, nbig, ctr + 8, status);
+                 pbytes, gpat, l1, nl1, biglist, nbig, ctr + 8, status, ctr + 12, hub_2l ? kH2Huge : (int64_t)0, P);
       if (hub_2l)
-        launch_pdl(k_count_hub2, num_sms(), kH2Threads, sizeof(Hub2Smem), s, row_ptr, col_idx, M, K, nnz, tm, tk, q,
-                   nact, nblk, pbytes, gpat, relb, biglist, nbig, ctr + 3, hublist2, hubch2, nhub2, bigscr, status);
+        launch_pdl(k_count_hub2, hub2_ctas, kH2Threads, sizeof(Hub2Smem), s, row_ptr, col_idx, M, K, nnz, tm, tk, q,
+                   nact, nblk, pbytes, gpat, relb, biglist, nbig, ctr + 3, hublist2, hubch2, nhub2, bigscr, status,
+                   ctr + 12, P);
       else if (hub_dense)
         launch_pdl(k_count_hub, num_sms(), kHubThreads, sizeof(HubSmem), s, row_ptr, col_idx, M, K, nnz, tm, tk, q,
                    nact, nblk, pbytes, gpat, relb, biglist, nbig, ctr + 3, hublist2, hubch2, nhub2, status);
