@@ -1895,6 +1895,7 @@ constexpr int kH2OrdCap = 8192;    // occupied words whose masks stay in shared 
 constexpr int kH2Stage = 8192;     // entries staged in shared memory
 constexpr int kH2PatSlots = 2048;  // brick-pattern window (u64 slots)
 constexpr int64_t kH2Huge = 65536; // panels with more entries are claimed first (the critical path of the kernel)
+constexpr int kE2Slots = 2048;     // brick slots (blocks x TM/16 x TK/4) per k_emit_hub2 work item
 #ifndef HRPB_H2_U
 #define HRPB_H2_U 4
 #endif
@@ -2139,10 +2140,161 @@ __global__ void __launch_bounds__(kH2Threads, HRPB_H2_MINB) k_count_hub2(const i
       nact_out[p] = nact;
       nblk_out[p] = nblk;
       pbytes_out[p] = bytes;
-      const unsigned long long items = (unsigned long long)(ceil_div(nblk, kHubMetaChunk) + ceil_div(E, kHubEntryChunk));
+      const unsigned long long items = (unsigned long long)ceil_div(nblk, kE2Slots / nbk);  // k_emit_hub2 items
       const unsigned long long old = atomicAdd(nhub, (1ull << 32) + items);
       hublist[old >> 32] = (uint32_t)p;
       hubch[old >> 32] = (uint32_t)old;
+    }
+  }
+}
+
+// Hub panels' output (after k_count_hub2 and the global scan), in block order: work item = kE2Slots / nbk
+// consecutive blocks of one hub. The item stages its blocks' patterns in shared memory, writes their sizePtr,
+// HRPB-v1 headers, patterns and padding, then finds in every row the entries whose ranks fall in its blocks (one
+// contiguous range per row: ranks ascend along a row, R23) and writes their activeCols and values at popcount
+// ranks — the stores of an item land in one contiguous output region.
+constexpr int kE2Threads = 512;
+constexpr int kE2U = 4;  // entries per thread in flight
+__global__ void __launch_bounds__(kE2Threads, 3) k_emit_hub2(const int64_t* __restrict__ rp,
+                                                         const int32_t* __restrict__ ci,
+                                                         const float* __restrict__ vals, int64_t M, int64_t K,
+                                                         int64_t nnz, int tm, int tk, const uint32_t* __restrict__ q,
+                                                         const uint32_t* __restrict__ nact_in,
+                                                         const uint32_t* __restrict__ brp,
+                                                         const uint64_t* __restrict__ poff,
+                                                         const uint64_t* __restrict__ gpat,
+                                                         const uint32_t* __restrict__ relb, uint32_t* __restrict__ ac,
+                                                         uint64_t* __restrict__ sp, uint8_t* __restrict__ packed,
+                                                         const uint32_t* __restrict__ hublist,
+                                                         const uint32_t* __restrict__ hubch,
+                                                         const unsigned long long* __restrict__ nhub) {
+  pdl_wait();
+  __shared__ int64_t s_rp[129];
+  __shared__ unsigned long long s_pt[kE2Slots];
+  __shared__ uint16_t s_so[kE2Slots];
+  __shared__ uint64_t s_vb[kE2Slots / 4];
+  __shared__ uint32_t s_seg[128];
+  __shared__ uint32_t s_off[129];
+  __shared__ uint32_t s_hub;
+  const unsigned long long hc = *nhub;
+  const uint32_t count = (uint32_t)(hc >> 32), total = (uint32_t)hc;
+  const int tid = threadIdx.x;
+  const int nbc = tk / HRPB_BRICK_K, nbrow = tm / HRPB_BRICK_M, nbk = nbc * nbrow;
+  const int tk_sh = tk == 16 ? 4 : 5;
+  const uint32_t bpi = (uint32_t)(kE2Slots / nbk);  // blocks per item
+  for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
+    if (tid < 32) {  // last hub t with hubch[t] <= g: 32-way search by warp 0
+      uint32_t lo = 0, n = count;
+      while (n > 1) {
+        const uint32_t step = (n + 31) / 32;
+        const uint32_t i = lo + tid * step;
+        const bool le = i < lo + n && hubch[i] <= g;
+        const uint32_t k = 31 - __clz(__ballot_sync(0xffffffffu, le) | 1u);
+        lo += k * step;
+        n = min(step, n - k * step);
+      }
+      if (tid == 0) s_hub = lo;
+    }
+    __syncthreads();
+    const uint32_t hub = s_hub;
+    const int64_t p = hublist[hub];
+    const uint32_t item = g - hubch[hub];
+    load_panel_rows(rp, M, nnz, tm, p, s_rp, nullptr);  // (barriers)
+    const int nrows = (int)min((int64_t)tm, M - p * tm);
+    const int64_t e0 = s_rp[0];
+    const uint32_t b0 = brp[p], nblk = brp[p + 1] - b0, nact = nact_in[p];
+    const uint64_t pbase = poff[p];
+    const uint64_t* gp = gpat + pat_base(e0, p, nbk, tk);
+    const uint32_t* rel = relb + rel_base(e0, p, tk);
+    const uint32_t j0 = item * bpi, j1 = min(j0 + bpi, nblk), nb = j1 > j0 ? j1 - j0 : 0u;
+    for (uint32_t i = tid; i < nb * nbk; i += kE2Threads) s_pt[i] = gp[(int64_t)j0 * nbk + i];
+    {  // row r (warp r % 16): its entries with ranks in [j0 TK, j1 TK), by 32-way lower-bound searches on the
+       // ascending ranks of the row (~3 dependent loads per search)
+      const int lane = tid & 31;
+      for (int r = tid >> 5; r < nrows; r += kE2Threads / 32) {
+        const int64_t rb = s_rp[r], re = s_rp[r + 1];
+        auto lower = [&](uint32_t x) {  // first e in [rb, re) with q[e] >= x
+          int64_t lo = rb, n = re - rb;  // answer in [lo, lo + n]
+          while (n > 0) {
+            const int64_t step = (n + 31) / 32;
+            const int64_t i = lo + (int64_t)lane * step;
+            const bool lt = i < lo + n && q[i] < x;
+            const int k = __popc(__ballot_sync(0xffffffffu, lt));  // probes below x (a prefix of the lanes)
+            if (k == 0) break;
+            lo += (int64_t)(k - 1) * step + 1;
+            n = min(step - 1, re - lo);
+          }
+          return lo;
+        };
+        const int64_t a = lower(j0 << tk_sh), b = max(a, lower(j1 << tk_sh));
+        if (lane == 0) {
+          s_seg[r] = (uint32_t)(a - e0);
+          s_off[r] = (uint32_t)(b - a);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {  // flattened entry ranges: exclusive prefix over the rows
+      uint32_t carry = 0;
+      for (int r0 = 0; r0 < nrows; r0 += 32) {
+        const int r = r0 + tid;
+        const uint32_t len = r < nrows ? s_off[r] : 0u;
+        uint32_t tot;
+        const uint32_t ex = warp_excl_scan(len, &tot);
+        if (r < nrows) s_off[r] = carry + ex;
+        carry += tot;
+      }
+      if (tid == 0) s_off[nrows] = carry;
+    }
+    if (tid < nb) {  // block j0 + tid: sizePtr, header, patterns, padding, its values' base and brick offsets
+      const unsigned long long* pj = s_pt + tid * nbk;
+      uint32_t nbr = 0, nz = 0;
+      for (int i = 0; i < nbk; ++i) {
+        s_so[tid * nbk + i] = (uint16_t)nz;
+        nbr += pj[i] != 0ull;
+        nz += __popcll(pj[i]);
+      }
+      const uint32_t j = j0 + tid;
+      const uint64_t off = pbase + rel[j];
+      sp[b0 + j] = off;
+      emit_block_meta_dyn(packed + off, pj, nbc, nbrow, nbr, nz, block_bytes(nbc, nbr, nz));
+      s_vb[tid] = off + ((nbc + 1 + nbr + 7) & ~7u) + 8 * nbr;
+      if (j + 1 == nblk)
+        for (uint32_t t = nact; t < nblk * (uint32_t)tk; ++t) ac[(int64_t)b0 * tk + t] = (uint32_t)K;
+    }
+    __syncthreads();
+    const uint32_t ne = s_off[nrows];
+    int r = 0;
+    for (uint32_t i0 = 0; i0 < ne; i0 += kE2Threads * kE2U) {
+      uint32_t qq[kE2U];
+      int32_t cv[kE2U];
+      float vv[kE2U];
+      int rr[kE2U];
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) {
+        const uint32_t i = i0 + u * kE2Threads + tid;
+        qq[u] = 0xFFFFFFFFu;
+        rr[u] = 0;
+        if (i < ne) {
+          while (s_off[r + 1] <= i) ++r;
+          rr[u] = r;
+          const int64_t e = e0 + s_seg[r] + (i - s_off[r]);
+          qq[u] = q[e];
+          cv[u] = ci[e];
+          vv[u] = vals[e];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) {
+        const uint32_t jj = qq[u] >> tk_sh;
+        if (qq[u] >= nact || jj < j0 || jj >= j1) continue;  // (only for invalid CSR input)
+        const uint32_t jl = jj - j0, lc = qq[u] & (tk - 1);
+        ac[((int64_t)b0 + jj) * tk + lc] = (uint32_t)cv[u];
+        const int bit = ((rr[u] & 15) << 2) | (int)(lc & 3);
+        const uint32_t slot = jl * nbk + (lc >> 2) * nbrow + (rr[u] >> 4);
+        const uint32_t off = s_so[slot] + __popcll(s_pt[slot] & ((1ull << bit) - 1ull));
+        reinterpret_cast<float*>(packed + s_vb[jl])[off] = vv[u];
+      }
     }
   }
 }
@@ -2671,7 +2823,10 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
                     poff, h->ac, h->sp, h->packed, status);
       launch_pdl(k_emit, emit_ctas, kEmitNT, emit_smem, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp,
                  poff, gpat, h->ac, h->sp, h->packed, l1, nl1, hublist, hubch, nhub, ctr + 5, (int)hub_dense);
-      if (hub_dense)
+      if (hub_2l)
+        launch_pdl(k_emit_hub2, 3 * num_sms(), kE2Threads, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact,
+                   h->brp, poff, gpat, relb, h->ac, h->sp, h->packed, hublist2, hubch2, nhub2);
+      else if (hub_dense)
         launch_pdl(k_emit_hub, mid_ctas, kEmitNT, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp,
                    poff, gpat, relb, h->ac, h->sp, h->packed, hublist2, hubch2, nhub2);
       else
