@@ -245,7 +245,7 @@ def run_reference(args, rank, world):
               f"oracle CSR SpMM (FP64 acc, OpenMP)")
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.workload], "sample_rows": rows},
             "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": th, "kind": "oracle", "sample": sample,
@@ -543,7 +543,7 @@ def run_ours(args, rank, world, local_rank):
         roof["note"] = "rank 0's SpMM; times are the max over ranks"
     line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "tf32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "tf32",
             "data": "synthetic (seeded generators, synth/)",
             "config": {"workload": WORKLOADS[args.workload], "nnz": int(total_nnz), "N": N, "M": M, "K": K,
                        "TM": tm, "TK": 16, "TM_choice": "library (hrpb_config_t.tm = 0)" if args.tm == 0 else "fixed",
@@ -608,7 +608,7 @@ def run_cpu_check(args, rank, world):
     if rank == 0:
         print(json.dumps({"impl": "cpu-check", "n_gpus": world, "world": world, "rows": rows, "M": w.M, "nnz": nnz,
                           "total_nnz": w.nnz, "parity": ok, "ms": round(dt * 1e3, 3),
-                          "scaling": "strong" if world > 1 else "weak"}), flush=True)
+                          "scaling": "strong"}), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -12,7 +12,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 }
 
 template <int N, int AMAJ>
-__global__ void rate(int R, long long* out) {
+__global__ void rate(int R, int nacc, long long* out) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar;
@@ -24,7 +24,7 @@ __global__ void rate(int R, long long* out) {
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tslot)), "r"(128));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tslot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
@@ -38,9 +38,9 @@ __global__ void rate(int R, long long* out) {
     const uint64_t ad = AMAJ ? sdesc(su32(sm), 512, 2048, 1) : sdesc(su32(sm), 2048, 128, 0);
     const uint64_t bd = sdesc(su32(sm + 32768), N * 16, 128, 0);
     long long t0 = clock64();
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r < R; ++r) {  // nacc independent accumulators (TMEM columns tb + k N), round robin
       asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }"
-                   ::"r"(tb), "l"(ad), "l"(bd), "r"(idesc), "r"(r) : "memory");
+                   ::"r"(tb + (uint32_t)((r % nacc) * N)), "l"(ad), "l"(bd), "r"(idesc), "r"((int)(r >= nacc)) : "memory");
     }
     long long t1 = clock64();
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
@@ -53,26 +53,27 @@ __global__ void rate(int R, long long* out) {
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(128));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512));
 }
 
 template <int N, int AMAJ>
-void run(const char* name) {
+void run(const char* name, int nacc = 1) {
   long long* d;
   cudaMalloc(&d, 16);
   const int R = 20000;
   cudaFuncSetAttribute(rate<N, AMAJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024);
-  rate<N, AMAJ><<<148, 128, 70 * 1024>>>(R, d);
+  rate<N, AMAJ><<<148, 128, 70 * 1024>>>(R, nacc, d);
   cudaDeviceSynchronize();
   long long h[2];
   cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-  printf("%-32s issue %6.1f cyc/MMA, complete %6.1f cyc/MMA  (%s)\n", name, (double)h[0] / R, (double)h[1] / R,
+  printf("%-32s acc %d  issue %6.1f cyc/MMA, complete %6.1f cyc/MMA  (%s)\n", name, nacc, (double)h[0] / R, (double)h[1] / R,
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
 
 int main() {
-  run<16, 1>("M128 N16 K8 A=MN SW128_32B");
+  for (int a : {1, 2, 4, 8}) run<16, 1>("M128 N16 K8 A=MN SW128_32B", a);
+  for (int a : {1, 2, 4}) run<64, 1>("M128 N64 K8 A=MN SW128_32B", a);
   run<16, 0>("M128 N16 K8 A=K  none");
   run<64, 1>("M128 N64 K8 A=MN SW128_32B");
   run<64, 0>("M128 N64 K8 A=K  none");

@@ -1,8 +1,8 @@
 """Summarise ncu --set full reports into a markdown table + the per-kernel DRAM traffic JSON bench.py reads.
 
 usage: python tools/ncu_summary.py OUT_MD WORKLOAD_TAG REP [REP ...] [--traffic]
-(--traffic also records each kernel's DRAM bytes per launch in profiles/ncu_traffic.json; k_spmm is keyed by
- its TM template argument, k_spmm_tm<TM>, because bench.py picks TM per run)
+(--traffic also records each kernel's DRAM bytes per launch in profiles/ncu_traffic.json under
+ [WORKLOAD_TAG][kernel name], the key bench.py looks up: tag = "<config>_N<N>_tm<TM>", e.g. c3_N256_tm16)
 """
 import csv
 import io
@@ -45,7 +45,7 @@ def main():
     write_traffic = "--traffic" in sys.argv
     out_md, tag, reps = args[0], args[1], args[2:]
     rows = [d for rep in reps for d in read(rep)]
-    lines = ["| kernel | time us | DRAM read MB | DRAM write MB | DRAM % | L2 % | L2 hit % | L1 % | SM % | tensor % | warps % | regs | grid x block |",
+    lines = [f"\n**{tag}**\n", "| kernel | time us | DRAM read MB | DRAM write MB | DRAM % | L2 % | L2 hit % | L1 % | SM % | tensor % | warps % | regs | grid x block |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
                                 "ncu_traffic.json")
@@ -59,13 +59,10 @@ def main():
                      f"{g('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed'):.2f} | "
                      f"{g('sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} | {g('launch__registers_per_thread'):.0f} | "
                      f"{g('launch__grid_size'):.0f} x {g('launch__block_size'):.0f} |")
-        full = d["kernel"].replace("void ", "").split("::")[-1]
-        name = full.split("<")[0].strip()
-        if name == "k_spmm" and "<" in full:  # k_spmm<NT, GM, TM>
-            name += "_tm" + full.split("<")[1].rstrip(">").split(",")[2].strip()  # k_spmm<NT, GM, TM, TK>
-        traffic[name] = {"workload": tag,
-                         "dram_bytes_per_launch": int(g("dram__bytes_read.sum") + g("dram__bytes_write.sum")),
-                         "ncu_time_us": round(g("gpu__time_duration.sum") * 1e6, 2)}
+        name = d["kernel"].replace("void ", "").split("::")[-1].split("<")[0].strip()
+        traffic.setdefault(tag, {})[name] = {
+            "dram_bytes_per_launch": int(g("dram__bytes_read.sum") + g("dram__bytes_write.sum")),
+            "ncu_time_us": round(g("gpu__time_duration.sum") * 1e6, 2)}
     open(out_md, "a").write("\n".join(lines) + "\n")
     if write_traffic:
         json.dump(traffic, open(traffic_path, "w"), indent=1)
