@@ -81,7 +81,11 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
   if (r != CUDA_SUCCESS) return HRPB_ERROR_INVALID_VALUE;
   // columns per launch: NT <= 4, or <= 2 at TK = 32 (twice the stage size) and TM = 128 (two TMEM slots of
   // 2 x 128 columns fill the 512 TMEM columns)
-  const int64_t ncols = (h->tk == 32 || h->tm == 128) ? 256 : 512;
+  int64_t ncols = (h->tk == 32 || h->tm == 128) ? 256 : 512;
+  if (const char* nc = getenv("HRPB_NCOLS")) {  // experiment: columns per launch (multiple of 128)
+    const int64_t v = atoll(nc);
+    if (v >= 128 && v % 128 == 0 && v < ncols) ncols = v;
+  }
   for (int64_t n0 = 0; n0 < N; n0 += ncols) {
     const int64_t w = N - n0 < ncols ? N - n0 : ncols;
     const int nt = (int)ceil_div(w, 128);

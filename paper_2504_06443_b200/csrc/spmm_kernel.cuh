@@ -7,15 +7,15 @@
 // B200 design:
 //  * persistent CTAs (one per SM), each owning a contiguous panel range balanced on
 //    (blocks + panels) (S1);
-//  * warp 0: TMA producer — cp.async.bulk of the packed block bytes (S2) and
-//    cp.async.bulk.tensor.2d.tile::gather4 of the 16 B rows named by activeCols into an
-//    MN-major SWIZZLE_128B_BASE32B tile (S3); sentinel column K is out of bounds -> zero fill;
-//  * warp 1: decoder — lane l expands bits l and l+32 of every brick (prefix popcounts)
-//    into a zero-filled K-major TF32 tile (cvt.rna on A, reading R15) (S2);
-//  * warp 2: one thread issues tcgen05.mma.kind::tf32 computing the transposed product
-//    D[n, r] += sum_k Bg[k, n] * A[r, k]  (M = 128 dense columns, N = TM = 16 panel rows, K = 8 x 2),
-//    accumulating a whole panel in TMEM (double-buffered across panels) (S4);
-//  * warps 3..6: epilogue — tcgen05.ld 32x32b, coalesced 128-B row stores of C (S5);
+//  * warps 0..3: producers — block i of the CTA goes to warp i % 4: cp.async.bulk of the packed block bytes (S2)
+//    and cp.async 16-B copies of its TK gathered B rows (activeCols) into an MN-major SWIZZLE_128B_BASE32B tile;
+//    the sentinel column K is zero-filled (S3) (TMA tile::gather4 staging as the GM = 0 variant);
+//  * warps 4..7: decoders (block i -> warp 4 + i % 4) — prefix-popcount brick expansion into a
+//    K-major TF32 tile (integer RNA rounding of A, reading R15) (S2);
+//  * warps 8..9: one elected thread each issues tcgen05.mma.kind::tf32 computing the transposed product
+//    D[n, r] += sum_k Bg[k, n] * A[r, k]  (M = 128 dense columns, N = TM panel rows, K = 8 x 2); block i of the
+//    CTA goes to warp 8 + i % 2, which accumulates it into its own TMEM set of the panel's slot (S4);
+//  * warps 12..15: epilogue — tcgen05.ld 32x32b of the panel's sets, summed, coalesced 128-B row stores (S5);
 //  * mbarrier rings: full_a/full_b (TMA), dec (decoder), empty (tcgen05.commit), tfull/tempty.
 #pragma once
 #include <atomic>
@@ -30,13 +30,10 @@ namespace hrpb {
 
 constexpr int kProdWarps = 4;                              // warps 0..3: gather producers
 constexpr int kDecWarps = 4;                               // warps 4..7: brick decoders
-constexpr int kMmaWarp = kProdWarps + kDecWarps;           // warp 8: TMEM alloc; warps 8..9: MMA issue
-#ifndef HRPB_MMA_WARPS
-#define HRPB_MMA_WARPS 2
-#endif
-constexpr int kMmaWarps = HRPB_MMA_WARPS;                  // non-empty panel pc -> MMA warp 8 + pc % 2
-constexpr int kEpiWarp0 = kMmaWarp + kMmaWarps;            // warps 10..13: epilogue
-constexpr int kSpmmThreads = 32 * (kEpiWarp0 + 4);        // 448
+constexpr int kMmaWarp = kProdWarps + kDecWarps;           // warps 8..11: TMEM alloc (8) and MMA issue
+constexpr int kMmaWarps = 4;                               // MMA-issuing warps (at most; SmemLayout::kMW are used)
+constexpr int kEpiWarp0 = kMmaWarp + kMmaWarps;            // warps 12..15: epilogue (TMEM lane quadrant = warp % 4)
+constexpr int kSpmmThreads = 32 * (kEpiWarp0 + 4);        // 512
 constexpr int kMaxStages = 24;
 #ifndef HRPB_L2PF
 #define HRPB_L2PF 0
@@ -138,12 +135,26 @@ struct SmemLayout {
   static constexpr bool kInPlace = kItems <= 8;
   static_assert(!kInPlace || kARawBytes >= kATileBytes, "the raw slot must hold the decoded tile");
   static constexpr int kStage = kBTile + kARawBytes + (kInPlace ? 0 : kATileBytes);
-  // TMEM accumulator slots (panels in flight between the MMA warp and the epilogue): up to 4
-  static constexpr int kSlots = 4 * NT * TMV <= 512 ? 4 : 2;
-  static_assert(kSlots % (NT <= 2 ? kMmaWarps : 1) == 0, "a TMEM slot must always be used by the same MMA warp");
-  static constexpr int kSlotCols = kSlots * NT * TMV;
+  // MMA issue is latency-bound per issuing thread (~50 cycles per tcgen05.mma, ~180 per tcgen05.commit, measured:
+  // tools/microtests/umma_commit.cu), so kMW warps issue the blocks of a panel in turn (block i -> warp i % kMW),
+  // each into its own accumulator set; the epilogue adds the sets. kMW = the most warps whose sets leave room for
+  // two panels in flight in the 512 TMEM columns.
+  static constexpr int kCols1 = NT * TMV;  // one accumulator set: TM columns per 128-column N tile
+#ifndef HRPB_MW_MAX
+#define HRPB_MW_MAX 2
+#endif
+#ifndef HRPB_MW_TM64
+#define HRPB_MW_TM64 2
+#endif
+  static constexpr int kMWcap = TMV >= 64 ? HRPB_MW_TM64 : HRPB_MW_MAX;
+  static constexpr int kMW = 2 * 4 * kCols1 <= 512 && kMWcap >= 4 ? 4 : (2 * 2 * kCols1 <= 512 && kMWcap >= 2 ? 2 : 1);
+  static constexpr int kSetCols = kMW * kCols1;  // TMEM columns of one panel slot
+  // TMEM accumulator slots (panels in flight between the MMA warps and the epilogue): 2 to 4
+  static constexpr int kSlots = 512 / kSetCols < 4 ? 512 / kSetCols : 4;
+  static_assert(kSlots >= 2, "two panel slots must fit in the 512 TMEM columns");
+  static_assert(kMW <= kMmaWarps && kDecWarps % kMW == 0, "MMA warps");
+  static constexpr int kSlotCols = kSlots * kSetCols;
   static constexpr uint32_t kTmemCols = kSlotCols <= 32 ? 32 : (kSlotCols <= 64 ? 64 : (kSlotCols <= 128 ? 128 : (kSlotCols <= 256 ? 256 : 512)));
-  static_assert(2 * NT * TMV <= 512, "two TMEM accumulator slots must fit in 512 columns");
 };
 
 
@@ -154,17 +165,18 @@ struct SmemLayout {
 // tiles in CTA order (deterministic) into C.
 // kPanelW: units per panel epilogue per 16 panel rows (the C store of TM rows), 1 = one block's worth
 #ifndef HRPB_PANEL_W
-#define HRPB_PANEL_W 3
+#define HRPB_PANEL_W 5
 #endif
 constexpr uint64_t kPanelW = HRPB_PANEL_W;
 #ifndef HRPB_PANEL_W32
-#define HRPB_PANEL_W32 3
+#define HRPB_PANEL_W32 5
 #endif
 #ifndef HRPB_PANEL_W64
 #define HRPB_PANEL_W64 12
 #endif
-// measured on c3 (R-MAT, N = 256): TM = 16 → 3 units (22.1 → 18.1 ms), TM = 32 → 3 (6: 21.0 ms),
-// TM = 64 → 12 (3: 27.0 ms, 12: 18.8 ms); TM = 128 scales TM = 64's
+// measured on c3 (R-MAT, N = 256) with two MMA-issuing warps per panel: TM = 16 → 5 units (3 / 4 / 5 / 6 / 8:
+// 16.0 / 14.4-14.8 / 13.7 / 13.9 / 14.9 ms), TM = 32 → 5 (3 / 5 / 8: 16.1 / 14.3 / 14.4 ms), TM = 64 → 12 (20: 15.7 ms);
+// TM = 128 scales TM = 64's
 template <int TMV>
 __host__ __device__ constexpr uint64_t panel_weight() {
   return TMV == 16 ? kPanelW : TMV == 32 ? (uint64_t)HRPB_PANEL_W32 : TMV == 64 ? (uint64_t)HRPB_PANEL_W64
@@ -313,9 +325,6 @@ struct PanelCursor {
   }
 };
 
-// cross-warp progress words of the MMA issuers: shared-memory atomics (a plain volatile flag is a data race)
-__device__ __forceinline__ void st_relaxed_cta(uint32_t* p, uint32_t v) { atomicExch(p, v); }
-__device__ __forceinline__ uint32_t ld_relaxed_cta(uint32_t* p) { return atomicAdd(p, 0u); }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
@@ -356,9 +365,8 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   uint64_t* tempty = tfull + 4;
   uint32_t* misc = (uint32_t*)(tempty + 4);  // [0] tmem base
   int64_t* range = (int64_t*)(misc + 2);     // CtaWork: pa, pb, bB, bE, first_full, last_full
-  uint32_t* mma_prog = (uint32_t*)(range + 6);  // [kMmaWarps] next block each MMA warp waits for (relaxed atomics)
   // per decoder warp: brick-slot table (pattern, value offset) of the block being decoded
-  uint64_t* slot_pat = (uint64_t*)(range + 6 + kMmaWarps);     // [kDecWarps][kNbk]
+  uint64_t* slot_pat = (uint64_t*)(range + 6);                 // [kDecWarps][kNbk]
   uint32_t* slot_off = (uint32_t*)(slot_pat + kDecWarps * L::kNbk);  // [kDecWarps][kNbk]
   // per producer warp: ring of kPfRing own blocks {sizePtr[b], sizePtr[b + 1], activeCols[b * TK .. + TK)}
   uint32_t* pring = (uint32_t*)(((uintptr_t)(slot_off + kDecWarps * L::kNbk) + 15) & ~(uintptr_t)15);
@@ -376,10 +384,9 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       mbar_init(&full_b[s], (GM == 0 ? 1 : 32) + 1);
       mbar_init(&empty[s], 1);
     }
-    for (int i = 0; i < L::kSlots; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < L::kSlots; ++i) { mbar_init(&tfull[i], L::kMW); mbar_init(&tempty[i], 4); }
     fence_mbar_init();
 
-    for (int m = 0; m < kMmaWarps; ++m) st_relaxed_cta(&mma_prog[m], 0u);
     prefetch_tmap(&tmB);
   }
   if (warp == kMmaWarp) tmem_alloc(&misc[0], tmem_cols);
@@ -666,87 +673,68 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     }
   } else if (warp < kEpiWarp0) {
     // ---------------------------------------------------------------- MMA issuers (one thread per warp)
-    // Non-empty panel pc goes to MMA warp pc % kMmaWarps and TMEM slot pc % kSlots: a single issuing warp spends
-    // several hundred cycles of dependent issue latency per block (wait, 2 MMAs, commit), so two warps overlap.
-    // Blocks of other warps' panels are skipped. A warp publishes in mma_prog the block it is about to wait for
-    // (all its earlier blocks are consumed); before a panel whose last block is i it waits until every other
-    // warp has published a block > i - S, so no stage barrier it waits on can be two phases behind (parity is
-    // unambiguous).
-    // with NT >= 3 a block is >= 6 MMAs (>= 300 tensor cycles) and one issuing warp keeps up; the skew guard
-    // would only serialise (c5 at N = 512: panels longer than the S = 4 stages)
-    constexpr int kSplit = NT <= 2 ? kMmaWarps : 1;
+    // Block i of this CTA's range goes to MMA warp i % kMW (the decoders' and producers' interleave), which
+    // accumulates it into its own TMEM set of the panel's slot (pc % kSlots): the issue latency of one thread
+    // (~50 cycles per tcgen05.mma, ~180 per tcgen05.commit) no longer serialises a long panel. Every MMA warp walks
+    // every panel that has blocks here: it waits for the slot to be free, issues its blocks (if any) and commits
+    // (or, with none, plain-arrives) on tfull[slot] (kMW arrivals). Stage j % S is only ever consumed by warp
+    // j % kMW (S is a multiple of 4), in order, so its parity (j / S) & 1 is unambiguous.
+    constexpr int kMW = L::kMW;
     const int mw = warp - kMmaWarp;
-    const int64_t b_begin = cbB;
-    uint32_t pc = 0;
-    constexpr uint32_t kIdesc = idesc_tf32<TMV>();
-    // descriptors of stage 0; stage s adds s * stage bytes / 16 to the start-address field (no carry: < 256 KB)
-    const uint64_t adesc0 = umma_sdesc(smem_u32(btile0), 512, L::kNA * 512, 1);
-    const uint64_t bdesc0 = umma_sdesc(smem_u32(atile0), L::kLbo, 128, 0);
-    const uint32_t Su = (uint32_t)S;
-    PanelCursor cursor(brp, pa, pb, lane);
-    int64_t p;
-    uint32_t bb, be;
-    while (cursor.next(p, bb, be)) {
-      bb = bb > cbB ? bb : cbB;  // this CTA's blocks of the panel (all of them unless the panel is split)
-      be = be < cbE ? be : cbE;
-      if (bb >= be) continue;
-      if ((int)(pc % kSplit) != mw) {
-        ++pc;
-        continue;
-      }
-      const uint32_t slot = pc % L::kSlots;
-      uint32_t i = (uint32_t)(bb - b_begin);  // block index within this CTA's range
-      uint32_t st = i % Su, ph = (i / Su) & 1u;
-      if (kSplit > 1 && lane == 0) {
-        st_relaxed_cta(&mma_prog[mw], i);  // all of this warp's blocks before its new panel are consumed
-        const uint32_t last = i + (be - bb) - 1u;
-        if (last >= Su) {
-          const long long tg = tracing(prm) ? clock64() : 0;
-#pragma unroll
-          for (int m = 0; m < kSplit; ++m)
-            if (m != mw)
-              while (ld_relaxed_cta(&mma_prog[m]) <= last - Su) {
-              }
-          if (tracing(prm)) wacc += clock64() - tg;
-        }
-      }
-      __syncwarp();
-      mbar_wait_acc(prm, &tempty[slot], ((pc / L::kSlots) & 1) ^ 1, wacc);
-      tc_fence_after();
-      const uint32_t dcol = tbase + slot * NT * TMV;
-      for (uint32_t b = bb; b < be; ++b, ++i) {
-        const int s = (int)st;
-        if (kSplit > 1 && lane == 0) st_relaxed_cta(&mma_prog[mw], i);
-        mbar_wait_acc(prm, &full_b[s], ph, wacc);
+    if (mw < kMW) {
+      const int64_t b_begin = cbB;
+      uint32_t pc = 0;
+      constexpr uint32_t kIdesc = idesc_tf32<TMV>();
+      // descriptors of stage 0; stage s adds s * stage bytes / 16 to the start-address field (no carry: < 256 KB)
+      const uint64_t adesc0 = umma_sdesc(smem_u32(btile0), 512, L::kNA * 512, 1);
+      const uint64_t bdesc0 = umma_sdesc(smem_u32(atile0), L::kLbo, 128, 0);
+      const uint32_t Su = (uint32_t)S;
+      PanelCursor cursor(brp, pa, pb, lane);
+      int64_t p;
+      uint32_t bb, be;
+      while (cursor.next(p, bb, be)) {
+        bb = bb > cbB ? bb : cbB;  // this CTA's blocks of the panel (all of them unless the panel is split)
+        be = be < cbE ? be : cbE;
+        if (bb >= be) continue;
+        const uint32_t slot = pc % L::kSlots;
+        const uint32_t i0 = (uint32_t)(bb - b_begin), i1 = (uint32_t)(be - b_begin);  // CTA-local block range
+        const uint32_t j0 = i0 + (((uint32_t)mw + kMW - i0 % kMW) % kMW);              // first own block
+        mbar_wait_acc(prm, &tempty[slot], ((pc / L::kSlots) & 1) ^ 1, wacc);
         tc_fence_after();
-        if (lane == 0) {
-          trace_ev(prm, 3, i);
-          trace_ev(prm, 4, i);
-          if (dbg(prm, 4)) {
-            mbar_arrive(&empty[s]);
-          } else {
-            const uint64_t ad = adesc0 + (uint64_t)(st * (uint32_t)(L::kBTile >> 4));
-            const uint64_t bd = bdesc0 + (uint64_t)(st * (uint32_t)(kATileStride >> 4));
-            // K step outer, N tile inner: consecutive MMAs write different accumulators (independent), so the
-            // tensor pipe need not wait for one accumulation before starting the next
+        const uint32_t dcol = tbase + slot * L::kSetCols + mw * L::kCols1;
+        for (uint32_t j = j0; j < i1; j += kMW) {
+          const uint32_t st = j % Su, ph = (j / Su) & 1u;
+          mbar_wait_acc(prm, &full_b[st], ph, wacc);
+          tc_fence_after();
+          if (lane == 0) {
+            trace_ev(prm, 3, j);
+            trace_ev(prm, 4, j);
+            if (dbg(prm, 4)) {
+              mbar_arrive(&empty[st]);
+            } else {
+              const uint64_t ad = adesc0 + (uint64_t)(st * (uint32_t)(L::kBTile >> 4));
+              const uint64_t bd = bdesc0 + (uint64_t)(st * (uint32_t)(kATileStride >> 4));
+              // K step outer, N tile inner: consecutive MMAs write different accumulators (independent)
 #pragma unroll
-            for (int g = 0; g < TKV / 8; ++g) {
+              for (int g = 0; g < TKV / 8; ++g) {
 #pragma unroll
-              for (int t = 0; t < NT; ++t)
-                umma_tf32(dcol + t * TMV, ad + (uint64_t)(((2 * g * L::kNA + 4 * t) * 512) >> 4),
-                          bd + (uint64_t)((g * 2 * L::kLbo) >> 4), kIdesc, (b > bb || g > 0) ? 1u : 0u);
+                for (int t = 0; t < NT; ++t)
+                  umma_tf32(dcol + t * TMV, ad + (uint64_t)(((2 * g * L::kNA + 4 * t) * 512) >> 4),
+                            bd + (uint64_t)((g * 2 * L::kLbo) >> 4), kIdesc, (j > j0 || g > 0) ? 1u : 0u);
+              }
+              umma_commit(&empty[st]);
             }
-            umma_commit(&empty[s]);
           }
+          __syncwarp();
+        }
+        if (lane == 0) {
+          if (j0 < i1) umma_commit(&tfull[slot]);
+          else mbar_arrive(&tfull[slot]);  // no block of this panel here: its set is not read
         }
         __syncwarp();
-        if (++st == Su) { st = 0; ph ^= 1; }
+        ++pc;
       }
-      if (lane == 0) umma_commit(&tfull[slot]);
-      __syncwarp();
-      ++pc;
     }
-    if (kMmaWarps > 1 && lane == 0) st_relaxed_cta(&mma_prog[mw], 0xFFFFFFFFu);
   } else {
     // ---------------------------------------------------------------- epilogue (last 4 warps)
     const int qd = warp & 3;            // TMEM lane quadrant accessible to this warp
@@ -765,7 +753,15 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
         continue;
       }
       const bool full = (p != pa || first_full) && (p != pb - 1 || last_full);
-      if ((bb > cbB ? bb : cbB) >= (be < cbE ? be : cbE)) continue;  // split panel without blocks here
+      const uint32_t cb = bb > cbB ? bb : cbB, ce = be < cbE ? be : cbE;
+      if (cb >= ce) continue;  // split panel without blocks here
+      // accumulator sets written: MMA warp w took the blocks i = w (mod kMW) of the CTA-local range [i0, i0 + n)
+      constexpr int kMW = L::kMW;
+      const uint32_t i0 = cb - cbB, nblk = ce - cb;
+      uint32_t cmask = 0;
+#pragma unroll
+      for (int w = 0; w < kMW; ++w)
+        if (nblk >= (uint32_t)kMW || ((uint32_t)w + kMW - i0 % kMW) % kMW < nblk) cmask |= 1u << w;
       // a split panel's share goes to this CTA's workspace tile (slot 0: its first panel, 1: its last)
       float* const obase = full ? prm.C + row0 * N + n0
                                 : prm.ws + ((int64_t)(2 * blockIdx.x + (p == pa ? 0 : 1)) * TMV) * (128 * NT);
@@ -774,26 +770,45 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       mbar_wait_acc(prm, &tfull[slot], (pc / L::kSlots) & 1, wacc);
       if (et == 0) trace_ev(prm, 5, pc);
       tc_fence_after();
-      constexpr int kRows = TMV < 64 ? TMV : 64;  // rows per tcgen05.wait (TM = 128: two halves, 64 registers)
+      // rows per tcgen05.wait: 32 for one set; with kMW sets 16 rows of every written set are loaded before one
+      // wait and summed in set order (kMW x 16 registers; 512 threads leave 128 per thread)
+      constexpr int kRows = kMW > 1 ? 16 : (TMV < 32 ? TMV : 32);
+      const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16) + slot * L::kSetCols;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
 #pragma unroll
         for (int h0 = 0; h0 < TMV; h0 += kRows) {
-          uint32_t v[kRows / 16][16];  // panel rows [h0, h0 + kRows) of this lane's column
+          uint32_t v[kMW][kRows / 16][16];  // panel rows [h0, h0 + kRows) of this lane's column, per set
 #pragma unroll
-          for (int c16 = 0; c16 < kRows / 16; ++c16)
-            tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + slot * NT * TMV + t * TMV + h0 + c16 * 16, v[c16]);
+          for (int w = 0; w < kMW; ++w)
+            if ((cmask >> w) & 1u) {
+#pragma unroll
+              for (int c16 = 0; c16 < kRows / 16; ++c16)
+                tmem_ld16(tq + w * L::kCols1 + t * TMV + h0 + c16 * 16, v[w][c16]);
+            }
           tmem_ld_wait();
+          float a[kRows];  // sum of the written sets in set order (the first one copied: -0.0 stays -0.0)
+          bool first = true;
+#pragma unroll
+          for (int w = 0; w < kMW; ++w)
+            if ((cmask >> w) & 1u) {
+#pragma unroll
+              for (int r = 0; r < kRows; ++r) {
+                const float x = __uint_as_float(v[w][r >> 4][r & 15]);
+                a[r] = first ? x : a[r] + x;
+              }
+              first = false;
+            }
           const int64_t c = 128 * t + 32 * qd + lane;
           if (c < ncols && !(dbg(prm, 1))) {
             float* dst = obase + c + (int64_t)h0 * ostride;
             if (nrows == TMV) {
 #pragma unroll
-              for (int r = 0; r < kRows; ++r) __stcs(dst + (int64_t)r * ostride, __uint_as_float(v[r >> 4][r & 15]));
+              for (int r = 0; r < kRows; ++r) __stcs(dst + (int64_t)r * ostride, a[r]);
             } else {
 #pragma unroll
               for (int r = 0; r < kRows; ++r)
-                if (h0 + r < nrows) __stcs(dst + (int64_t)r * ostride, __uint_as_float(v[r >> 4][r & 15]));
+                if (h0 + r < nrows) __stcs(dst + (int64_t)r * ostride, a[r]);
             }
           }
         }
@@ -885,7 +900,7 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   // only ever filled by one warp, so a warp running ahead cannot alias an mbarrier phase.
   static_assert(kDecWarps % kProdWarps == 0, "stage ownership: decoder count must be a multiple of producers");
   auto smem_for = [](int st) {
-    return (size_t)1024 /*alignment*/ + (size_t)st * L::kStage + (3 * st + 8) * 8 + 128 + 8 * kMmaWarps +
+    return (size_t)1024 /*alignment*/ + (size_t)st * L::kStage + (3 * st + 8) * 8 + 128 +
            kDecWarps * L::kNbk * 12 + 16 + kProdWarps * kPfRing * (TKV + 4) * 4;
   };
   int stages = kMaxStages - kMaxStages % kDecWarps;
