@@ -241,6 +241,7 @@ __host__ __device__ inline WarpLayout warp_layout(int tm, int tk) {  // (also us
 struct WarpPanel {
   int64_t p, e0;
   int E, nrows;
+  int64_t Eall;     // entries of the panel (E is clamped to kWCap + 1)
   int32_t mn;
   uint32_t nact, nblk;
   bool sorted;      // rank by warp sort (column span wider than the bitmap, E <= kWSortCap)
@@ -297,6 +298,7 @@ __device__ __forceinline__ bool warp_panel_rows(const int64_t* __restrict__ rp, 
   w.e0 = e0;
   w.nrows = nrows;
   const int64_t E = e1 - e0;
+  w.Eall = E;
   w.E = (int)min(E, (int64_t)kWCap + 1);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -626,13 +628,18 @@ __device__ __forceinline__ void warp_panel_patterns(const WarpPanel& w, uint8_t*
 }
 
 // Classification pre-pass: panels the warp path cannot take (more than kWCap entries, column span wider than
-// the bitmap) are flagged and listed for the CTA / hub count kernels, which run before k_wbuild.
+// the bitmap) are flagged and listed: those with more than kSmallCap entries (hubs) for the hub count kernel
+// (panels above huge_cap, if > 0, from the end of biglist: that kernel claims them first), the others for the CTA
+// count kernel. The two count kernels then share no input and run concurrently, before k_wbuild.
 template <int tm, int tk>
 __global__ void __launch_bounds__(32 * kWWarps) k_wclassify(const int64_t* __restrict__ rp,
                                                            const int32_t* __restrict__ ci, int64_t M, int64_t nnz,
                                                            int64_t P, uint8_t* __restrict__ listed,
                                                            uint32_t* __restrict__ list,
-                                                           uint32_t* __restrict__ nlist) {
+                                                           uint32_t* __restrict__ nlist,
+                                                           uint32_t* __restrict__ biglist,
+                                                           uint32_t* __restrict__ nbig,
+                                                           uint32_t* __restrict__ nhuge, int64_t huge_cap) {
   pdl_wait();
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t p = (int64_t)blockIdx.x * kWWarps + wid; p < P; p += (int64_t)gridDim.x * kWWarps) {
@@ -643,7 +650,14 @@ __global__ void __launch_bounds__(32 * kWWarps) k_wclassify(const int64_t* __res
     if (ok && w.E > kWSortCap) ok = warp_panel_span<tm>(w, [&](uint32_t i) { return ci[w.e0 + i]; });
     if (lane == 0) {
       listed[p] = ok ? 0 : 1;
-      if (!ok) list[atomicAdd(nlist, 1u)] = (uint32_t)p;
+      if (!ok) {
+        if (w.Eall > kSmallCap) {
+          if (huge_cap > 0 && w.Eall > huge_cap) biglist[P - atomicAdd(nhuge, 1u)] = (uint32_t)p;
+          else biglist[atomicAdd(nbig, 1u)] = (uint32_t)p;
+        } else {
+          list[atomicAdd(nlist, 1u)] = (uint32_t)p;
+        }
+      }
     }
   }
 }
@@ -2694,8 +2708,10 @@ static int wbuild_ctas() {  // resident CTAs of k_wbuild per SM (the ticket loop
 }
 
 static void launch_wclassify(int tm, int tk, unsigned grid, cudaStream_t s, const int64_t* rp, const int32_t* ci,
-                             int64_t M, int64_t nnz, int64_t P, uint8_t* listed, uint32_t* list, uint32_t* nlist) {
-#define HRPB_WC(A, B) k_wclassify<A, B><<<grid, 32 * kWWarps, 0, s>>>(rp, ci, M, nnz, P, listed, list, nlist)
+                             int64_t M, int64_t nnz, int64_t P, uint8_t* listed, uint32_t* list, uint32_t* nlist,
+                             uint32_t* biglist, uint32_t* nbig, uint32_t* nhuge, int64_t huge_cap) {
+#define HRPB_WC(A, B) \
+  k_wclassify<A, B><<<grid, 32 * kWWarps, 0, s>>>(rp, ci, M, nnz, P, listed, list, nlist, biglist, nbig, nhuge, huge_cap)
   HRPB_WDISPATCH(HRPB_WC);
 #undef HRPB_WC
 }
@@ -2804,10 +2820,14 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     cudaMemsetAsync(h->brp, 0, sizeof(uint32_t), s);  // P == 0: blockedRowPtr = {0}
     cudaMemsetAsync(poff, 0, sizeof(uint64_t), s);
     if (P > 0) {
-      // classification; listed panels counted by a CTA (<= kSmallCap entries) or the hub bitmap kernel
-      launch_wclassify(tm, tk, wgrid, s, row_ptr, col_idx, M, nnz, P, listed, l1, nl1);
+      // classification: warp-path panels, listed panels (counted by a CTA, <= kSmallCap entries) and hub panels
+      // (measured: running the hub kernels on a side stream beside the listed-panel kernels gained nothing on c3 —
+      // each fills the SMs' shared memory, so they do not co-reside)
+      const int64_t huge_cap = hub_2l ? kH2Huge : (int64_t)0;
+      launch_wclassify(tm, tk, wgrid, s, row_ptr, col_idx, M, nnz, P, listed, l1, nl1, biglist, nbig, ctr + 12,
+                       huge_cap);
       launch_pdl(k_count, count_ctas, kMidThreads, count_smem, s, row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
-                 pbytes, gpat, l1, nl1, biglist, nbig, ctr + 8, status, ctr + 12, hub_2l ? kH2Huge : (int64_t)0, P);
+                 pbytes, gpat, l1, nl1, biglist, nbig, ctr + 8, status, ctr + 12, huge_cap, P);
       if (hub_2l)
         launch_pdl(k_count_hub2, hub2_ctas, kH2Threads, sizeof(Hub2Smem), s, row_ptr, col_idx, M, K, nnz, tm, tk, q,
                    nact, nblk, pbytes, gpat, relb, biglist, nbig, ctr + 3, hublist2, hubch2, nhub2, bigscr, status,

@@ -63,6 +63,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 #endif
 }
 
+// the same with a __nanosleep back-off between polls: for waits off the critical path (the epilogue's wait for a
+// finished panel), so that spinning warps do not take issue slots from the producers and decoders
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity, uint32_t ns) {
+  while (!mbar_try_wait(b, parity)) __nanosleep(ns);
+}
+
 // ------------------------------------------------------------------ TMA / bulk copies
 // 1-D bulk copy global -> shared, completes bytes on `bar` (size and addresses 16-B aligned).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,

@@ -43,6 +43,12 @@ constexpr int kMaxStages = 24;
 // (2 / 4 / 8: c4 5.68 -> 8.3 / 10.0 / 10.0 ms, c2a TM = 64 0.247 -> 0.338 ms, c3 19.1 -> 19.4 ms): the prefetches
 // queue in the same bulk-copy path as the A blocks
 constexpr int kL2Pf = HRPB_L2PF;
+#ifndef HRPB_EPI_SLEEP
+#define HRPB_EPI_SLEEP 0
+#endif
+#ifndef HRPB_L2PF_MODE
+#define HRPB_L2PF_MODE 1  // 1: prefetch.global.L2 per 128-B line, 0: cp.async.bulk.prefetch.L2 per row
+#endif
 constexpr int kPfRing = 8 + kL2Pf;  // producer look-ahead ring in own blocks (x4 producer warps)
 
 // per-call scratch of hrpb_spmm: split-panel workspace, its flag word and this call's epoch
@@ -492,9 +498,21 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       const uint32_t* slot = myring + q * kSlotW;
       if constexpr (kL2Pf > 0) {
         const int qp = q + kL2Pf < kPfRing ? q + kL2Pf : q + kL2Pf - kPfRing;
-        if (lane < TKV && b + 4 * kL2Pf < b_end && pf_bytes) {
-          const uint32_t rk = myring[qp * kSlotW + 4 + lane];
-          if (rk < Kr) prefetch_l2_bulk(Bsrc + (uint64_t)rk * ldb32, pf_bytes);
+        if (b + 4 * kL2Pf < b_end && pf_bytes) {
+#if HRPB_L2PF_MODE == 1
+          // per-lane prefetch.global.L2 of the 128-B lines of the TK rows (LSU path, no shared memory held)
+          const uint32_t lines = (pf_bytes + 127) >> 7;
+          for (uint32_t x = lane; x < TKV * lines; x += 32) {
+            const uint32_t rw = x / lines, ln = x - rw * lines;
+            const uint32_t rk = myring[qp * kSlotW + 4 + rw];
+            if (rk < Kr) asm volatile("prefetch.global.L2 [%0];" ::"l"(Bsrc + (uint64_t)rk * ldb32 + 32 * ln));
+          }
+#else
+          if (lane < TKV) {
+            const uint32_t rk = myring[qp * kSlotW + 4 + lane];
+            if (rk < Kr) prefetch_l2_bulk(Bsrc + (uint64_t)rk * ldb32, pf_bytes);
+          }
+#endif
         }
       }
       mbar_wait_acc(prm, &empty[s], ph ^ 1, wacc);
@@ -767,6 +785,10 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
                                 : prm.ws + ((int64_t)(2 * blockIdx.x + (p == pa ? 0 : 1)) * TMV) * (128 * NT);
       const int64_t ostride = full ? N : 128 * NT;
       const uint32_t slot = pc % L::kSlots;
+#if HRPB_EPI_SLEEP > 0
+      if (!tracing(prm)) mbar_wait_backoff(&tfull[slot], (pc / L::kSlots) & 1, HRPB_EPI_SLEEP);
+      else
+#endif
       mbar_wait_acc(prm, &tfull[slot], (pc / L::kSlots) & 1, wacc);
       if (et == 0) trace_ev(prm, 5, pc);
       tc_fence_after();
