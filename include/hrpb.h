@@ -106,6 +106,24 @@ hrpb_status_t hrpb_spmm(const hrpb_t A, const float* B, float* C, int64_t M, int
                         hrpb_stream_t stream);
 
 /*
+ * hrpb_spmm_sharded — C = A.B with B ROW-SHARDED (the repeated-SpMM use case of P:L484 with a
+ * B too large or too costly to replicate): shard r holds B rows [r*rows_per_shard, min((r+1)*rows_per_shard, K))
+ * as a row-major (rows x N) array, ld = N. Each gathered B row (S3) is read from its shard in place: a shard may be
+ * local device memory or another GPU's memory mapped into this device's address space (CUDA IPC / peer access
+ * over NVLink), so no B replica and no broadcast are needed. Same kernel, arithmetic, determinism and work split
+ * as hrpb_spmm (the result is bit-identical to hrpb_spmm on the concatenated B).
+ *   shards         : HOST array [nshards] of device pointers, each 16-B aligned; read-only, owned by the caller,
+ *                    valid until the call's work on `stream` has completed.
+ *   nshards        : 1..32 and equal to ceil(K / rows_per_shard) (1 when K = 0).
+ *   rows_per_shard : >= 1.
+ *   N              : >= 0 and a multiple of 4 (rows stay 16-B aligned: no padded copy is made).
+ *   C, M, K, stream: as for hrpb_spmm.
+ * Errors: INVALID_VALUE (shard table, alignment or N), DIMENSION_MISMATCH, NOT_SUPPORTED, OUT_OF_MEMORY, CUDA.
+ */
+hrpb_status_t hrpb_spmm_sharded(const hrpb_t A, const float* const* shards, int32_t nshards, int64_t rows_per_shard,
+                                float* C, int64_t M, int64_t K, int64_t N, hrpb_stream_t stream);
+
+/*
  * hrpb_build_spmm — the whole hot path on device buffers in one call: hrpb_build then hrpb_spmm, enqueued
  * back to back on `stream` (the SpMM does not wait for the build's size read-back), one synchronization at the
  * end. Arguments as for hrpb_build / hrpb_spmm (all DEVICE pointers).

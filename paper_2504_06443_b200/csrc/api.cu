@@ -356,6 +356,18 @@ hrpb_status_t hrpb_spmm(const hrpb_t A, const float* B, float* C, int64_t M, int
   return st;
 }
 
+hrpb_status_t hrpb_spmm_sharded(const hrpb_t A, const float* const* shards, int32_t nshards, int64_t rows_per_shard,
+                                float* C, int64_t M, int64_t K, int64_t N, hrpb_stream_t stream) {
+  if (!A || N < 0 || !shards) return HRPB_ERROR_INVALID_VALUE;
+  if (M != A->M || K != A->K) return HRPB_ERROR_DIMENSION_MISMATCH;
+  if (N >= (1ll << 31)) return HRPB_ERROR_INVALID_VALUE;
+  if (N == 0 || M == 0) return HRPB_SUCCESS;
+  if (!C) return HRPB_ERROR_INVALID_VALUE;
+  const hrpb_status_t st = spmm_sharded_impl(A, shards, nshards, rows_per_shard, C, N, (cudaStream_t)stream);
+  if (st == HRPB_SUCCESS) note_use(A, (cudaStream_t)stream);
+  return st;
+}
+
 hrpb_status_t hrpb_build_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr_h,
                                    const int32_t* col_idx_h, const float* values_h, const float* B_h, float* C_h,
                                    const hrpb_config_t* cfg, hrpb_stream_t stream) {

@@ -48,6 +48,13 @@ hrpb_status_t choose_tm(int64_t M, int64_t K, int64_t nnz, const int64_t* row_pt
 hrpb_status_t sticky_take(cudaStream_t s);
 
 hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, cudaStream_t s);
+struct ShardDesc;
+// common body of the SpMM entry points: panels [p_lo, p_hi); sd = NULL, or the row-sharded B of hrpb_spmm_sharded
+hrpb_status_t spmm_core(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, int64_t p_lo,
+                        int64_t p_hi, const ShardDesc* sd, cudaStream_t s);
+// NEXT-3: B rows [r rps, min((r + 1) rps, K)) at shards[r] (ld = N), r < nshards = ceil(K / rps)
+hrpb_status_t spmm_sharded_impl(const hrpb_handle* h, const float* const* shards, int32_t nshards,
+                                int64_t rows_per_shard, float* C, int64_t N, cudaStream_t s);
 // C rows of panels [p_lo, p_hi) only (the pipelined host entry point)
 hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, int64_t p_lo,
                               int64_t p_hi, cudaStream_t s);

@@ -1,5 +1,8 @@
 // spmm.cu — host side of hrpb_spmm_sm100: B row-pitch padding, the B tensor map, N-tile loop and the panel-range
-// entry points (the kernel itself is in spmm_kernel.cuh, instantiated per TK in spmm_tk16.cu / spmm_tk32.cu).
+// entry points, and the row-sharded B entry point (NEXT-3) (the kernel itself is in spmm_kernel.cuh, instantiated per TK
+// in spmm_tk16.cu / spmm_tk32.cu, the row-sharded variant in spmm_sharded.cu).
+#include <cstring>
+
 #include "spmm_kernel.cuh"
 
 namespace hrpb {
@@ -37,6 +40,43 @@ hrpb_status_t spmm_impl(const hrpb_handle* h, const float* B, int64_t ldb, float
 
 hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, int64_t p_lo,
                               int64_t p_hi, cudaStream_t s) {
+  return spmm_core(h, B, ldb, C, N, p_lo, p_hi, nullptr, s);
+}
+
+// NEXT-3: B row-sharded over devices (shard r = rows [r rps, min((r + 1) rps, K)), ld = N). No padded copy: every
+// shard must be 16-B aligned with N % 4 == 0, and the gather runs as cp.async (GM = 2).
+hrpb_status_t spmm_sharded_impl(const hrpb_handle* h, const float* const* shards, int32_t nshards,
+                                int64_t rows_per_shard, float* C, int64_t N, cudaStream_t s) {
+  if (nshards < 1 || nshards > kMaxShards || rows_per_shard < 1 || rows_per_shard >= (1ll << 31))
+    return HRPB_ERROR_INVALID_VALUE;
+  if (ceil_div(h->K, rows_per_shard) != nshards && !(h->K == 0 && nshards == 1)) return HRPB_ERROR_INVALID_VALUE;
+  if (N % 4) return HRPB_ERROR_INVALID_VALUE;
+  ShardDesc sd{};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (int r = 0; r < nshards; ++r) {
+    if (!shards[r] || (reinterpret_cast<uintptr_t>(shards[r]) & 15)) return HRPB_ERROR_INVALID_VALUE;
+    sd.ptr[r] = shards[r];
+    // a shard in another GPU's memory (CUDA IPC mapping): enable peer access from this device once per pair
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, shards[r]) == cudaSuccess && at.type == cudaMemoryTypeDevice &&
+        at.device != dev && dev >= 0 && dev < 64 && at.device >= 0 && at.device < 64) {
+      static std::atomic<uint64_t> enabled[64];
+      if (!(enabled[dev].load() >> at.device & 1)) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_status(e);
+        cudaGetLastError();  // (clears cudaErrorPeerAccessAlreadyEnabled)
+        enabled[dev].fetch_or(1ull << at.device);
+      }
+    }
+  }
+  sd.rps = (uint32_t)rows_per_shard;
+  sd.nsh = nshards;
+  return spmm_core(h, shards[0], N, C, N, 0, h->P, &sd, s);
+}
+
+hrpb_status_t spmm_core(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, int64_t p_lo,
+                        int64_t p_hi, const ShardDesc* sd, cudaStream_t s) {
   if (N == 0 || h->M == 0 || p_hi <= p_lo) return HRPB_SUCCESS;
   if (h->NB == 0) {  // A has no entries: C = 0 (rows of the range; NB < 0 = not known yet: the kernel copes)
     const int64_t r0 = p_lo * h->tm, r1 = p_hi * h->tm < h->M ? p_hi * h->tm : h->M;
@@ -51,7 +91,7 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
   const float* Bt = B;
   int64_t ld = ldb;
   float* bpad = nullptr;
-  if ((reinterpret_cast<uintptr_t>(B) & 15) || (ld * 4) % 16) {
+  if (!sd && ((reinterpret_cast<uintptr_t>(B) & 15) || (ld * 4) % 16)) {
     const int64_t ldp = align_up(N, 4);
     bpad = (float*)dalloc((size_t)h->K * ldp * sizeof(float), s);
     if (!bpad) return HRPB_ERROR_OUT_OF_MEMORY;
@@ -69,16 +109,23 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
     return HRPB_ERROR_OUT_OF_MEMORY;
   }
   uint64_t* flag = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ws) + ws_bytes);
-  Scratch scr{ws, flag, next_epoch(), flag + 8};
+  Scratch scr{ws, flag, next_epoch(), flag + 8, sd};
   CUtensorMap tm;
-  cuuint64_t gdim[2] = {(cuuint64_t)N, (cuuint64_t)h->K};
-  cuuint64_t gstr[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {32, 1};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Bt), gdim, gstr, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return HRPB_ERROR_INVALID_VALUE;
+  memset(&tm, 0, sizeof(tm));  // (unused by the row-sharded cp.async gather: passed zeroed)
+  if (!sd) {
+    cuuint64_t gdim[2] = {(cuuint64_t)N, (cuuint64_t)h->K};
+    cuuint64_t gstr[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {32, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Bt), gdim, gstr, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      dfree(ws, s);
+      dfree(bpad, s);
+      return HRPB_ERROR_INVALID_VALUE;
+    }
+  }
   // columns per launch: NT <= 4, or <= 2 at TK = 32 (twice the stage size) and TM = 128 (two TMEM slots of
   // 2 x 128 columns fill the 512 TMEM columns)
   int64_t ncols = (h->tk == 32 || h->tm == 128) ? 256 : 512;
@@ -94,7 +141,8 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
     // every config measured, kept selectable per call and parity-tested)
     const char* genv = getenv("HRPB_GATHER");
     const int gm = genv ? atoi(genv) : 1;
-    if (h->tk == 16) st = spmm_dispatch<16>(h, tm, Bt, ld, C, N, (int)n0, nt, gm, p_lo, p_hi, scr, s);
+    if (sd) st = spmm_dispatch_sharded(h, tm, C, N, (int)n0, nt, p_lo, p_hi, scr, s);
+    else if (h->tk == 16) st = spmm_dispatch<16>(h, tm, Bt, ld, C, N, (int)n0, nt, gm, p_lo, p_hi, scr, s);
     else st = spmm_dispatch<32>(h, tm, Bt, ld, C, N, (int)n0, nt, 1, p_lo, p_hi, scr, s);
     if (st != HRPB_SUCCESS) {
       dfree(ws, s);

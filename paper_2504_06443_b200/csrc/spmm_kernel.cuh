@@ -51,12 +51,21 @@ constexpr int kL2Pf = HRPB_L2PF;
 #endif
 constexpr int kPfRing = 8 + kL2Pf;  // producer look-ahead ring in own blocks (x4 producer warps)
 
+// NEXT-3: B row-sharded (hrpb_spmm_sharded). Shard r holds rows [r rps, min((r + 1) rps, K)) at ptr[r] (ld = ldb),
+// local or peer-mapped (another GPU's memory over NVLink); the producer picks the shard per gathered row.
+constexpr int kMaxShards = 32;
+struct ShardDesc {
+  const float* ptr[kMaxShards];
+  uint32_t rps;  // rows per shard
+  int nsh;
+};
 // per-call scratch of hrpb_spmm: split-panel workspace, its flag word and this call's epoch
 struct Scratch {
   float* ws;
   uint64_t* flag;
   uint64_t epoch;
   uint64_t* ranges;  // [grid][4]: every CTA's S1 range (CtaWork), read by k_spmm_fixup
+  const ShardDesc* sd = nullptr;  // GM = 2 launches only
 };
 inline uint64_t next_epoch() {
   static std::atomic<uint64_t> e{0};
@@ -80,6 +89,11 @@ struct SpmmParams {
   int n0;      // first output column of this launch
   int stages;  // pipeline depth
   long long* trace;  // optional: per-block event timestamps of CTA 0 (HRPB_TRACE), [6][kTraceN]
+  // GM = 2 (row-sharded B): shard table (see ShardDesc); inv = 1 / rps for the shard estimate of a row
+  const float* sh_ptr[kMaxShards];
+  uint32_t sh_rps;
+  float sh_inv;
+  int nsh;
   int debug;         // HRPB_DEBUG bits (experiments only): 1 = skip C stores, 2 = skip decode, 4 = skip MMA issue,
                      // 8 = skip A bulk copy, 16 = B gather zero-fill only (no global reads), 32 = no B cp.async at all
 };
@@ -348,11 +362,12 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 // GM = gather mode: 0 = TMA tile::gather4 (one issuing lane per producer warp),
 //                   1 = cp.async 16-B copies by all 128 producer threads into the same swizzled layout.
 template <int NT, int GM, int TMV, int TKV>
-__global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant__ CUtensorMap tmB, SpmmParams prm) {
+__global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant__ CUtensorMap tmB,
+                                                    const __grid_constant__ SpmmParams prm) {
   pdl_wait();
   constexpr uint64_t kPW = panel_weight<TMV>();  // S1 units per panel epilogue
   using L = SmemLayout<NT, TMV, TKV>;
-  static_assert(GM == 1 || TKV == 16, "TMA gather4 staging is written for TK = 16");
+  static_assert(GM != 0 || TKV == 16, "TMA gather4 staging is written for TK = 16");
   constexpr int kARawBytes = L::kARawBytes, kATileBytes = L::kATileBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment by pointer arithmetic on the __shared__ array (an integer round trip would make every
@@ -387,7 +402,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       mbar_init(&full_a[s], 1);
       // B rows landed (one producer warp per block: 1 expect_tx arrive or 32 cp.async noinc arrivals) AND the
       // block's A tile is decoded (+1 decoder arrival): the MMA warp waits on this single barrier per block
-      mbar_init(&full_b[s], (GM == 0 ? 1 : 32) + 1);
+      mbar_init(&full_b[s], (GM == 0 ? 1 : 32) + 1);  // (GM 1, 2: cp.async)
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < L::kSlots; ++i) { mbar_init(&tfull[i], L::kMW); mbar_init(&tempty[i], 4); }
@@ -552,7 +567,17 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
           if (dbg(prm, 32)) break;
           const uint32_t rk = rr[rw];
           const bool real = rk < Kr && !(dbg(prm, 16));  // sentinel K -> zero fill (src-size 0)
-          const float* src = Blane + (uint64_t)(real ? rk : 0u) * ldb32;
+          const float* src;
+          if constexpr (GM == 2) {  // row-sharded B: shard r = rk / rps (float estimate, corrected by one step)
+            const uint32_t rq = real ? rk : 0u, rps = prm.sh_rps;
+            uint32_t r = __float2uint_rz(__uint2float_rz(rq) * prm.sh_inv);
+            r = min(r, (uint32_t)prm.nsh - 1u);
+            if (rq < r * rps) --r;
+            else if (r + 1u < (uint32_t)prm.nsh && rq >= (r + 1u) * rps) ++r;
+            src = prm.sh_ptr[r] + n0 + 4 * lane + (uint64_t)(rq - r * rps) * ldb32;
+          } else {
+            src = Blane + (uint64_t)(real ? rk : 0u) * ldb32;
+          }
           const uint32_t rowb = bt + (rw >> 2) * (L::kNA * 512) + (rw & 3) * 128;
 #ifdef HRPB_HOT_EXP  // experiment: L2 priority by an R-MAT popularity proxy (few one bits in the id)
           const uint64_t pol = __popc(rk) <= HRPB_HOT_EXP ? pol_hot : pol_cold;
@@ -957,7 +982,14 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   int grid = num_sms();
   if ((int64_t)grid > p_hi - p_lo) grid = (int)(p_hi > p_lo ? p_hi - p_lo : 1);
   SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, p_lo, p_hi, scr.ws, scr.flag, scr.epoch,
-                 scr.ranges, B, h->K, ldb, n0, stages, trace, debug};
+                 scr.ranges, B, h->K, ldb, n0, stages, trace, {}, 0u, 0.f, 0, debug};
+  if (GM == 2) {
+    if (!scr.sd) return HRPB_ERROR_INVALID_VALUE;
+    for (int r = 0; r < scr.sd->nsh; ++r) prm.sh_ptr[r] = scr.sd->ptr[r];
+    prm.sh_rps = scr.sd->rps;
+    prm.sh_inv = 1.0f / (float)scr.sd->rps;
+    prm.nsh = scr.sd->nsh;
+  }
   launch_pdl(k_spmm<NT, GM, TMV, TKV>, grid, kSpmmThreads, smem, s, tm, prm);
   launch_pdl(k_spmm_fixup<TMV>, grid, 128, 0, s, h->brp, (const uint64_t*)scr.ranges, scr.ws, C, h->M, N, n0, 128 * NT,
              scr.flag, scr.epoch);
@@ -976,7 +1008,10 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);
 }
 
-// one translation unit per TK instantiates its kernels (parallel compilation): spmm_tk16.cu, spmm_tk32.cu
+// one translation unit per TK instantiates its kernels (parallel compilation): spmm_tk16.cu, spmm_tk32.cu; the
+// row-sharded B variant (GM = 2) for both TK in spmm_sharded.cu
+hrpb_status_t spmm_dispatch_sharded(const hrpb_handle* h, const CUtensorMap& tm, float* C, int64_t N, int n0, int nt,
+                                    int64_t p_lo, int64_t p_hi, const Scratch& scr, cudaStream_t s);
 template <int TKV>
 hrpb_status_t spmm_dispatch(const hrpb_handle* h, const CUtensorMap& tm, const float* Bt, int64_t ld, float* C,
                             int64_t N, int n0, int nt, int gm, int64_t p_lo, int64_t p_hi, const Scratch& scr,

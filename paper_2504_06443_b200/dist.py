@@ -105,3 +105,40 @@ def _cuda_compute(rp_l, ci_l, v_l, nrows, K, B):
     t = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(dev)
     A = hp.build(t(rp_l), t(ci_l), t(v_l), nrows, K)
     return hp.spmm(A, B)
+
+
+# ------------------------------------------------------------------ NEXT-3: B row-sharded, peer gathers
+def b_row_shards(K: int, world: int) -> tuple[int, list[tuple[int, int]]]:
+    """Row sharding of B for hrpb_spmm_sharded: rows_per_shard = ceil(K / world) and every
+    rank's [row0, row1) (the last ranks may hold fewer rows, or none when world > K). The kernel takes exactly
+    ceil(K / rows_per_shard) shards, so ranks past that count hold no rows and are not in the shard table."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    rps = max(1, -(-K // world))
+    return rps, [(min(r * rps, K), min((r + 1) * rps, K)) for r in range(world)]
+
+
+def peer_shards(B_local, K: int, group=None):
+    """Every rank holds its B row shard (rows b_row_shards(K, world)[1][rank], CUDA, contiguous); returns the shard
+    table for hrpb_spmm_sharded: this rank's own tensor and every other rank's shard mapped into this process by
+    CUDA IPC (device memory of the peer GPU, read over NVLink by the SpMM's gathers; peer access is enabled by the
+    library per device pair). One all_gather of IPC handles is the only exchange (no B replica, no broadcast).
+    Needs one process per GPU on one node with every GPU visible (torchrun's default)."""
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    rps, rows = b_row_shards(K, world)
+    nsh = -(-K // rps) if K > 0 else 1
+    if tuple(B_local.shape[:1]) != (rows[rank][1] - rows[rank][0],):
+        raise ValueError(f"rank {rank} must hold {rows[rank][1] - rows[rank][0]} rows of B")
+    mine = reduce_tensor(B_local) if B_local.numel() else None
+    handles = [None] * world
+    dist.all_gather_object(handles, mine, group=group)
+    shards = []
+    for r in range(nsh):
+        if r == rank:
+            shards.append(B_local)
+        else:
+            fn, args = handles[r]
+            shards.append(fn(*args))
+    return rps, shards

@@ -58,6 +58,7 @@ def lib():
         i64, vp = C.c_int64, C.c_void_p
         L.hrpb_build.argtypes = [i64, i64, i64, vp, vp, vp, C.POINTER(_Config), vp, C.POINTER(vp)]
         L.hrpb_spmm.argtypes = [vp, vp, vp, i64, i64, i64, vp]
+        L.hrpb_spmm_sharded.argtypes = [vp, C.POINTER(vp), C.c_int32, i64, vp, i64, i64, i64, vp]
         L.hrpb_build_spmm_host.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Config), vp]
         L.hrpb_build_spmm.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Config), vp,
                                       C.POINTER(vp), C.POINTER(C.c_float)]
@@ -70,7 +71,7 @@ def lib():
         L.hrpb_get_error_string.restype = C.c_char_p
         L.hrpb_last_cuda_error.restype = C.c_int
         L.hrpb_launch_count.restype = C.c_int64
-        for f in ("hrpb_build", "hrpb_spmm", "hrpb_build_spmm", "hrpb_build_spmm_async", "hrpb_sync_status",
+        for f in ("hrpb_build", "hrpb_spmm", "hrpb_spmm_sharded", "hrpb_build_spmm", "hrpb_build_spmm_async", "hrpb_sync_status",
                   "hrpb_build_spmm_host", "hrpb_free", "hrpb_get_view", "hrpb_copy_view_to_host"):
             getattr(L, f).restype = C.c_int
         _lib = L
@@ -201,6 +202,36 @@ def spmm(A: Hrpb, B, out=None, stream=None):
     st = lib().hrpb_spmm(A.handle, _dev(B, torch.float32, "B"), _dev(out, torch.float32, "out"), A.M, A.K, N,
                          _stream(stream))
     _check(st, "hrpb_spmm")
+    return out
+
+
+def spmm_sharded(A: Hrpb, shards, rows_per_shard: int, out=None, stream=None):
+    """hrpb_spmm_sharded: C = A.B with B given as row shards: shards[r] is a CUDA float32
+    tensor holding B rows [r * rows_per_shard, min((r + 1) * rows_per_shard, K)) — on this device, or another GPU's
+    memory mapped here (dist.peer_shards). Returns C (M x N) on the current device."""
+    import torch
+    shards = list(shards)
+    if not shards:
+        raise ValueError("at least one shard")
+    N = int(shards[0].shape[1]) if shards[0].dim() == 2 else -1
+    nsh = len(shards)
+    for r, t in enumerate(shards):
+        rows = max(0, min((r + 1) * rows_per_shard, A.K) - r * rows_per_shard)
+        if t.dim() != 2 or tuple(t.shape) != (rows, N):
+            raise ValueError(f"shard {r} must be ({rows}, {N}), got {tuple(t.shape)}")
+        if t.dtype != torch.float32 or not t.is_contiguous() or not t.is_cuda:
+            raise TypeError(f"shard {r} must be a contiguous CUDA float32 tensor")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if out is None:
+        out = torch.empty((A.M, N), dtype=torch.float32, device=dev)
+    elif tuple(out.shape) != (A.M, N):
+        raise ValueError(f"out must be ({A.M}, {N}), got {tuple(out.shape)}")
+    else:
+        _dev(out, torch.float32, "out", A.M * N)
+    ptrs = (C.c_void_p * nsh)(*[t.data_ptr() if t.numel() else 16 for t in shards])  # (empty shard: never read)
+    st = lib().hrpb_spmm_sharded(A.handle, ptrs, nsh, int(rows_per_shard), C.c_void_p(out.data_ptr()), A.M, A.K, N,
+                                 _stream(stream))
+    _check(st, "hrpb_spmm_sharded")
     return out
 
 

@@ -130,3 +130,18 @@ def test_shard_plan_explicit_weights():
     assert max(per) - wts.sum() / 4 <= wts.max() + 1
     with pytest.raises(ValueError):
         hd.shard_plan(w.row_ptr, 4, 16, wts[:-1])
+
+
+def test_b_row_shards_cover_rows():
+    for K in (0, 1, 7, 100, 4194304):
+        for world in (1, 2, 3, 8):
+            rps, rows = hd.b_row_shards(K, world)
+            assert rows[0][0] == 0 and rows[-1][1] == K
+            for (a0, a1), (b0, b1) in zip(rows, rows[1:]):
+                assert a1 == b0 and a0 <= a1
+            nsh = -(-K // rps) if K else 1
+            assert nsh <= world
+            # the shards the kernel addresses: rank r < nsh holds rows [r rps, min((r + 1) rps, K))
+            for r in range(nsh):
+                assert rows[r] == (r * rps, min((r + 1) * rps, K))
+            assert all(a == b for a, b in rows[nsh:]) or K == 0
