@@ -19,6 +19,7 @@
 #include <cstdio>
 
 #include <cub/block/block_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
 #include "internal.h"
@@ -35,6 +36,10 @@ enum : uint32_t {
 
 constexpr int kSmallThreads = 128;
 constexpr int kSmallCap = 2048;      // entries per panel handled in shared memory
+#ifndef HRPB_3P_MIN_PANELS
+#define HRPB_3P_MIN_PANELS 196608
+#endif
+constexpr int64_t kThreePhaseMinPanels = HRPB_3P_MIN_PANELS;  // k_wbuild count / scan / emit from this many panels
 constexpr int kSpanWords = 512;      // bitmap ranking when the panel's column span <= 16384
 constexpr int kBigThreads = 512;
 #ifndef HRPB_BIG_CTAS_PER_SM
@@ -824,7 +829,12 @@ __device__ unsigned long long g_btrace[8];  // per-phase cycles summed over warp
 // sizePtr, HRPB-v1 headers + patterns + zero padding (R7), values in brick-CSC order at popcount
 // ranks, activeCols with sentinel K (R2, R6). Listed panels only take part in the scan
 // with the (nblk, bytes) their CTA / hub count produced; k_emit writes them afterwards.
-template <int tm, int tk>
+// MODE 0: single pass (the look-back above). MODE 1 (count): every panel's packed (blocks << 34 | bytes) into
+// lb[p], no emission; a device scan then gives the exclusive prefixes; MODE 2 (emit): the panel is ranked again and
+// emitted at the scanned offset lb[p], no waiting. The look-back ties every warp to the slowest panel among the
+// ~4K in flight (each waits for all predecessors' aggregates): on irregular matrices (c3: 4 us to 20 us panels)
+// counting twice is cheaper than waiting.
+template <int tm, int tk, int MODE>
 __global__ void __launch_bounds__(32 * kWWarps, HRPB_WB_MINB) k_wbuild(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                                         const float* __restrict__ vals, int64_t M, int64_t K,
                                                         int64_t nnz, int64_t P, const uint8_t* __restrict__ listed,
@@ -888,8 +898,8 @@ __global__ void __launch_bounds__(32 * kWWarps, HRPB_WB_MINB) k_wbuild(const int
         warp_panel_rank<tm, tk>(scol, K, w, my, L, status);
         BT_MARK(3);
         __syncwarp();  // the staged columns are dead: the values go into the same window, landing meanwhile
-        vsh = warp_stage(vals, nnz, w.e0, w.E, my + L.off_stage, al16);
-        prep = !w.sorted && w.nblk <= kChunkBlk;
+        if (MODE != 1) vsh = warp_stage(vals, nnz, w.e0, w.E, my + L.off_stage, al16);
+        prep = MODE != 1 && !w.sorted && w.nblk <= kChunkBlk;
         for (uint32_t jb0 = 0; jb0 < w.nblk; jb0 += kChunkBlk) {
           const uint32_t nb = min(kChunkBlk, w.nblk - jb0);
           if (!w.patterns_done) warp_panel_patterns<tm, tk>(w, my, L, jb0, nb);
@@ -923,7 +933,11 @@ __global__ void __launch_bounds__(32 * kWWarps, HRPB_WB_MINB) k_wbuild(const int
     }
     BT_MARK(4);
     const uint64_t agg = ((uint64_t)w.nblk << 34) | bytes;
-    warp_lb_publish(lb, p, agg);
+    if (MODE == 1) {  // count pass: the aggregate only (the device scan turns lb into exclusive prefixes)
+      if (lane == 0) lb[p] = agg;
+      continue;
+    }
+    if (MODE == 0) warp_lb_publish(lb, p, agg);
     if (prep) {  // entry destinations: sq[i] <- (block << 11) | value index in the block (0xFFFF stays invalid)
       __syncwarp();
       uint16_t* sqw = reinterpret_cast<uint16_t*>(my + L.off_q);
@@ -952,7 +966,7 @@ __global__ void __launch_bounds__(32 * kWWarps, HRPB_WB_MINB) k_wbuild(const int
           if (c0 + 32 * u + lane < w.E) sqw[c0 + 32 * u + lane] = (uint16_t)code[u];
       }
     }
-    const uint64_t ex = warp_lb_wait(lb, p, agg);
+    const uint64_t ex = MODE == 0 ? warp_lb_wait(lb, p, agg) : lb[p];
     BT_MARK(5);
     const uint32_t b0 = (uint32_t)(ex >> 34);
     const uint64_t pbase = ex & ((1ull << 34) - 1);
@@ -2693,20 +2707,19 @@ __global__ void k_finalize(const int64_t* __restrict__ rp, int64_t M, int64_t nn
     }                                                                                \
   } while (0)
 
-template <int TM, int TK>
+template <int TM, int TK, int MODE>
 static int wbuild_ctas() {  // resident CTAs of k_wbuild per SM (the ticket loop is persistent)
   static std::atomic<uint64_t> done{0};  // the shared-memory attribute is per device
   static std::atomic<int> n{0};
   if (first_on_device(done)) {
     const size_t smem = (size_t)warp_layout(TM, TK).bytes * kWWarps;
-    cudaFuncSetAttribute(k_wbuild<TM, TK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_wbuild<TM, TK, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int m = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k_wbuild<TM, TK>, 32 * kWWarps, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k_wbuild<TM, TK, MODE>, 32 * kWWarps, smem);
     n = m < 1 ? 1 : m;
   }
   return n;
 }
-
 static void launch_wclassify(int tm, int tk, unsigned grid, cudaStream_t s, const int64_t* rp, const int32_t* ci,
                              int64_t M, int64_t nnz, int64_t P, uint8_t* listed, uint32_t* list, uint32_t* nlist,
                              uint32_t* biglist, uint32_t* nbig, uint32_t* nhuge, int64_t huge_cap) {
@@ -2716,21 +2729,42 @@ static void launch_wclassify(int tm, int tk, unsigned grid, cudaStream_t s, cons
 #undef HRPB_WC
 }
 
-static void launch_wbuild(int tm, int tk, cudaStream_t s, const int64_t* rp, const int32_t* ci, const float* vals,
-                          int64_t M, int64_t K, int64_t nnz, int64_t P, const uint8_t* listed,
+static void launch_wbuild(int mode, int tm, int tk, cudaStream_t s, const int64_t* rp, const int32_t* ci,
+                          const float* vals, int64_t M, int64_t K, int64_t nnz, int64_t P, const uint8_t* listed,
                           const uint32_t* nblk_listed, const uint32_t* pbytes_listed, uint32_t* ticket,
                           uint64_t* lb, uint32_t* brp, uint64_t* poff, uint32_t* ac,
                           uint64_t* sp, uint8_t* packed, uint32_t* status) {
   const size_t smem = (size_t)warp_layout(tm, tk).bytes * kWWarps;
-#define HRPB_WB(A, B)                                                                                          \
+#define HRPB_WB_M(A, B, MO)                                                                                    \
   {                                                                                                            \
-    const int64_t want = ceil_div(P, kWWarps), have = (int64_t)wbuild_ctas<A, B>() * num_sms();                \
-    launch_pdl(k_wbuild<A, B>, (unsigned)(want < have ? want : have), 32 * kWWarps, smem, s,                   \
+    const int64_t want = ceil_div(P, kWWarps), have = (int64_t)wbuild_ctas<A, B, MO>() * num_sms();            \
+    launch_pdl(k_wbuild<A, B, MO>, (unsigned)(want < have ? want : have), 32 * kWWarps, smem, s,               \
         rp, ci, vals, M, K, nnz, P, listed, nblk_listed, pbytes_listed, ticket, lb, brp, poff,                \
         ac, sp, packed, status);                                                                               \
   }
+#define HRPB_WB(A, B)                                                                                          \
+  {                                                                                                            \
+    if (mode == 1) HRPB_WB_M(A, B, 1) else if (mode == 2) HRPB_WB_M(A, B, 2) else HRPB_WB_M(A, B, 0)          \
+  }
   HRPB_WDISPATCH(HRPB_WB);
 #undef HRPB_WB
+#undef HRPB_WB_M
+}
+
+// three-phase warp path (count, scan, emit) instead of the single pass with look-back: chosen by panel count
+// (HRPB_WB_MODE=1 / 0 forces it on / off for experiments). Measured (build ms, single pass -> three-phase): c3
+// (262K panels, 24% listed, warp panels of 1..512 entries) 5.69 -> 5.31; c4 (131K uniform 128-entry panels) 0.79
+// -> 0.99; c2a / c2b (16K panels at TM = 64) 0.27 -> 0.34; c5 (31K listed panels) 1.10 -> 1.07. The look-back
+// only costs when thousands of in-flight panels of very different sizes wait on each other, which takes a large
+// panel count; the count pass repeats the ranking, which costs on uniform matrices.
+static bool use_three_phase(int64_t M, int64_t nnz, int64_t P, int tm) {
+  static const int forced = [] {
+    const char* e = getenv("HRPB_WB_MODE");
+    return e ? atoi(e) : -1;
+  }();
+  if (forced >= 0) return forced != 0;
+  (void)M; (void)nnz; (void)tm;
+  return P >= kThreePhaseMinPanels;
 }
 
 hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
@@ -2763,6 +2797,16 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   // nbig, nl1, ticket, hub work, status, emit work, hub (count << 32 | chunks) x2, count work
   uint32_t* ctr = (uint32_t*)dalloc(16 * sizeof(uint32_t), s);
   uint64_t* lb = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t), s);  // look-back states (blocks << 34 | bytes)
+  // three-phase warp path (see k_wbuild): when not every panel is on the warp path, or on many small panels
+  const bool three_phase = use_three_phase(M, nnz, P, tm);
+  uint64_t* lbx = nullptr;
+  void* scan_tmp_p = nullptr;
+  size_t scan_tmp = 0;
+  if (three_phase && P > 0) {
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, lb, lb, (int)(P + 1), s);
+    lbx = (uint64_t*)dalloc((P + 1) * sizeof(uint64_t) + scan_tmp + 16, s);
+    scan_tmp_p = lbx ? (void*)(lbx + P + 1) : nullptr;
+  }
   uint8_t* listed = (uint8_t*)dalloc(P + 1, s);
   uint64_t* info = (uint64_t*)dalloc(4 * sizeof(uint64_t), s);  // [3] = status word | hub count
   const int big_ctas = HRPB_BIG_CTAS_PER_SM * num_sms();
@@ -2787,7 +2831,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   if (nb_cap >= (1ll << 28) || bytes_cap >= (1ll << 34)) {
     st = HRPB_ERROR_NOT_SUPPORTED;
   } else if (!h->brp || !h->ac || !h->sp || !h->packed || !q || !cnt || !poff || !gpat || !biglist || !info ||
-             !bigscr || !ctr || !lb || !listed || !relb || !hub2) {
+             !bigscr || !ctr || !lb || !listed || !relb || !hub2 || (three_phase && P > 0 && !lbx)) {
     st = HRPB_ERROR_OUT_OF_MEMORY;
   }
   uint64_t hinfo[3] = {0, 0, 0};
@@ -2838,9 +2882,20 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
       else
         launch_pdl(k_count_big, big_ctas, kBigThreads, 0, s, row_ptr, col_idx, M, K, nnz, tm, tk, q, nact, nblk,
                    pbytes, gpat, biglist, nbig, bigscr, words, ctr + 3, status);
-      // B1-B5 for warp-path panels + the single-pass scans B2 / B4 for all panels
-      launch_wbuild(tm, tk, s, row_ptr, col_idx, values, M, K, nnz, P, listed, nblk, pbytes, ticket, lb, h->brp,
-                    poff, h->ac, h->sp, h->packed, status);
+      // B1-B5 for warp-path panels + the scans B2 / B4 for all panels: one pass with a decoupled look-back, or
+      // (three-phase) count pass, device scan of the packed (blocks << 34 | bytes), emit pass
+      if (three_phase) {
+        launch_wbuild(1, tm, tk, s, row_ptr, col_idx, values, M, K, nnz, P, listed, nblk, pbytes, ctr + 14, lb,
+                      h->brp, poff, h->ac, h->sp, h->packed, status);
+        size_t tb = scan_tmp;
+        cub::DeviceScan::ExclusiveSum(scan_tmp_p, tb, lb, lbx, (int)(P + 1), s);
+        launch_wbuild(2, tm, tk, s, row_ptr, col_idx, values, M, K, nnz, P, listed, nblk, pbytes, ticket, lbx,
+                      h->brp, poff, h->ac, h->sp, h->packed, status);
+        note_launch(2);
+      } else {
+        launch_wbuild(0, tm, tk, s, row_ptr, col_idx, values, M, K, nnz, P, listed, nblk, pbytes, ticket, lb,
+                      h->brp, poff, h->ac, h->sp, h->packed, status);
+      }
       launch_pdl(k_emit, emit_ctas, kEmitNT, emit_smem, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp,
                  poff, gpat, h->ac, h->sp, h->packed, l1, nl1, hublist, hubch, nhub, ctr + 5, (int)hub_dense);
       if (hub_2l)
@@ -2883,7 +2938,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
   }
   dfree(q, s); dfree(cnt, s); dfree(poff, s); dfree(gpat, s); dfree(biglist, s); dfree(info, s);
   dfree(bigscr, s); dfree(relb, s); dfree(hub2, s);
-  dfree(ctr, s); dfree(lb, s); dfree(listed, s);
+  dfree(ctr, s); dfree(lb, s); dfree(lbx, s); dfree(listed, s);
   if (deferred_info) {
     h->NB = -1;  // unknown until build_finish
     return st;
