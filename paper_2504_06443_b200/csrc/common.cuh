@@ -69,6 +69,12 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity, 
   while (!mbar_try_wait(b, parity)) __nanosleep(ns);
 }
 
+__device__ __forceinline__ uint64_t globaltimer() {  // ns, comparable across SMs
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ------------------------------------------------------------------ TMA / bulk copies
 // 1-D bulk copy global -> shared, completes bytes on `bar` (size and addresses 16-B aligned).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,

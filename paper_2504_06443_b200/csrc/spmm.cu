@@ -100,16 +100,27 @@ hrpb_status_t spmm_core(const hrpb_handle* h, const float* B, int64_t ldb, float
     Bt = bpad;
     ld = ldp;
   }
-  // grid x 2 tiles x TM x (128 NT) partial tiles (TM * 128 NT <= 64 * 512 for every instantiated pair), the
-  // split flag, and the grid's S1 ranges
-  const size_t ws_bytes = (size_t)num_sms() * 2 * 64 * 512 * sizeof(float);
-  float* ws = (float*)dalloc(ws_bytes + 64 + (size_t)num_sms() * 4 * sizeof(uint64_t), s);
+  // S1 shares: one per CTA (static), or kDynShares per SM claimed dynamically on long launches (DESIGN.md §6 S1:
+  // the static cost model leaves c3's CTAs at 1.15x max/mean; the share claimed last ends at most about one share
+  // after the mean). The host cannot see the block count of an asynchronous build, so "long" is read from nnz.
+  const int64_t ncols_max = N < 512 ? N : 512;
+  // (HRPB_STATIC_S1 / HRPB_DYN_S1: force either, for experiments and the parity tests of small matrices)
+  const int64_t shares = min((int64_t)kDynShares * num_sms(), p_hi - p_lo);
+  const bool dyn = getenv("HRPB_STATIC_S1") == nullptr && h->tm <= 32 && shares >= num_sms() &&
+                   (h->nnz >= kDynMinNnz || getenv("HRPB_DYN_S1") != nullptr);
+  const uint32_t nchunks = dyn ? (uint32_t)shares : 0u;
+  // shares x 2 tiles x TM x (128 NT) partial tiles (static: TM * 128 NT <= 64 * 512 for every instantiated pair),
+  // the split flag, the claim counter and the shares' S1 ranges
+  const size_t ws_bytes = dyn ? (size_t)nchunks * 2 * h->tm * (size_t)(ceil_div(ncols_max, 128) * 128) * sizeof(float)
+                              : (size_t)num_sms() * 2 * 64 * 512 * sizeof(float);
+  const size_t nshares = dyn ? nchunks : (size_t)num_sms();
+  float* ws = (float*)dalloc(ws_bytes + 64 + nshares * 4 * sizeof(uint64_t), s);
   if (!ws) {
     dfree(bpad, s);
     return HRPB_ERROR_OUT_OF_MEMORY;
   }
   uint64_t* flag = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ws) + ws_bytes);
-  Scratch scr{ws, flag, next_epoch(), flag + 8, sd};
+  Scratch scr{ws, flag, next_epoch(), flag + 8, sd, nchunks, reinterpret_cast<uint32_t*>(flag + 4)};
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));  // (unused by the row-sharded cp.async gather: passed zeroed)
   if (!sd) {

@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -64,8 +65,10 @@ struct Scratch {
   float* ws;
   uint64_t* flag;
   uint64_t epoch;
-  uint64_t* ranges;  // [grid][4]: every CTA's S1 range (CtaWork), read by k_spmm_fixup
+  uint64_t* ranges;  // [shares][4]: every S1 share's range (CtaWork), read by k_spmm_fixup
   const ShardDesc* sd = nullptr;  // GM = 2 launches only
+  uint32_t nchunks = 0;   // dynamic S1: shares (0 = static, one share per CTA)
+  uint32_t* ctr = nullptr;  // dynamic S1 claim counter
 };
 inline uint64_t next_epoch() {
   static std::atomic<uint64_t> e{0};
@@ -94,6 +97,10 @@ struct SpmmParams {
   uint32_t sh_rps;
   float sh_inv;
   int nsh;
+  uint32_t nchunks;     // 0: static S1 (CTA c takes share c of G); else dynamic: nchunks shares (ranges precomputed by
+                        // k_spmm_chunks), CTA c starts with share c and then claims shares G, G + 1, ... in order
+  uint32_t* chunk_ctr;  // claim counter (zeroed by k_spmm_chunks)
+  long long* cta_t;  // optional (HRPB_CTA_TIMES): per CTA {globaltimer at entry, at exit, blocks, panels}
   int debug;         // HRPB_DEBUG bits (experiments only): 1 = skip C stores, 2 = skip decode, 4 = skip MMA issue,
                      // 8 = skip A bulk copy, 16 = B gather zero-fill only (no global reads), 32 = no B cp.async at all
 };
@@ -188,6 +195,13 @@ struct SmemLayout {
 #define HRPB_PANEL_W 5
 #endif
 constexpr uint64_t kPanelW = HRPB_PANEL_W;
+// dynamic S1 (long launches): shares per SM, claimed in order by the persistent CTAs, and the nnz from which a launch
+// counts as long (c3, 128M nnz, ~13 ms; c4 / c5 / c2a at <= 40M nnz are balanced by the static model)
+#ifndef HRPB_DYN_SHARES
+#define HRPB_DYN_SHARES 16
+#endif
+constexpr int kDynShares = HRPB_DYN_SHARES;
+constexpr int64_t kDynMinNnz = 64ll << 20;
 #ifndef HRPB_PANEL_W32
 #define HRPB_PANEL_W32 5
 #endif
@@ -263,13 +277,14 @@ struct CtaWork {
   uint32_t bB, bE;     // its flat block range
   bool first_full, last_full;  // owns all units of pa / of pb - 1
 };
+// the share between boundaries f0 < f1 of a grid of G equal shares (cta_work: f0 = c, f1 = c + 1)
 template <uint64_t PW, typename FIND>
-__device__ __forceinline__ CtaWork cta_work(const uint32_t* brp, int64_t p_lo, int64_t p_hi, uint64_t c, uint64_t G,
-                                            FIND find) {
+__device__ __forceinline__ CtaWork cta_work_span(const uint32_t* brp, int64_t p_lo, int64_t p_hi, uint64_t f0,
+                                                 uint64_t f1, uint64_t G, FIND find) {
   CtaWork w;
   int64_t p0, p1;
-  const uint64_t t0 = work_boundary<PW>(brp, p_lo, p_hi, c, G, p0, find);
-  const uint64_t t1 = work_boundary<PW>(brp, p_lo, p_hi, c + 1, G, p1, find);
+  const uint64_t t0 = work_boundary<PW>(brp, p_lo, p_hi, f0, G, p0, find);
+  const uint64_t t1 = work_boundary<PW>(brp, p_lo, p_hi, f1, G, p1, find);
   if (t1 <= t0) {
     w.pa = w.pb = p_lo;
     w.bB = w.bE = brp[p_lo];
@@ -298,6 +313,11 @@ __device__ __forceinline__ CtaWork cta_work(const uint32_t* brp, int64_t p_lo, i
     }
   }
   return w;
+}
+template <uint64_t PW, typename FIND>
+__device__ __forceinline__ CtaWork cta_work(const uint32_t* brp, int64_t p_lo, int64_t p_hi, uint64_t c, uint64_t G,
+                                            FIND find) {
+  return cta_work_span<PW>(brp, p_lo, p_hi, c, c + 1, G, find);
 }
 template <uint64_t PW>
 struct WarpFind {
@@ -394,6 +414,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   long long wacc = 0;
+  if (prm.cta_t && tid == 0) prm.cta_t[4 * blockIdx.x] = (long long)globaltimer();
   const long long t_start = kInstr ? clock64() : 0;
   const uint32_t tmem_cols = L::kTmemCols;
 
@@ -411,29 +432,43 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     prefetch_tmap(&tmB);
   }
   if (warp == kMmaWarp) tmem_alloc(&misc[0], tmem_cols);
+  const uint32_t* __restrict__ brp = prm.brp;
+  const int n0 = prm.n0;
+  const int64_t N = prm.N, M = prm.M;
+  uint32_t tbase = 0;
+  // running state across this CTA's shares (dynamic S1): blocks of earlier shares (the block index that picks
+  // stages, parities and the MMA warp continues), and the panel counters of the MMA warps and the epilogue (TMEM
+  // slot sequence)
+  uint32_t base = 0, pc_mma = 0, pc_epi = 0;
+  uint32_t chunk = blockIdx.x;
+  for (;;) {
   if (warp == 0) {  // S1: contiguous range of ~equal work (blocks + panels) in [p_lo, p_hi); big panels may split
-    const CtaWork cw = cta_work<kPW>(prm.brp, prm.p_lo, prm.p_hi, blockIdx.x, gridDim.x, WarpFind<kPW>());
-    if (lane == 0) {
-      range[0] = cw.pa; range[1] = cw.pb; range[2] = cw.bB; range[3] = cw.bE;
-      range[4] = cw.first_full; range[5] = cw.last_full;
-      if (cw.bB < cw.bE && !(cw.first_full && cw.last_full)) *prm.split_flag = prm.epoch;
-      uint64_t* rg = prm.ranges + 4 * blockIdx.x;  // (the fix-up reads the ranges instead of re-deriving them)
-      rg[0] = (uint64_t)cw.pa;
-      rg[1] = (uint64_t)cw.pb;
-      rg[2] = (uint64_t)cw.bB | ((uint64_t)cw.bE << 32);
-      rg[3] = (uint64_t)cw.first_full | ((uint64_t)cw.last_full << 1);
+    if (prm.nchunks == 0) {
+      const CtaWork cw = cta_work<kPW>(prm.brp, prm.p_lo, prm.p_hi, blockIdx.x, gridDim.x, WarpFind<kPW>());
+      if (lane == 0) {
+        range[0] = cw.pa; range[1] = cw.pb; range[2] = cw.bB; range[3] = cw.bE;
+        range[4] = cw.first_full; range[5] = cw.last_full;
+        if (cw.bB < cw.bE && !(cw.first_full && cw.last_full)) *prm.split_flag = prm.epoch;
+        uint64_t* rg = prm.ranges + 4 * blockIdx.x;  // (the fix-up reads the ranges instead of re-deriving them)
+        rg[0] = (uint64_t)cw.pa;
+        rg[1] = (uint64_t)cw.pb;
+        rg[2] = (uint64_t)cw.bB | ((uint64_t)cw.bE << 32);
+        rg[3] = (uint64_t)cw.first_full | ((uint64_t)cw.last_full << 1);
+      }
+    } else if (lane == 0) {  // the share's range, precomputed by k_spmm_chunks
+      const uint64_t* rg = prm.ranges + 4 * (size_t)chunk;
+      range[0] = (int64_t)rg[0]; range[1] = (int64_t)rg[1];
+      range[2] = (int64_t)(uint32_t)rg[2]; range[3] = (int64_t)(rg[2] >> 32);
+      range[4] = (int64_t)(rg[3] & 1); range[5] = (int64_t)((rg[3] >> 1) & 1);
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = misc[0];
+  tbase = misc[0];
   const int64_t pa = range[0], pb = range[1];
   const uint32_t cbB = (uint32_t)range[2], cbE = (uint32_t)range[3];
   const bool first_full = range[4] != 0, last_full = range[5] != 0;
-  const uint32_t* __restrict__ brp = prm.brp;
-  const int n0 = prm.n0;
-  const int64_t N = prm.N, M = prm.M;
 
   if (warp < kProdWarps) {
     // ---------------------------------------------------------------- producers (warps 0..3)
@@ -496,8 +531,9 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       for (int rq = 0; rq < 4; ++rq) doff[t][rq] = at * 512 + ((g ^ rq) << 5) + ((c & 1) << 4);
       col_ok[t] = (n0 + 4 * c) < N && at < na_eff;
     }
-    int s = pw % S;
-    uint32_t ph = (pw / S) & 1;
+    const uint32_t i0p = base + (uint32_t)pw;  // running block index of this warp's first block of the share
+    int s = (int)(i0p % (uint32_t)S);
+    uint32_t ph = (i0p / (uint32_t)S) & 1u;
     int64_t b = b_begin + pw;
 #pragma unroll
     for (int q = 0; q < kPfRing; ++q) fetch(b + 4 * q, q);
@@ -602,6 +638,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       s += 4;
       if (s >= S) { s -= S; ph ^= 1; }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // (the look-ahead groups past the share's end)
   } else if (warp < kMmaWarp) {
     // ---------------------------------------------------------------- decoders (block i -> warp 4 + i % 4)
     // Lane l expands bits l and l+32 of each brick. All four patterns are loaded first, then
@@ -610,8 +647,9 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     const int64_t b_begin = cbB, b_end = cbE;
     const uint32_t nib_sh = (uint32_t)(lane & 15) * 4u;            // tile row r with r % 16 == lane % 16
     const uint64_t below_row = (1ull << nib_sh) - 1ull;            // pattern bits of the rows above it
-    int s = dw % S;
-    uint32_t ph = (dw / S) & 1;
+    const uint32_t i0d = base + (uint32_t)dw;
+    int s = (int)(i0d % (uint32_t)S);
+    uint32_t ph = (i0d / (uint32_t)S) & 1u;
     for (int64_t b = b_begin + dw; b < b_end; b += kDecWarps) {
       mbar_wait_acc(prm, &full_a[s], ph, wacc);
       if (lane == 0) trace_ev(prm, 1, (uint32_t)(b - b_begin));
@@ -726,7 +764,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     const int mw = warp - kMmaWarp;
     if (mw < kMW) {
       const int64_t b_begin = cbB;
-      uint32_t pc = 0;
+      uint32_t pc = pc_mma;
       constexpr uint32_t kIdesc = idesc_tf32<TMV>();
       // descriptors of stage 0; stage s adds s * stage bytes / 16 to the start-address field (no carry: < 256 KB)
       const uint64_t adesc0 = umma_sdesc(smem_u32(btile0), 512, L::kNA * 512, 1);
@@ -740,7 +778,8 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
         be = be < cbE ? be : cbE;
         if (bb >= be) continue;
         const uint32_t slot = pc % L::kSlots;
-        const uint32_t i0 = (uint32_t)(bb - b_begin), i1 = (uint32_t)(be - b_begin);  // CTA-local block range
+        // running block range of the panel here (the index continues across this CTA's shares)
+        const uint32_t i0 = base + (uint32_t)(bb - b_begin), i1 = base + (uint32_t)(be - b_begin);
         const uint32_t j0 = i0 + (((uint32_t)mw + kMW - i0 % kMW) % kMW);              // first own block
         mbar_wait_acc(prm, &tempty[slot], ((pc / L::kSlots) & 1) ^ 1, wacc);
         tc_fence_after();
@@ -777,13 +816,14 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
         __syncwarp();
         ++pc;
       }
+      pc_mma = pc;
     }
   } else {
     // ---------------------------------------------------------------- epilogue (last 4 warps)
     const int qd = warp & 3;            // TMEM lane quadrant accessible to this warp
     const int et = tid - 32 * kEpiWarp0;  // 0..127
     const int64_t ncols = min((int64_t)128 * NT, N - n0);
-    uint32_t pc = 0;
+    uint32_t pc = pc_epi;
     PanelCursor cursor(brp, pa, pb, lane);
     int64_t p;
     uint32_t bb, be;
@@ -800,14 +840,14 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       if (cb >= ce) continue;  // split panel without blocks here
       // accumulator sets written: MMA warp w took the blocks i = w (mod kMW) of the CTA-local range [i0, i0 + n)
       constexpr int kMW = L::kMW;
-      const uint32_t i0 = cb - cbB, nblk = ce - cb;
+      const uint32_t i0 = base + (cb - cbB), nblk = ce - cb;
       uint32_t cmask = 0;
 #pragma unroll
       for (int w = 0; w < kMW; ++w)
         if (nblk >= (uint32_t)kMW || ((uint32_t)w + kMW - i0 % kMW) % kMW < nblk) cmask |= 1u << w;
       // a split panel's share goes to this CTA's workspace tile (slot 0: its first panel, 1: its last)
       float* const obase = full ? prm.C + row0 * N + n0
-                                : prm.ws + ((int64_t)(2 * blockIdx.x + (p == pa ? 0 : 1)) * TMV) * (128 * NT);
+                                : prm.ws + ((int64_t)(2 * (int64_t)chunk + (p == pa ? 0 : 1)) * TMV) * (128 * NT);
       const int64_t ostride = full ? N : 128 * NT;
       const uint32_t slot = pc % L::kSlots;
 #if HRPB_EPI_SLEEP > 0
@@ -865,7 +905,19 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       if (lane == 0) mbar_arrive(&tempty[slot]);
       ++pc;
     }
+    pc_epi = pc;
   }
+  base += cbE - cbB;
+  if (prm.nchunks == 0) break;
+  // dynamic S1: every role is done with this share (the epilogue has stored its last panel, so every MMA, gather
+  // and decode of it completed); claim the next share in order
+  tc_fence_before();
+  if (tid == 0) misc[1] = atomicAdd(prm.chunk_ctr, 1u) + gridDim.x;
+  __syncthreads();
+  tc_fence_after();
+  chunk = misc[1];
+  if (chunk >= prm.nchunks) break;
+  }  // shares
   if (tracing(prm) && blockIdx.x == 0 && lane == 0) {
     prm.trace[8 * kTraceN + 2 * warp] = wacc;
     prm.trace[8 * kTraceN + 2 * warp + 1] = clock64() - t_start;
@@ -882,6 +934,36 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tbase, tmem_cols);
+  }
+  if (prm.cta_t && tid == 0) {
+    prm.cta_t[4 * blockIdx.x + 1] = (long long)globaltimer();
+    prm.cta_t[4 * blockIdx.x + 2] = (long long)range[3] - (long long)range[2];
+    prm.cta_t[4 * blockIdx.x + 3] = (long long)range[1] - (long long)range[0];
+  }
+}
+
+// Dynamic S1 (Scratch::nchunks > 0): the ranges of all shares, one warp each, before k_spmm (which then only
+// reads them as its CTAs claim shares), and the claim counter reset.
+template <uint64_t PW>
+__global__ void __launch_bounds__(128) k_spmm_chunks(const uint32_t* __restrict__ brp, int64_t p_lo, int64_t p_hi,
+                                                     uint32_t nchunks, uint64_t* __restrict__ ranges,
+                                                     uint64_t* split_flag, uint64_t epoch, uint32_t* ctr) {
+  pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ctr = 0u;
+  const uint64_t c = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (c >= nchunks) return;
+  // guided sizes: the first half of the shares are 3 fine units of a grid of 2 nchunks (3/4 of the work), the
+  // second half 1 unit each, so the shares claimed last (which decide when the launch ends) are 3x smaller
+  const uint64_t nA = nchunks / 2, F = 3 * nA + (nchunks - nA);
+  auto fine = [&](uint64_t x) { return x <= nA ? 3 * x : 3 * nA + (x - nA); };
+  const CtaWork cw = cta_work_span<PW>(brp, p_lo, p_hi, fine(c), fine(c + 1), F, WarpFind<PW>());
+  if ((threadIdx.x & 31) == 0) {
+    if (cw.bB < cw.bE && !(cw.first_full && cw.last_full)) *split_flag = epoch;
+    uint64_t* rg = ranges + 4 * c;
+    rg[0] = (uint64_t)cw.pa;
+    rg[1] = (uint64_t)cw.pb;
+    rg[2] = (uint64_t)cw.bB | ((uint64_t)cw.bE << 32);
+    rg[3] = (uint64_t)cw.first_full | ((uint64_t)cw.last_full << 1);
   }
 }
 
@@ -981,8 +1063,14 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   }();
   int grid = num_sms();
   if ((int64_t)grid > p_hi - p_lo) grid = (int)(p_hi > p_lo ? p_hi - p_lo : 1);
+  static const char* cta_path = getenv("HRPB_CTA_TIMES");  // diagnostics: per-CTA wall times of this launch
+  long long* cta_t = nullptr;
+  if (cta_path) {
+    cta_t = (long long*)dalloc(4 * (size_t)grid * sizeof(long long), s);
+    cudaMemsetAsync(cta_t, 0, 4 * (size_t)grid * sizeof(long long), s);
+  }
   SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, p_lo, p_hi, scr.ws, scr.flag, scr.epoch,
-                 scr.ranges, B, h->K, ldb, n0, stages, trace, {}, 0u, 0.f, 0, debug};
+                 scr.ranges, B, h->K, ldb, n0, stages, trace, {}, 0u, 0.f, 0, 0u, nullptr, nullptr, debug};
   if (GM == 2) {
     if (!scr.sd) return HRPB_ERROR_INVALID_VALUE;
     for (int r = 0; r < scr.sd->nsh; ++r) prm.sh_ptr[r] = scr.sd->ptr[r];
@@ -990,9 +1078,28 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     prm.sh_inv = 1.0f / (float)scr.sd->rps;
     prm.nsh = scr.sd->nsh;
   }
+  prm.cta_t = cta_t;
+  const uint32_t nch = scr.nchunks >= (uint32_t)grid ? scr.nchunks : 0u;  // dynamic S1 (shares >= CTAs)
+  if (nch) {
+    prm.nchunks = nch;
+    prm.chunk_ctr = scr.ctr;
+    launch_pdl(k_spmm_chunks<panel_weight<TMV>()>, (nch + 3) / 4, 128, 0, s, h->brp, p_lo, p_hi, nch, scr.ranges,
+               scr.flag, scr.epoch, scr.ctr);
+    note_launch();
+  }
   launch_pdl(k_spmm<NT, GM, TMV, TKV>, grid, kSpmmThreads, smem, s, tm, prm);
-  launch_pdl(k_spmm_fixup<TMV>, grid, 128, 0, s, h->brp, (const uint64_t*)scr.ranges, scr.ws, C, h->M, N, n0, 128 * NT,
-             scr.flag, scr.epoch);
+  if (cta_t) {  // (blocks the stream: diagnostics only)
+    std::vector<long long> host(4 * (size_t)grid);
+    cudaMemcpyAsync(host.data(), cta_t, host.size() * sizeof(long long), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (FILE* f = fopen(cta_path, "wb")) {
+      fwrite(host.data(), sizeof(long long), host.size(), f);
+      fclose(f);
+    }
+    dfree(cta_t, s);
+  }
+  launch_pdl(k_spmm_fixup<TMV>, nch ? (int)nch : grid, 128, 0, s, h->brp, (const uint64_t*)scr.ranges, scr.ws, C,
+             h->M, N, n0, 128 * NT, scr.flag, scr.epoch);
   note_launch(2);
   if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)
     static long long host[kTraceSlots * kTraceN];

@@ -581,3 +581,44 @@ def test_free_orders_after_spmm_on_other_streams():
         s2.synchronize()
         check_exact(C.cpu().numpy(), Cref, "spmm vs free on another stream")
         junk.free()
+
+
+@pytest.fixture
+def dyn_s1(monkeypatch):
+    monkeypatch.setenv("HRPB_DYN_S1", "1")  # dynamic S1 shares (read per call) on matrices below its size threshold
+
+
+@pytest.mark.parametrize("tm", [16, 32])
+@pytest.mark.parametrize("name,scale,N", [("c3", 9, 256), ("c3p", 9, 64), ("c5", 5, 128), ("c2a", 7, 520)])
+def test_spmm_dynamic_s1_shares(dyn_s1, name, scale, N, tm):
+    """Dynamic S1 (16 shares per SM claimed in order, split panels across shares through the fix-up): exact mode
+    bit-identical to the oracle, float mode within tolerance."""
+    w = synth.make(name, scale=scale, N=N, mode=synth.EXACT)
+    B = w.B()
+    A = gpu_build(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm)
+    C = hp.spmm(A, dev(B)).cpu().numpy()
+    check_exact(C, oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B), f"{name} tm={tm}")
+    wf = synth.make(name, scale=scale, N=N)
+    Bf = wf.B()
+    Af = gpu_build(wf.M, wf.K, wf.row_ptr, wf.col_idx, wf.vals, tm=tm)
+    Cf = hp.spmm(Af, dev(Bf)).cpu().numpy()
+    Cref, S = oracle.csr_spmm(wf.M, wf.K, wf.row_ptr, wf.col_idx, wf.vals, Bf, with_bound=True)
+    check_float(Cf, Cref, S, f"{name} tm={tm} float")
+
+
+def test_spmm_dynamic_s1_split_hubs(dyn_s1):
+    """Hub panels much larger than a share: split over many shares (and CTAs), summed by the fix-up."""
+    rng = np.random.default_rng(9)
+    M, K, N = 16 * 3000, 40000, 128
+    rp, ci, v = rand_csr(M, K, 0.0003, 5)
+    dense = np.zeros((M, K), bool)
+    for i in range(M):
+        dense[i, ci[rp[i]:rp[i + 1]]] = True
+    dense[[0, 1, 2, 17, 24000], :] = rng.random((5, K)) < 0.7
+    rp = np.zeros(M + 1, np.int64); rp[1:] = np.cumsum(dense.sum(1))
+    ci = np.nonzero(dense)[1].astype(np.int32)
+    v = rng.choice(np.array([-2, -1, 1, 2], np.float32), size=ci.size).astype(np.float32)
+    B = rng.choice(np.array([-1, 1, 2], np.float32), size=(K, N)).astype(np.float32)
+    A = gpu_build(M, K, rp, ci, v)
+    C = hp.spmm(A, dev(B)).cpu().numpy()
+    check_exact(C, oracle.csr_spmm(M, K, rp, ci, v, B), "dynamic split hubs")
