@@ -201,6 +201,11 @@ constexpr uint64_t kPanelW = HRPB_PANEL_W;
 #define HRPB_DYN_SHARES 16
 #endif
 constexpr int kDynShares = HRPB_DYN_SHARES;
+#ifndef HRPB_DYN_REV
+#define HRPB_DYN_REV 1
+#endif
+// position in the matrix of the share claimed as number k (see k_spmm_chunks)
+__host__ __device__ __forceinline__ uint32_t share_pos(uint32_t k, uint32_t n) { return HRPB_DYN_REV ? n - 1 - k : k; }
 constexpr int64_t kDynMinNnz = 64ll << 20;
 #ifndef HRPB_PANEL_W32
 #define HRPB_PANEL_W32 5
@@ -456,7 +461,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
         rg[3] = (uint64_t)cw.first_full | ((uint64_t)cw.last_full << 1);
       }
     } else if (lane == 0) {  // the share's range, precomputed by k_spmm_chunks
-      const uint64_t* rg = prm.ranges + 4 * (size_t)chunk;
+      const uint64_t* rg = prm.ranges + 4 * (size_t)share_pos(chunk, prm.nchunks);
       range[0] = (int64_t)rg[0]; range[1] = (int64_t)rg[1];
       range[2] = (int64_t)(uint32_t)rg[2]; range[3] = (int64_t)(rg[2] >> 32);
       range[4] = (int64_t)(rg[3] & 1); range[5] = (int64_t)((rg[3] >> 1) & 1);
@@ -847,7 +852,9 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
         if (nblk >= (uint32_t)kMW || ((uint32_t)w + kMW - i0 % kMW) % kMW < nblk) cmask |= 1u << w;
       // a split panel's share goes to this CTA's workspace tile (slot 0: its first panel, 1: its last)
       float* const obase = full ? prm.C + row0 * N + n0
-                                : prm.ws + ((int64_t)(2 * (int64_t)chunk + (p == pa ? 0 : 1)) * TMV) * (128 * NT);
+                                : prm.ws + ((int64_t)(2 * (int64_t)(prm.nchunks ? share_pos(chunk, prm.nchunks)
+                                                                                : blockIdx.x) +
+                                                         (p == pa ? 0 : 1)) * TMV) * (128 * NT);
       const int64_t ostride = full ? N : 128 * NT;
       const uint32_t slot = pc % L::kSlots;
 #if HRPB_EPI_SLEEP > 0
@@ -952,11 +959,18 @@ __global__ void __launch_bounds__(128) k_spmm_chunks(const uint32_t* __restrict_
   if (blockIdx.x == 0 && threadIdx.x == 0) *ctr = 0u;
   const uint64_t c = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   if (c >= nchunks) return;
-  // guided sizes: the first half of the shares are 3 fine units of a grid of 2 nchunks (3/4 of the work), the
-  // second half 1 unit each, so the shares claimed last (which decide when the launch ends) are 3x smaller
+  // c = position of the share in the matrix (ranges, workspace tiles and the fix-up are indexed by position); it
+  // is claimed as number n - 1 - c: the matrix is walked from its end (#if HRPB_DYN_REV). Guided sizes: the first
+  // half of the claims are 3 fine units of a grid of 2 n (3/4 of the work), the second half 1 unit each, so the
+  // shares claimed last (which decide when the launch ends) are 3x smaller.
   const uint64_t nA = nchunks / 2, F = 3 * nA + (nchunks - nA);
-  auto fine = [&](uint64_t x) { return x <= nA ? 3 * x : 3 * nA + (x - nA); };
-  const CtaWork cw = cta_work_span<PW>(brp, p_lo, p_hi, fine(c), fine(c + 1), F, WarpFind<PW>());
+  auto fine = [&](uint64_t x) { return x <= nA ? 3 * x : 3 * nA + (x - nA); };  // claims -> fine units
+#if HRPB_DYN_REV
+  const uint64_t f0 = F - fine(nchunks - c), f1 = F - fine(nchunks - 1 - c);
+#else
+  const uint64_t f0 = fine(c), f1 = fine(c + 1);
+#endif
+  const CtaWork cw = cta_work_span<PW>(brp, p_lo, p_hi, f0, f1, F, WarpFind<PW>());
   if ((threadIdx.x & 31) == 0) {
     if (cw.bB < cw.bE && !(cw.first_full && cw.last_full)) *split_flag = epoch;
     uint64_t* rg = ranges + 4 * c;
