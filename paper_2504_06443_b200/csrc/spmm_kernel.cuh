@@ -386,7 +386,8 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 
 // GM = gather mode: 0 = TMA tile::gather4 (one issuing lane per producer warp),
 //                   1 = cp.async 16-B copies by all 128 producer threads into the same swizzled layout.
-template <int NT, int GM, int TMV, int TKV>
+// DYN: dynamic S1 shares (a separate instantiation: the share loop costs the static kernel registers and time)
+template <int NT, int GM, int TMV, int TKV, bool DYN = false>
 __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant__ CUtensorMap tmB,
                                                     const __grid_constant__ SpmmParams prm) {
   pdl_wait();
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
   uint32_t chunk = blockIdx.x;
   for (;;) {
   if (warp == 0) {  // S1: contiguous range of ~equal work (blocks + panels) in [p_lo, p_hi); big panels may split
-    if (prm.nchunks == 0) {
+    if (!DYN) {
       const CtaWork cw = cta_work<kPW>(prm.brp, prm.p_lo, prm.p_hi, blockIdx.x, gridDim.x, WarpFind<kPW>());
       if (lane == 0) {
         range[0] = cw.pa; range[1] = cw.pb; range[2] = cw.bB; range[3] = cw.bE;
@@ -852,7 +853,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
         if (nblk >= (uint32_t)kMW || ((uint32_t)w + kMW - i0 % kMW) % kMW < nblk) cmask |= 1u << w;
       // a split panel's share goes to this CTA's workspace tile (slot 0: its first panel, 1: its last)
       float* const obase = full ? prm.C + row0 * N + n0
-                                : prm.ws + ((int64_t)(2 * (int64_t)(prm.nchunks ? share_pos(chunk, prm.nchunks)
+                                : prm.ws + ((int64_t)(2 * (int64_t)(DYN ? share_pos(chunk, prm.nchunks)
                                                                                 : blockIdx.x) +
                                                          (p == pa ? 0 : 1)) * TMV) * (128 * NT);
       const int64_t ostride = full ? N : 128 * NT;
@@ -915,7 +916,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     pc_epi = pc;
   }
   base += cbE - cbB;
-  if (prm.nchunks == 0) break;
+  if (!DYN) break;
   // dynamic S1: every role is done with this share (the epilogue has stored its last panel, so every MMA, gather
   // and decode of it completed); claim the next share in order
   tc_fence_before();
@@ -1057,9 +1058,15 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   // tcgen05.alloc on the TMEM columns the first one holds (TM = 128 at N > 128 allocates all 512)
   const size_t smem = smem_for(stages) > 116 * 1024 ? smem_for(stages) : 116 * 1024;
   if (smem > 227 * 1024) return HRPB_ERROR_NOT_SUPPORTED;  // (not reachable with the instantiated NT / TM / TK)
+  // dynamic S1 instantiated for the long-launch shapes only (cp.async gather, TK = 16, TM <= 32)
+  constexpr bool kDynOk = GM == 1 && TKV == 16 && TMV <= 32;
   static std::atomic<uint64_t> attr_set{0};  // per device: an attribute applies to the current device only
   if (first_on_device(attr_set)) {
-    cudaError_t e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV, TKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV, TKV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e == cudaSuccess && kDynOk)
+      e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV, TKV, kDynOk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               227 * 1024);
     if (e != cudaSuccess) {
       attr_set = 0;
       return cuda_status(e);
@@ -1093,7 +1100,7 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     prm.nsh = scr.sd->nsh;
   }
   prm.cta_t = cta_t;
-  const uint32_t nch = scr.nchunks >= (uint32_t)grid ? scr.nchunks : 0u;  // dynamic S1 (shares >= CTAs)
+  const uint32_t nch = kDynOk && scr.nchunks >= (uint32_t)grid ? scr.nchunks : 0u;  // dynamic S1 (shares >= CTAs)
   if (nch) {
     prm.nchunks = nch;
     prm.chunk_ctr = scr.ctr;
@@ -1101,7 +1108,8 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
                scr.flag, scr.epoch, scr.ctr);
     note_launch();
   }
-  launch_pdl(k_spmm<NT, GM, TMV, TKV>, grid, kSpmmThreads, smem, s, tm, prm);
+  if (nch) launch_pdl(k_spmm<NT, GM, TMV, TKV, kDynOk>, grid, kSpmmThreads, smem, s, tm, prm);
+  else launch_pdl(k_spmm<NT, GM, TMV, TKV, false>, grid, kSpmmThreads, smem, s, tm, prm);
   if (cta_t) {  // (blocks the stream: diagnostics only)
     std::vector<long long> host(4 * (size_t)grid);
     cudaMemcpyAsync(host.data(), cta_t, host.size() * sizeof(long long), cudaMemcpyDeviceToHost, s);
