@@ -106,8 +106,9 @@ hrpb_status_t spmm_core(const hrpb_handle* h, const float* B, int64_t ldb, float
   const int64_t ncols_max = N < 512 ? N : 512;
   // (HRPB_STATIC_S1 / HRPB_DYN_S1: force either, for experiments and the parity tests of small matrices)
   const int64_t shares = min((int64_t)kDynShares * num_sms(), p_hi - p_lo);
+  // (whole-matrix launches only: the chunked launches of the pipelined host path are short)
   const bool dyn = getenv("HRPB_STATIC_S1") == nullptr && h->tm <= 32 && shares >= num_sms() &&
-                   (h->nnz >= kDynMinNnz || getenv("HRPB_DYN_S1") != nullptr);
+                   ((h->nnz >= kDynMinNnz && p_lo == 0 && p_hi == h->P) || getenv("HRPB_DYN_S1") != nullptr);
   const uint32_t nchunks = dyn ? (uint32_t)shares : 0u;
   // shares x 2 tiles x TM x (128 NT) partial tiles (static: TM * 128 NT <= 64 * 512 for every instantiated pair),
   // the split flag, the claim counter and the shares' S1 ranges

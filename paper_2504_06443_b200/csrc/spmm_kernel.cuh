@@ -201,6 +201,7 @@ constexpr uint64_t kPanelW = HRPB_PANEL_W;
 #define HRPB_DYN_SHARES 16
 #endif
 constexpr int kDynShares = HRPB_DYN_SHARES;
+constexpr int kFixThreads = 512;  // k_spmm_fixup threads (one CTA per share boundary)
 #ifndef HRPB_DYN_REV
 #define HRPB_DYN_REV 1
 #endif
@@ -987,53 +988,68 @@ __global__ void __launch_bounds__(128) k_spmm_chunks(const uint32_t* __restrict_
 // the partial tiles of every CTA holding blocks of q, in CTA order (deterministic), and writes q's rows of C. The
 // contributing CTAs are listed once per CTA in shared memory (no per-element work search).
 template <int TMV>
-__global__ void __launch_bounds__(128) k_spmm_fixup(const uint32_t* __restrict__ brp, const uint64_t* __restrict__ ranges,
-                                                    const float* __restrict__ ws, float* __restrict__ C, int64_t M,
-                                                    int64_t N, int n0, int wcols, const uint64_t* split_flag,
-                                                    uint64_t epoch) {
+__global__ void __launch_bounds__(kFixThreads) k_spmm_fixup(const uint32_t* __restrict__ brp,
+                                                          const uint64_t* __restrict__ ranges,
+                                                          const float* __restrict__ ws, float* __restrict__ C,
+                                                          int64_t M, int64_t N, int n0, int wcols,
+                                                          const uint64_t* split_flag, uint64_t epoch) {
   pdl_wait();
   constexpr int kMaxSrc = 256;
-  __shared__ int s_src[kMaxSrc];  // (cc << 1) | workspace slot of each contributing CTA
+  __shared__ int s_src[kMaxSrc];  // (cc << 1) | workspace slot of each contributing share, one batch
   __shared__ int s_n;
+  __shared__ uint64_t s_next;     // share to continue the contributor scan from (next batch)
   __shared__ int64_t s_q;
   const uint64_t G = gridDim.x, c = blockIdx.x;
   if (c == 0 || *split_flag != epoch) return;  // no split panel in this launch
   if (threadIdx.x == 0) {
     s_n = 0;
+    s_next = G;
     const uint64_t* A = ranges + 4 * (c - 1);
     const int64_t pa = (int64_t)A[0], pb = (int64_t)A[1];
     const uint32_t bB = (uint32_t)A[2], bE = (uint32_t)(A[2] >> 32);
     const bool ff = A[3] & 1, lf = (A[3] >> 1) & 1;
     const int64_t q = pb - 1;
     s_q = q;
-    if (bB < bE && !lf && (pa != q || ff)) {  // boundary c is the first one strictly inside panel q
-      const uint32_t q0 = brp[q], q1 = brp[q + 1];
-      for (uint64_t cc = c - 1; cc < G && s_n < kMaxSrc; ++cc) {
-        const uint64_t* W = ranges + 4 * cc;
-        const int64_t wpa = (int64_t)W[0];
-        if (wpa > q) break;
-        const uint32_t b0 = max(q0, (uint32_t)W[2]), b1 = min(q1, (uint32_t)(W[2] >> 32));
-        if (b0 >= b1) continue;  // no blocks of q in CTA cc
-        s_src[s_n++] = (int)(cc << 1) | (q == wpa ? 0 : 1);
-      }
-    }
+    if (bB < bE && !lf && (pa != q || ff)) s_next = c - 1;  // boundary c is the first one strictly inside panel q
   }
   __syncthreads();
-  const int n = s_n;
-  if (n == 0) return;
+  if (s_next >= G) return;
   const int64_t q = s_q;
   const int64_t row0 = q * TMV;
   const int nrows = (int)min((int64_t)TMV, M - row0);
   const int ncols = (int)min((int64_t)wcols, N - n0);
-  for (int r = 0; r < nrows; ++r)
-    for (int col = threadIdx.x; col < ncols; col += blockDim.x) {
-      float acc = 0.f;
+  const uint32_t q0 = brp[q], q1 = brp[q + 1];
+  // contributors in share order, in batches of kMaxSrc (a panel may span more shares than one batch holds): the
+  // first batch writes C, later ones add to it — the same order of additions as one pass (deterministic)
+  for (int batch = 0;; ++batch) {
+    if (threadIdx.x == 0) {
+      int n = 0;
+      uint64_t cc = s_next;
+      for (; cc < G && n < kMaxSrc; ++cc) {
+        const uint64_t* W = ranges + 4 * cc;
+        const int64_t wpa = (int64_t)W[0];
+        if (wpa > q) { cc = G; break; }
+        const uint32_t b0 = max(q0, (uint32_t)W[2]), b1 = min(q1, (uint32_t)(W[2] >> 32));
+        if (b0 >= b1) continue;  // no blocks of q in share cc
+        s_src[n++] = (int)(cc << 1) | (q == wpa ? 0 : 1);
+      }
+      s_n = n;
+      s_next = cc;
+    }
+    __syncthreads();
+    const int n = s_n;
+    for (int e = threadIdx.x; e < nrows * ncols; e += kFixThreads) {
+      const int r = e / ncols, col = e - r * ncols;
+      float acc = batch == 0 ? 0.f : C[(row0 + r) * N + n0 + col];
       for (int k = 0; k < n; ++k) {
         const int src = s_src[k];
         acc += ws[((int64_t)(2 * (src >> 1) + (src & 1)) * TMV + r) * wcols + col];
       }
       C[(row0 + r) * N + n0 + col] = acc;
     }
+    __syncthreads();
+    if (s_next >= G) break;
+  }
 }
 
 template <int NT, int GM, int TMV, int TKV>
@@ -1120,7 +1136,7 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     }
     dfree(cta_t, s);
   }
-  launch_pdl(k_spmm_fixup<TMV>, nch ? (int)nch : grid, 128, 0, s, h->brp, (const uint64_t*)scr.ranges, scr.ws, C,
+  launch_pdl(k_spmm_fixup<TMV>, nch ? (int)nch : grid, kFixThreads, 0, s, h->brp, (const uint64_t*)scr.ranges, scr.ws, C,
              h->M, N, n0, 128 * NT, scr.flag, scr.epoch);
   note_launch(2);
   if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)

@@ -622,3 +622,21 @@ def test_spmm_dynamic_s1_split_hubs(dyn_s1):
     A = gpu_build(M, K, rp, ci, v)
     C = hp.spmm(A, dev(B)).cpu().numpy()
     check_exact(C, oracle.csr_spmm(M, K, rp, ci, v, B), "dynamic split hubs")
+
+
+def test_spmm_dynamic_s1_hub_over_many_shares(dyn_s1):
+    """One hub panel spread over more than 256 shares (the fix-up reduces its partial tiles in batches)."""
+    rng = np.random.default_rng(21)
+    M, K, N = 16 * 2400, 40000, 64
+    rp, ci, v = rand_csr(M, K, 0.00005, 3)
+    dense = np.zeros((M, K), bool)
+    for i in range(M):
+        dense[i, ci[rp[i]:rp[i + 1]]] = True
+    dense[16 * 1200:16 * 1200 + 4, :] = rng.random((4, K)) < 0.9  # ~2300 blocks in one panel
+    rp = np.zeros(M + 1, np.int64); rp[1:] = np.cumsum(dense.sum(1))
+    ci = np.nonzero(dense)[1].astype(np.int32)
+    v = rng.choice(np.array([-2, -1, 1, 2], np.float32), size=ci.size).astype(np.float32)
+    B = rng.choice(np.array([-1, 1, 2], np.float32), size=(K, N)).astype(np.float32)
+    A = gpu_build(M, K, rp, ci, v)
+    C = hp.spmm(A, dev(B)).cpu().numpy()
+    check_exact(C, oracle.csr_spmm(M, K, rp, ci, v, B), "hub over > 256 shares")
