@@ -124,6 +124,32 @@ hrpb_status_t hrpb_spmm_sharded(const hrpb_t A, const float* const* shards, int3
                                 float* C, int64_t M, int64_t K, int64_t N, hrpb_stream_t stream);
 
 /*
+ * hrpb_reorder_rows — NEXT-4 (the paper's "Matrix Reordering"): a row permutation that puts
+ * rows with overlapping column sets into the same TM-row panel (fewer distinct columns per panel, fewer blocks,
+ * denser bricks), computed on the GPU, and the row-permuted CSR. Key of row i, sorted ascending and stably:
+ * (31 - floor(log2(max(deg_i, 1)))) << 40 | min over the row's columns c of ((c * 0x9E3779B97F4A7C15) mod 2^64) >> 40
+ * (degree buckets largest first, then the min-hash of the column set; empty rows: min-hash 2^24 - 1).
+ *   M, K, nnz, row_ptr, col_idx, values : the input CSR (device, as for hrpb_build; assumed valid — row pointers are
+ *                                         clamped into [0, nnz] so an invalid one cannot read out of bounds).
+ *   perm        : device int32 [M], out: row i of the output is row perm[i] of the input.
+ *   row_ptr_out : device int64 [M + 1], col_idx_out : device int32 [nnz], values_out : device float [nnz], out: the
+ *                 permuted CSR (entries of each row in their original order). Caller-owned, not aliasing the input.
+ * Build the HRPB from the permuted CSR, then hrpb_set_row_map(A, perm): hrpb_spmm then writes C in the ORIGINAL
+ * row order. Synchronizes nothing (async on `stream`).
+ * Errors: INVALID_VALUE, OUT_OF_MEMORY, CUDA.
+ */
+hrpb_status_t hrpb_reorder_rows(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                                const float* values, int32_t* perm, int64_t* row_ptr_out, int32_t* col_idx_out,
+                                float* values_out, hrpb_stream_t stream);
+
+/*
+ * hrpb_set_row_map — declares that A was built from row-permuted rows: hrpb_spmm / hrpb_spmm_sharded write A's row i
+ * into C row row_map[i] (device int32 [M], a permutation of 0..M-1, caller-owned, valid while the handle is used;
+ * NULL restores the identity). Errors: INVALID_VALUE (A NULL).
+ */
+hrpb_status_t hrpb_set_row_map(hrpb_t A, const int32_t* row_map);
+
+/*
  * hrpb_build_spmm — the whole hot path on device buffers in one call: hrpb_build then hrpb_spmm, enqueued
  * back to back on `stream` (the SpMM does not wait for the build's size read-back), one synchronization at the
  * end. Arguments as for hrpb_build / hrpb_spmm (all DEVICE pointers).

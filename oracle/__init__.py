@@ -55,6 +55,7 @@ def _L():
         lib.oracle_hrpb_check.argtypes = [i64, i64, i64, i64, i64, vp, vp, vp, vp, C.c_char_p, C.c_int]
         lib.oracle_hrpb_check.restype = C.c_int
         lib.oracle_hrpb_spmm_f64.argtypes = [i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp]
+        lib.oracle_reorder_rows.argtypes = [i64, vp, vp, vp]
         lib.oracle_num_threads.restype = C.c_int
         _lib = lib
     return _lib
@@ -177,6 +178,15 @@ def hrpb_spmm(h: Hrpb, B):
     _L().oracle_hrpb_spmm_f64(h.M, h.K, N, h.tm, h.tk, _p(h.blockedRowPtr), _p(ac), _p(h.sizePtr),
                               _p(packed), _p(Bc), _p(Cm))
     return Cm
+
+
+def reorder_rows(M, row_ptr, col_idx):
+    """O8: the NEXT-4 row permutation (degree buckets descending, then the column-set min-hash; stable)."""
+    rp, ci = _c(row_ptr, np.int64), _c(col_idx, np.int32)
+    perm = np.zeros(max(M, 1), np.int32)
+    if _L().oracle_reorder_rows(M, _p(rp), _p(ci), _p(perm)) != 0:
+        raise MemoryError("oracle_reorder_rows")
+    return perm[:M]
 
 
 def num_threads():

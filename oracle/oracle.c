@@ -454,6 +454,40 @@ void oracle_hrpb_spmm_f64(int64_t M, int64_t K, int64_t N, int64_t tm, int64_t t
   }
 }
 
+/* ---------------------------------------------------------------- O8: row reordering (NEXT-4) */
+/* The row permutation of the reordering preprocessing (the paper names matrix reordering as
+ * ongoing work, without an algorithm: reading R25 in DESIGN.md). Key of row i:
+ *   ((31 - floor(log2(max(deg_i, 1)))) << 40) | min over the row's columns c of h(c),
+ *   h(c) = (c * 0x9E3779B97F4A7C15 mod 2^64) >> 40 (24 bits; an empty row: 2^24 - 1),
+ * rows sorted by ascending key, ties by ascending row id (a stable sort). perm[i] = the row placed at i. */
+typedef struct { uint64_t key; int32_t row; } reo_t;
+static int cmp_reo(const void* a, const void* b) {
+  const reo_t* x = (const reo_t*)a;
+  const reo_t* y = (const reo_t*)b;
+  if (x->key != y->key) return x->key < y->key ? -1 : 1;
+  return x->row < y->row ? -1 : (x->row > y->row);
+}
+int oracle_reorder_rows(int64_t M, const int64_t* rp, const int32_t* ci, int32_t* perm) {
+  reo_t* r = (reo_t*)malloc((size_t)(M > 0 ? M : 1) * sizeof(reo_t));
+  if (!r) return 1;
+  for (int64_t i = 0; i < M; ++i) {
+    const int64_t deg = rp[i + 1] - rp[i];
+    uint64_t lg = 0;
+    while (lg < 31 && (2ll << lg) <= deg) ++lg; /* floor(log2(deg)) for deg >= 1, 0 for deg <= 1 */
+    uint64_t mh = 0xFFFFFFull;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const uint64_t h = ((uint64_t)(uint32_t)ci[k] * 0x9E3779B97F4A7C15ull) >> 40;
+      if (h < mh) mh = h;
+    }
+    r[i].key = ((31 - lg) << 40) | mh;
+    r[i].row = (int32_t)i;
+  }
+  qsort(r, (size_t)M, sizeof(reo_t), cmp_reo);
+  for (int64_t i = 0; i < M; ++i) perm[i] = r[i].row;
+  free(r);
+  return 0;
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

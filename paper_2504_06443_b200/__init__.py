@@ -5,5 +5,5 @@ GPU CSR->HRPB builder kernels and a tcgen05/TMA SpMM kernel. This package is a t
 binding (argument marshalling only); torch supplies device memory, streams and process groups.
 There is no CPU fallback: if the extension is missing or the device is not sm_100, calls raise.
 """
-from .hrpb import (Hrpb, HrpbError, build, spmm, spmm_sharded, build_spmm, build_spmm_async, sync_status, build_spmm_host, launch_count, lib_path,  # noqa: F401
+from .hrpb import (Hrpb, HrpbError, build, spmm, spmm_sharded, reorder_rows, build_spmm, build_spmm_async, sync_status, build_spmm_host, launch_count, lib_path,  # noqa: F401
                    EXPORTED_SYMBOLS)

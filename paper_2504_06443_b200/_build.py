@@ -12,7 +12,7 @@ import tempfile
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libhrpb.so")
 SOURCES = ["csrc/api.cu", "csrc/build.cu", "csrc/spmm.cu", "csrc/spmm_tk16.cu", "csrc/spmm_tk32.cu",
-           "csrc/spmm_sharded.cu"]
+           "csrc/spmm_sharded.cu", "csrc/reorder.cu"]
 DEPS = SOURCES + ["csrc/common.cuh", "csrc/internal.h", "csrc/spmm_kernel.cuh", "../include/hrpb.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -368,6 +368,24 @@ hrpb_status_t hrpb_spmm_sharded(const hrpb_t A, const float* const* shards, int3
   return st;
 }
 
+hrpb_status_t hrpb_reorder_rows(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                                const float* values, int32_t* perm, int64_t* row_ptr_out, int32_t* col_idx_out,
+                                float* values_out, hrpb_stream_t stream) {
+  if (M < 0 || K < 0 || nnz < 0 || M >= (1ll << 31) || nnz >= (1ll << 31) || !row_ptr || !row_ptr_out ||
+      (M > 0 && !perm) || (nnz > 0 && (!col_idx || !values || !col_idx_out || !values_out)))
+    return HRPB_ERROR_INVALID_VALUE;
+  hrpb_status_t st = check_device();
+  if (st != HRPB_SUCCESS) return st;
+  return reorder_impl(M, K, nnz, row_ptr, col_idx, values, perm, row_ptr_out, col_idx_out, values_out,
+                      (cudaStream_t)stream);
+}
+
+hrpb_status_t hrpb_set_row_map(hrpb_t A, const int32_t* row_map) {
+  if (!A) return HRPB_ERROR_INVALID_VALUE;
+  A->row_map = row_map;
+  return HRPB_SUCCESS;
+}
+
 hrpb_status_t hrpb_build_spmm_host(int64_t M, int64_t K, int64_t N, int64_t nnz, const int64_t* row_ptr_h,
                                    const int32_t* col_idx_h, const float* values_h, const float* B_h, float* C_h,
                                    const hrpb_config_t* cfg, hrpb_stream_t stream) {

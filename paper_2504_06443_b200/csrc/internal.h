@@ -23,6 +23,9 @@ struct hrpb_handle {
   bool use_overflow;
   cudaStream_t use_st[kMaxUse];
   cudaEvent_t use_ev[kMaxUse];
+  // NEXT-4: the handle was built from a row-permuted CSR (hrpb_reorder_rows); the SpMM writes its row i to C row
+  // row_map[i] (caller-owned device int32 [M]), so C = A.B in the original row order. NULL = identity.
+  const int32_t* row_map;
 };
 
 namespace hrpb {
@@ -62,6 +65,10 @@ hrpb_status_t spmm_range_impl(const hrpb_handle* h, const float* B, int64_t ldb,
 hrpb_status_t chunk_maxcol(const hrpb_handle* h, int64_t per, int nchunks, int* dev_out, cudaStream_t s);
 
 int num_sms();
+// NEXT-4: row permutation (degree buckets descending, then min-hash of the column set) and the permuted CSR
+hrpb_status_t reorder_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                           const float* values, int32_t* perm, int64_t* row_ptr_out, int32_t* col_idx_out,
+                           float* values_out, cudaStream_t s);
 
 // per-device one-time initialisation (kernel attributes, pools): true the first time it is called for the current
 // device with this flag word (always true on device ids >= 64)

@@ -78,7 +78,8 @@ hrpb_status_t spmm_sharded_impl(const hrpb_handle* h, const float* const* shards
 hrpb_status_t spmm_core(const hrpb_handle* h, const float* B, int64_t ldb, float* C, int64_t N, int64_t p_lo,
                         int64_t p_hi, const ShardDesc* sd, cudaStream_t s) {
   if (N == 0 || h->M == 0 || p_hi <= p_lo) return HRPB_SUCCESS;
-  if (h->NB == 0) {  // A has no entries: C = 0 (rows of the range; NB < 0 = not known yet: the kernel copes)
+  if (h->NB == 0 && !h->row_map) {  // A has no entries: C = 0 (rows of the range; NB < 0 = not known yet: the kernel
+    // copes; so does it with a row map, whose rows are not contiguous)
     const int64_t r0 = p_lo * h->tm, r1 = p_hi * h->tm < h->M ? p_hi * h->tm : h->M;
     cudaError_t e = cudaMemsetAsync(C + r0 * N, 0, (size_t)(r1 - r0) * N * sizeof(float), s);
     return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);

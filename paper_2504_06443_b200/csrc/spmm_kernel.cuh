@@ -100,6 +100,7 @@ struct SpmmParams {
   uint32_t nchunks;     // 0: static S1 (CTA c takes share c of G); else dynamic: nchunks shares (ranges precomputed by
                         // k_spmm_chunks), CTA c starts with share c and then claims shares G, G + 1, ... in order
   uint32_t* chunk_ctr;  // claim counter (zeroed by k_spmm_chunks)
+  const int32_t* row_map;  // NEXT-4: C row of each A row (hrpb_set_row_map), NULL = identity
   long long* cta_t;  // optional (HRPB_CTA_TIMES): per CTA {globaltimer at entry, at exit, blocks, panels}
   int debug;         // HRPB_DEBUG bits (experiments only): 1 = skip C stores, 2 = skip decode, 4 = skip MMA issue,
                      // 8 = skip A bulk copy, 16 = B gather zero-fill only (no global reads), 32 = no B cp.async at all
@@ -838,8 +839,10 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       const int64_t row0 = p * TMV;
       const int nrows = (int)min((int64_t)TMV, M - row0);
       if (bb == be) {  // empty panel (always owned whole): zero rows (R13)
-        for (int r = 0; r < nrows; ++r)
-          for (int64_t c = et; c < ncols; c += 128) prm.C[(row0 + r) * N + n0 + c] = 0.f;
+        for (int r = 0; r < nrows; ++r) {
+          const int64_t cr = prm.row_map ? (int64_t)prm.row_map[row0 + r] : row0 + r;
+          for (int64_t c = et; c < ncols; c += 128) prm.C[cr * N + n0 + c] = 0.f;
+        }
         continue;
       }
       const bool full = (p != pa || first_full) && (p != pb - 1 || last_full);
@@ -898,7 +901,12 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
           const int64_t c = 128 * t + 32 * qd + lane;
           if (c < ncols && !(dbg(prm, 1))) {
             float* dst = obase + c + (int64_t)h0 * ostride;
-            if (nrows == TMV) {
+            if (full && prm.row_map) {  // reordered rows (NEXT-4): each row to its original C row
+#pragma unroll
+              for (int r = 0; r < kRows; ++r)
+                if (h0 + r < nrows)
+                  __stcs(prm.C + (int64_t)prm.row_map[row0 + h0 + r] * N + n0 + c, a[r]);
+            } else if (nrows == TMV) {
 #pragma unroll
               for (int r = 0; r < kRows; ++r) __stcs(dst + (int64_t)r * ostride, a[r]);
             } else {
@@ -992,7 +1000,8 @@ __global__ void __launch_bounds__(kFixThreads) k_spmm_fixup(const uint32_t* __re
                                                           const uint64_t* __restrict__ ranges,
                                                           const float* __restrict__ ws, float* __restrict__ C,
                                                           int64_t M, int64_t N, int n0, int wcols,
-                                                          const uint64_t* split_flag, uint64_t epoch) {
+                                                          const uint64_t* split_flag, uint64_t epoch,
+                                                          const int32_t* __restrict__ row_map) {
   pdl_wait();
   constexpr int kMaxSrc = 256;
   __shared__ int s_src[kMaxSrc];  // (cc << 1) | workspace slot of each contributing share, one batch
@@ -1040,12 +1049,13 @@ __global__ void __launch_bounds__(kFixThreads) k_spmm_fixup(const uint32_t* __re
     const int n = s_n;
     for (int e = threadIdx.x; e < nrows * ncols; e += kFixThreads) {
       const int r = e / ncols, col = e - r * ncols;
-      float acc = batch == 0 ? 0.f : C[(row0 + r) * N + n0 + col];
+      const int64_t cr = row_map ? (int64_t)row_map[row0 + r] : row0 + r;
+      float acc = batch == 0 ? 0.f : C[cr * N + n0 + col];
       for (int k = 0; k < n; ++k) {
         const int src = s_src[k];
         acc += ws[((int64_t)(2 * (src >> 1) + (src & 1)) * TMV + r) * wcols + col];
       }
-      C[(row0 + r) * N + n0 + col] = acc;
+      C[cr * N + n0 + col] = acc;
     }
     __syncthreads();
     if (s_next >= G) break;
@@ -1107,7 +1117,8 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     cudaMemsetAsync(cta_t, 0, 4 * (size_t)grid * sizeof(long long), s);
   }
   SpmmParams prm{h->brp, h->ac, h->sp, h->packed, C, h->M, N, h->P, h->NB, p_lo, p_hi, scr.ws, scr.flag, scr.epoch,
-                 scr.ranges, B, h->K, ldb, n0, stages, trace, {}, 0u, 0.f, 0, 0u, nullptr, nullptr, debug};
+                 scr.ranges, B, h->K, ldb, n0, stages, trace, {}, 0u, 0.f, 0, 0u, nullptr, h->row_map, nullptr,
+                 debug};
   if (GM == 2) {
     if (!scr.sd) return HRPB_ERROR_INVALID_VALUE;
     for (int r = 0; r < scr.sd->nsh; ++r) prm.sh_ptr[r] = scr.sd->ptr[r];
@@ -1137,7 +1148,7 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     dfree(cta_t, s);
   }
   launch_pdl(k_spmm_fixup<TMV>, nch ? (int)nch : grid, kFixThreads, 0, s, h->brp, (const uint64_t*)scr.ranges, scr.ws, C,
-             h->M, N, n0, 128 * NT, scr.flag, scr.epoch);
+             h->M, N, n0, 128 * NT, scr.flag, scr.epoch, h->row_map);
   note_launch(2);
   if (trace) {  // debugging aid: dump CTA 0's per-block timestamps (blocks the stream)
     static long long host[kTraceSlots * kTraceN];

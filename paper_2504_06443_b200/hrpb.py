@@ -59,6 +59,8 @@ def lib():
         L.hrpb_build.argtypes = [i64, i64, i64, vp, vp, vp, C.POINTER(_Config), vp, C.POINTER(vp)]
         L.hrpb_spmm.argtypes = [vp, vp, vp, i64, i64, i64, vp]
         L.hrpb_spmm_sharded.argtypes = [vp, C.POINTER(vp), C.c_int32, i64, vp, i64, i64, i64, vp]
+        L.hrpb_reorder_rows.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.hrpb_set_row_map.argtypes = [vp, vp]
         L.hrpb_build_spmm_host.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Config), vp]
         L.hrpb_build_spmm.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Config), vp,
                                       C.POINTER(vp), C.POINTER(C.c_float)]
@@ -71,7 +73,7 @@ def lib():
         L.hrpb_get_error_string.restype = C.c_char_p
         L.hrpb_last_cuda_error.restype = C.c_int
         L.hrpb_launch_count.restype = C.c_int64
-        for f in ("hrpb_build", "hrpb_spmm", "hrpb_spmm_sharded", "hrpb_build_spmm", "hrpb_build_spmm_async", "hrpb_sync_status",
+        for f in ("hrpb_build", "hrpb_spmm", "hrpb_spmm_sharded", "hrpb_reorder_rows", "hrpb_set_row_map", "hrpb_build_spmm", "hrpb_build_spmm_async", "hrpb_sync_status",
                   "hrpb_build_spmm_host", "hrpb_free", "hrpb_get_view", "hrpb_copy_view_to_host"):
             getattr(L, f).restype = C.c_int
         _lib = L
@@ -170,6 +172,16 @@ class Hrpb:
                                             packed.ctypes.data), "hrpb_copy_view_to_host")
         return brp, ac[: self.num_blocks * self.tk], sp, packed[: self.packed_bytes]
 
+    def set_row_map(self, row_map):
+        """hrpb_set_row_map (NEXT-4): this handle was built from reordered rows; SpMM writes A row i to C row
+        row_map[i] (CUDA int32 tensor [M], kept alive by the handle). None restores the identity."""
+        import torch
+        ptr = None
+        if row_map is not None:
+            ptr = _dev(row_map, torch.int32, "row_map", self.M)
+        self._row_map = row_map  # (owned by the caller in C; the binding keeps it alive with the handle)
+        _check(lib().hrpb_set_row_map(self._h, ptr), "hrpb_set_row_map")
+
     def free(self):
         if self._h:
             lib().hrpb_free(self._h)
@@ -233,6 +245,22 @@ def spmm_sharded(A: Hrpb, shards, rows_per_shard: int, out=None, stream=None):
                                  _stream(stream))
     _check(st, "hrpb_spmm_sharded")
     return out
+
+
+def reorder_rows(row_ptr, col_idx, values, M: int, K: int, stream=None):
+    """hrpb_reorder_rows (NEXT-4): returns (perm, row_ptr_out, col_idx_out, values_out) as CUDA tensors — row i of the
+    permuted CSR is input row perm[i]. Build from the permuted CSR, then A.set_row_map(perm)."""
+    import torch
+    rp, ci, va, nnz = _csr_dev(row_ptr, col_idx, values, M)
+    dev = row_ptr.device
+    perm = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+    rp2 = torch.empty(M + 1, dtype=torch.int64, device=dev)
+    ci2 = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    v2 = torch.empty(max(nnz, 1), dtype=torch.float32, device=dev)
+    st = lib().hrpb_reorder_rows(M, K, nnz, rp, ci, va, C.c_void_p(perm.data_ptr()), C.c_void_p(rp2.data_ptr()),
+                                 C.c_void_p(ci2.data_ptr()), C.c_void_p(v2.data_ptr()), _stream(stream))
+    _check(st, "hrpb_reorder_rows")
+    return perm[:M], rp2, ci2[:nnz], v2[:nnz]
 
 
 def build_spmm(row_ptr, col_idx, values, B, M: int, K: int, out=None, tm: int = 16, tk: int = 16, stream=None,

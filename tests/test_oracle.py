@@ -387,3 +387,37 @@ def test_emulator_equals_csr_exact(tm):
     B = w.B()
     h = oracle.csr_to_hrpb(w.M, w.K, w.row_ptr, w.col_idx, w.vals, tm=tm)
     assert np.array_equal(oracle.hrpb_spmm(h, B), oracle.csr_spmm(w.M, w.K, w.row_ptr, w.col_idx, w.vals, B))
+
+
+# --------------------------------------------------------------------------- O8: NEXT-4 row reordering
+def test_o8_reorder_hand_example():
+    """DESIGN.md R25 key, worked by hand: degrees 2 / 0 / 5 / 1 -> log2 buckets 1 / 0 / 2 / 0, so row 2 (bucket 2)
+    comes first, then row 0 (bucket 1); rows 1 and 3 share bucket 0 and row 3 (one column: a 24-bit hash) sorts
+    before the empty row 1 (min-hash 2^24 - 1)."""
+    rp = np.array([0, 2, 2, 7, 8], np.int64)
+    ci = np.array([3, 9, 0, 1, 2, 3, 4, 5], np.int32)
+    assert oracle.reorder_rows(4, rp, ci).tolist() == [2, 0, 3, 1]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_o8_reorder_invariants(seed):
+    """A permutation; degree buckets floor(log2(max(deg, 1))) never increase along it; rows with identical column
+    sets in the same bucket keep their relative (row id) order."""
+    rng = np.random.default_rng(seed)
+    M, K = 300, 500
+    rp, ci, _ = rand_csr(M, K, float(rng.choice([0.002, 0.02, 0.1])), seed)
+    # duplicate some rows' column sets (identical keys)
+    perm = oracle.reorder_rows(M, rp, ci)
+    assert sorted(perm.tolist()) == list(range(M))
+    deg = np.diff(rp)[perm]
+    bucket = np.floor(np.log2(np.maximum(deg, 1))).astype(int)
+    assert np.all(np.diff(bucket) <= 0)
+    sets = {}
+    for pos, r in enumerate(perm):
+        sets.setdefault(tuple(ci[rp[r]:rp[r + 1]].tolist()), []).append(r)
+    for rows in sets.values():
+        assert rows == sorted(rows)
+
+
+def test_o8_reorder_empty():
+    assert oracle.reorder_rows(0, np.zeros(1, np.int64), np.zeros(0, np.int32)).size == 0
