@@ -145,7 +145,8 @@ hrpb_status_t hrpb_reorder_rows(int64_t M, int64_t K, int64_t nnz, const int64_t
 /*
  * hrpb_set_row_map — declares that A was built from row-permuted rows: hrpb_spmm / hrpb_spmm_sharded write A's row i
  * into C row row_map[i] (device int32 [M], a permutation of 0..M-1, caller-owned, valid while the handle is used;
- * NULL restores the identity). Errors: INVALID_VALUE (A NULL).
+ * NULL restores the identity). Supported with TK = 16 and the default cp.async gather (hrpb_spmm); other
+ * configurations and hrpb_spmm_sharded then return NOT_SUPPORTED. Errors: INVALID_VALUE (A NULL).
  */
 hrpb_status_t hrpb_set_row_map(hrpb_t A, const int32_t* row_map);
 

@@ -388,8 +388,9 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 
 // GM = gather mode: 0 = TMA tile::gather4 (one issuing lane per producer warp),
 //                   1 = cp.async 16-B copies by all 128 producer threads into the same swizzled layout.
-// DYN: dynamic S1 shares (a separate instantiation: the share loop costs the static kernel registers and time)
-template <int NT, int GM, int TMV, int TKV, bool DYN = false>
+// DYN: dynamic S1 shares (a separate instantiation: the share loop costs the static kernel registers and time);
+// RMAP: C rows through the handle's row map (NEXT-4; separate for the same reason: c2b 0.172 -> 0.207 ms)
+template <int NT, int GM, int TMV, int TKV, bool DYN = false, bool RMAP = false>
 __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant__ CUtensorMap tmB,
                                                     const __grid_constant__ SpmmParams prm) {
   pdl_wait();
@@ -840,7 +841,7 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
       const int nrows = (int)min((int64_t)TMV, M - row0);
       if (bb == be) {  // empty panel (always owned whole): zero rows (R13)
         for (int r = 0; r < nrows; ++r) {
-          const int64_t cr = prm.row_map ? (int64_t)prm.row_map[row0 + r] : row0 + r;
+          const int64_t cr = RMAP ? (int64_t)prm.row_map[row0 + r] : row0 + r;
           for (int64_t c = et; c < ncols; c += 128) prm.C[cr * N + n0 + c] = 0.f;
         }
         continue;
@@ -901,11 +902,10 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
           const int64_t c = 128 * t + 32 * qd + lane;
           if (c < ncols && !(dbg(prm, 1))) {
             float* dst = obase + c + (int64_t)h0 * ostride;
-            if (full && prm.row_map) {  // reordered rows (NEXT-4): each row to its original C row
+            if (RMAP && full) {  // reordered rows (NEXT-4): each row to its original C row
 #pragma unroll
               for (int r = 0; r < kRows; ++r)
-                if (h0 + r < nrows)
-                  __stcs(prm.C + (int64_t)prm.row_map[row0 + h0 + r] * N + n0 + c, a[r]);
+                if (h0 + r < nrows) __stcs(prm.C + (int64_t)prm.row_map[row0 + h0 + r] * N + n0 + c, a[r]);
             } else if (nrows == TMV) {
 #pragma unroll
               for (int r = 0; r < kRows; ++r) __stcs(dst + (int64_t)r * ostride, a[r]);
@@ -1084,8 +1084,11 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
   // tcgen05.alloc on the TMEM columns the first one holds (TM = 128 at N > 128 allocates all 512)
   const size_t smem = smem_for(stages) > 116 * 1024 ? smem_for(stages) : 116 * 1024;
   if (smem > 227 * 1024) return HRPB_ERROR_NOT_SUPPORTED;  // (not reachable with the instantiated NT / TM / TK)
-  // dynamic S1 instantiated for the long-launch shapes only (cp.async gather, TK = 16, TM <= 32)
+  // dynamic S1 instantiated for the long-launch shapes only (cp.async gather, TK = 16, TM <= 32); row-mapped C
+  // (NEXT-4) for the cp.async gather with TK = 16
   constexpr bool kDynOk = GM == 1 && TKV == 16 && TMV <= 32;
+  constexpr bool kRmapOk = GM == 1 && TKV == 16;
+  if (h->row_map && !kRmapOk) return HRPB_ERROR_NOT_SUPPORTED;
   static std::atomic<uint64_t> attr_set{0};  // per device: an attribute applies to the current device only
   if (first_on_device(attr_set)) {
     cudaError_t e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV, TKV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1093,6 +1096,12 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
     if (e == cudaSuccess && kDynOk)
       e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV, TKV, kDynOk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                227 * 1024);
+    if (e == cudaSuccess && kRmapOk)
+      e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV, TKV, false, kRmapOk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               227 * 1024);
+    if (e == cudaSuccess && kDynOk && kRmapOk)
+      e = cudaFuncSetAttribute(k_spmm<NT, GM, TMV, TKV, kDynOk, kRmapOk>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) {
       attr_set = 0;
       return cuda_status(e);
@@ -1135,7 +1144,10 @@ static hrpb_status_t launch_nt(const hrpb_handle* h, const CUtensorMap& tm, cons
                scr.flag, scr.epoch, scr.ctr);
     note_launch();
   }
-  if (nch) launch_pdl(k_spmm<NT, GM, TMV, TKV, kDynOk>, grid, kSpmmThreads, smem, s, tm, prm);
+  const bool rmap = h->row_map != nullptr;
+  if (nch && rmap) launch_pdl(k_spmm<NT, GM, TMV, TKV, kDynOk, kRmapOk>, grid, kSpmmThreads, smem, s, tm, prm);
+  else if (nch) launch_pdl(k_spmm<NT, GM, TMV, TKV, kDynOk>, grid, kSpmmThreads, smem, s, tm, prm);
+  else if (rmap) launch_pdl(k_spmm<NT, GM, TMV, TKV, false, kRmapOk>, grid, kSpmmThreads, smem, s, tm, prm);
   else launch_pdl(k_spmm<NT, GM, TMV, TKV, false>, grid, kSpmmThreads, smem, s, tm, prm);
   if (cta_t) {  // (blocks the stream: diagnostics only)
     std::vector<long long> host(4 * (size_t)grid);
