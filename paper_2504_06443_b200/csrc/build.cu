@@ -1920,7 +1920,10 @@ constexpr int kH2Threads = HRPB_H2_THREADS;
 #endif
 constexpr int kH2OccWords = 8192;  // one bit per 32-column word: K <= 2^23
 constexpr int kH2OrdCap = 8192;    // occupied words whose masks stay in shared memory
-constexpr int kH2Stage = 8192;     // entries staged in shared memory
+#ifndef HRPB_H2_STAGE
+#define HRPB_H2_STAGE 8192
+#endif
+constexpr int kH2Stage = HRPB_H2_STAGE;  // entries staged in shared memory
 constexpr int kH2PatSlots = 2048;  // brick-pattern window (u64 slots)
 constexpr int64_t kH2Huge = 65536; // panels with more entries are claimed first (the critical path of the kernel)
 constexpr int kE2Slots = 2048;     // brick slots (blocks x TM/16 x TK/4) per k_emit_hub2 work item
@@ -2051,7 +2054,7 @@ __global__ void __launch_bounds__(kH2Threads, HRPB_H2_MINB) k_count_hub2(const i
     if (staged) {
       for (uint32_t i = tid; i < E; i += kH2Threads) {
         const uint32_t c = S.col[i];
-        atomicOr(&S.mask[ordinal(c)], 1u << (c & 31));  // (staged: nocc <= E <= kH2OrdCap)
+        atomicOr(&mask[ordinal(c)], 1u << (c & 31));  // (shared memory unless nocc > kH2OrdCap)
       }
     } else {
       for (uint32_t i0 = 0; i0 < E; i0 += kH2Threads * kH2U) {
