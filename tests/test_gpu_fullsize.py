@@ -101,6 +101,16 @@ def test_config3_rmat_exact_mode():  # exact mode on the power-law structure (ro
     run_case("c3", 64, 16, mode=synth.EXACT, rows_sample=256, panels_sample=8, full_check=False)
 
 
+def test_config3_rmat_static_s1(monkeypatch):  # the headline size through the static S1 kernel too
+    monkeypatch.setenv("HRPB_STATIC_S1", "1")
+    run_case("c3", 64, 16, mode=synth.EXACT, rows_sample=256, panels_sample=8, full_check=False)
+
+
+def test_config4_uniform_dynamic_s1(monkeypatch):  # dynamic S1 forced below its size threshold, full size
+    monkeypatch.setenv("HRPB_DYN_S1", "1")
+    run_case("c4", 512, 16, rows_sample=256, panels_sample=8, full_check=False)
+
+
 def test_config4_uniform_full():  # configs[3]: 2M^2, 8 nnz/row, N = 512
     run_case("c4", 512, 16, rows_sample=256, panels_sample=24)
 
