@@ -85,6 +85,10 @@ hrpb_status_t spmm_core(const hrpb_handle* h, const float* B, int64_t ldb, float
     return e == cudaSuccess ? HRPB_SUCCESS : cuda_status(e);
   }
   if (!tile_supported(h->tm, h->tk)) return HRPB_ERROR_NOT_SUPPORTED;
+  if (const char* pm = getenv("HRPB_L2_PERSIST_MB")) {  // experiment: L2 set-aside for evict_last lines
+    static std::once_flag once;
+    std::call_once(once, [pm] { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(pm) << 20); });
+  }
   EncodeTiledFn enc = get_encode();
   if (!enc) return HRPB_ERROR_NOT_SUPPORTED;
   // per-call scratch, stream-ordered on s (a handle may serve concurrent calls on different streams): the padded
