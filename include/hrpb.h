@@ -92,11 +92,13 @@ hrpb_status_t hrpb_build(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
  *   M, K must equal the handle's (else DIMENSION_MISMATCH); N >= 0 (N = 0 is a no-op).
  * Arithmetic: TF32 tensor cores (A rounded to nearest TF32, ties away — cvt.rna semantics, done with integer ops;
  * B truncated by the tensor core), FP32 accumulation in TMEM. A must be finite too (a NaN payload may round to Inf).
- * Work split (S1): one persistent CTA per SM takes a contiguous range of equal cost (1 per block + 3 per panel
- * epilogue, DESIGN.md NEXT-2); a panel larger than
- * a whole CTA's share is split between CTAs, which write partial tiles to a per-call workspace, and a fix-up
- * kernel adds them in CTA order: results are deterministic for a given (handle, N), but the bits of a split
- * panel's rows may differ between launch configurations (e.g. the chunked launches of hrpb_build_spmm_host).
+ * Work split (S1): one persistent CTA per SM takes a contiguous range of equal cost (1 per block + w per panel
+ * epilogue, w = 5 / 5 / 12 / 24 at TM = 16 / 32 / 64 / 128, DESIGN.md NEXT-2); on long launches (nnz >= 64M,
+ * TM <= 32) the work is cut into 16 guided shares per SM that the CTAs claim dynamically. A panel larger than two
+ * shares is split between them: partial tiles go to a per-call workspace and a fix-up kernel adds them in share
+ * order. Within a panel the blocks alternate between two TMEM accumulator sets that the epilogue adds. Results are
+ * deterministic for a given (handle, N) and launch configuration, but the bits of a split panel's rows may differ
+ * between configurations (e.g. the chunked launches of hrpb_build_spmm_host).
  * Scratch (the split-panel workspace, a padded copy of B when its rows are not 16-B aligned) is allocated per
  * call, stream-ordered (so concurrent calls on different streams never share it). Asynchronous on `stream`; no
  * host synchronization. A call on a stream other than the build stream is recorded on the handle so that
