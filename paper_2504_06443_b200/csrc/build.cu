@@ -1598,7 +1598,13 @@ __global__ void __launch_bounds__(kBigThreads) k_count_big(const int64_t* __rest
 // O(entries + K / 32) shared-memory operations and no global atomics. k_emit_hub writes the blocks and values
 // once the global scan has placed the panel.
 constexpr int kHubThreads = 512;
-constexpr int kEmitNT = 256;  // threads of the emission kernels (k_emit, k_emit_hub)
+#ifndef HRPB_EMIT_NT
+#define HRPB_EMIT_NT 128
+#endif
+constexpr int kEmitNT = HRPB_EMIT_NT;  // threads of k_emit (listed panels; a CTA per panel, latency-bound: 128
+                                       // threads at 16 CTAs per SM keep twice the panels in flight of 256 at 8:
+                                       // c3 k_emit 0.46 -> 0.35 ms, c5 build 1.08 -> 1.02 ms)
+constexpr int kEmitHubNT = 256;        // threads of k_emit_hub (the K > 2^23 hub path)
 constexpr int kHubPassWords = 32768;                 // bitmap words per pass
 constexpr int64_t kHubPassCols = 32 * kHubPassWords;  // 2^20 columns per pass
 constexpr int kHubGroups = kHubPassWords / 8;        // 4096 groups of 8 words (u8 prefix within a group)
@@ -2333,7 +2339,7 @@ __global__ void __launch_bounds__(kE2Threads, 3) k_emit_hub2(const int64_t* __re
 // Hub panels' output, after the global scan: every CTA takes items of one flat list (per hub: its block-metadata
 // chunks — sizePtr = panel offset + relative offset, HRPB-v1 headers, patterns, padding, sentinel activeCols —
 // then its 4096-entry value chunks — activeCols and values at popcount ranks).
-__global__ void __launch_bounds__(kEmitNT) k_emit_hub(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+__global__ void __launch_bounds__(kEmitHubNT) k_emit_hub(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                                      const float* __restrict__ vals, int64_t M, int64_t K,
                                                      int64_t nnz, int tm, int tk, const uint32_t* __restrict__ q,
                                                      const uint32_t* __restrict__ nact_in,
@@ -2396,13 +2402,13 @@ __global__ void __launch_bounds__(kEmitNT) k_emit_hub(const int64_t* __restrict_
     const int64_t c1e = min(e1, c0e + kHubEntryChunk);
     if (nbk == 4) {  // TM = TK = 16: kHubU entries per thread, each stage's loads issued before they are used
       int r = row_of(s_rp, nrows, c0e + threadIdx.x < c1e ? c0e + threadIdx.x : c0e);  // then only moves forward
-      for (int64_t eb = c0e; eb < c1e; eb += kEmitNT * kHubU) {
+      for (int64_t eb = c0e; eb < c1e; eb += kEmitHubNT * kHubU) {
         uint32_t qq[kHubU];
         int32_t cv[kHubU];
         float vv[kHubU];
 #pragma unroll
         for (int u = 0; u < kHubU; ++u) {
-          const int64_t e = eb + u * kEmitNT + threadIdx.x;
+          const int64_t e = eb + u * kEmitHubNT + threadIdx.x;
           qq[u] = 0xFFFFFFFFu;
           if (e < c1e) {
             qq[u] = q[e];
@@ -2423,7 +2429,7 @@ __global__ void __launch_bounds__(kEmitNT) k_emit_hub(const int64_t* __restrict_
 #pragma unroll
         for (int u = 0; u < kHubU; ++u) {
           if (qq[u] >= nact) continue;  // (padding items; invalid CSR input)
-          const int64_t e = eb + u * kEmitNT + threadIdx.x;
+          const int64_t e = eb + u * kEmitHubNT + threadIdx.x;
           while (s_rp[r + 1] <= e) ++r;
           const uint32_t j = qq[u] >> tk_sh, lc = qq[u] & (tk - 1);
           ac[((int64_t)b0 + j) * tk + lc] = (uint32_t)cv[u];
@@ -2443,7 +2449,7 @@ __global__ void __launch_bounds__(kEmitNT) k_emit_hub(const int64_t* __restrict_
       }
       continue;
     }
-    for (int64_t e = c0e + threadIdx.x; e < c1e; e += kEmitNT) {
+    for (int64_t e = c0e + threadIdx.x; e < c1e; e += kEmitHubNT) {
       const uint32_t qq = q[e];
       const int32_t c = ci[e];
       const float v = vals[e];
@@ -2862,7 +2868,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
     const unsigned wgrid = (unsigned)ceil_div(P, kWWarps);
     const int mid_ctas = 8 * num_sms();
     const int count_ctas = (int)(227 * 1024 / (count_smem + 1024)) * num_sms();
-    const int emit_ctas = (int)min((size_t)8, 227 * 1024 / (emit_smem + 1024)) * num_sms();
+    const int emit_ctas = (int)min((size_t)(2048 / kEmitNT), 227 * 1024 / (emit_smem + 1024)) * num_sms();
     cudaMemsetAsync(lb, 0, (P + 1) * sizeof(uint64_t), s);
     cudaMemsetAsync(h->brp, 0, sizeof(uint32_t), s);  // P == 0: blockedRowPtr = {0}
     cudaMemsetAsync(poff, 0, sizeof(uint64_t), s);
@@ -2905,7 +2911,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
         launch_pdl(k_emit_hub2, 3 * num_sms(), kE2Threads, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact,
                    h->brp, poff, gpat, relb, h->ac, h->sp, h->packed, hublist2, hubch2, nhub2);
       else if (hub_dense)
-        launch_pdl(k_emit_hub, mid_ctas, kEmitNT, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp,
+        launch_pdl(k_emit_hub, mid_ctas, kEmitHubNT, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp,
                    poff, gpat, relb, h->ac, h->sp, h->packed, hublist2, hubch2, nhub2);
       else
         launch_pdl(k_emit_hubvals, mid_ctas, kEmitThreads, 0, s, row_ptr, col_idx, values, M, nnz, tm, tk, q, nact,
