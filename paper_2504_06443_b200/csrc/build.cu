@@ -1932,7 +1932,12 @@ constexpr int kH2OrdCap = 8192;    // occupied words whose masks stay in shared 
 constexpr int kH2Stage = HRPB_H2_STAGE;  // entries staged in shared memory
 constexpr int kH2PatSlots = 2048;  // brick-pattern window (u64 slots)
 constexpr int64_t kH2Huge = 65536; // panels with more entries are claimed first (the critical path of the kernel)
-constexpr int kE2Slots = 2048;     // brick slots (blocks x TM/16 x TK/4) per k_emit_hub2 work item
+#ifndef HRPB_E2_THREADS
+#define HRPB_E2_THREADS 512
+#endif
+constexpr int kE2Threads = HRPB_E2_THREADS;  // k_emit_hub2 threads (one per block of a work item at nbk = 4)
+constexpr int kE2Slots = 4 * kE2Threads;     // brick slots (blocks x TM/16 x TK/4) per k_emit_hub2 work item
+constexpr int kE2MinB = 1536 / kE2Threads;   // k_emit_hub2 CTAs per SM
 #ifndef HRPB_H2_U
 #define HRPB_H2_U 4
 #endif
@@ -2190,9 +2195,8 @@ __global__ void __launch_bounds__(kH2Threads, HRPB_H2_MINB) k_count_hub2(const i
 // HRPB-v1 headers, patterns and padding, then finds in every row the entries whose ranks fall in its blocks (one
 // contiguous range per row: ranks ascend along a row, R23) and writes their activeCols and values at popcount
 // ranks — the stores of an item land in one contiguous output region.
-constexpr int kE2Threads = 512;
 constexpr int kE2U = 4;  // entries per thread in flight
-__global__ void __launch_bounds__(kE2Threads, 3) k_emit_hub2(const int64_t* __restrict__ rp,
+__global__ void __launch_bounds__(kE2Threads, kE2MinB) k_emit_hub2(const int64_t* __restrict__ rp,
                                                          const int32_t* __restrict__ ci,
                                                          const float* __restrict__ vals, int64_t M, int64_t K,
                                                          int64_t nnz, int tm, int tk, const uint32_t* __restrict__ q,
@@ -2908,7 +2912,7 @@ hrpb_status_t build_impl(int64_t M, int64_t K, int64_t nnz, const int64_t* row_p
       launch_pdl(k_emit, emit_ctas, kEmitNT, emit_smem, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp,
                  poff, gpat, h->ac, h->sp, h->packed, l1, nl1, hublist, hubch, nhub, ctr + 5, (int)hub_dense);
       if (hub_2l)
-        launch_pdl(k_emit_hub2, 3 * num_sms(), kE2Threads, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact,
+        launch_pdl(k_emit_hub2, kE2MinB * num_sms(), kE2Threads, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact,
                    h->brp, poff, gpat, relb, h->ac, h->sp, h->packed, hublist2, hubch2, nhub2);
       else if (hub_dense)
         launch_pdl(k_emit_hub, mid_ctas, kEmitHubNT, 0, s, row_ptr, col_idx, values, M, K, nnz, tm, tk, q, nact, h->brp,
