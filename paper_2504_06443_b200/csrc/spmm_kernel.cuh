@@ -44,6 +44,9 @@ constexpr int kMaxStages = 24;
 // (2 / 4 / 8: c4 5.68 -> 8.3 / 10.0 / 10.0 ms, c2a TM = 64 0.247 -> 0.338 ms, c3 19.1 -> 19.4 ms): the prefetches
 // queue in the same bulk-copy path as the A blocks
 constexpr int kL2Pf = HRPB_L2PF;
+#ifndef HRPB_AC_EF
+#define HRPB_AC_EF 0
+#endif
 #ifndef HRPB_EPI_SLEEP
 #define HRPB_EPI_SLEEP 0
 #endif
@@ -519,12 +522,21 @@ __global__ void __launch_bounds__(kSpmmThreads, 1) k_spmm(const __grid_constant_
     auto fetch = [&](int64_t bl, int q) {  // stage block bl's look-ahead data into ring slot q (all lanes call)
       uint32_t* slot = myring + q * kSlotW;
       if (bl < b_end) {
+#if HRPB_AC_EF  // experiment: activeCols / sizePtr (streamed once) with the L2 evict-first policy
+        if (lane < TKV)
+          asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(smem_u32(slot + 4 + lane)),
+                       "l"(acp + bl * TKV + lane), "l"(pol_a) : "memory");
+        if (lane < 2)
+          asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(smem_u32(slot + 2 * lane)),
+                       "l"(spp + bl + lane), "l"(pol_a) : "memory");
+#else
         if (lane < TKV)
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot + 4 + lane)),
                        "l"(acp + bl * TKV + lane) : "memory");
         if (lane < 2)
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(slot + 2 * lane)),
                        "l"(spp + bl + lane) : "memory");
+#endif
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
